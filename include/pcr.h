@@ -1,0 +1,213 @@
+/*
+ * pcr.h — C-ABI of libpcr.so, the B200-native reuse-prefill hot path of PCR
+ * (arXiv 2603.23049, "prefetch-enhanced KV-cache reuse for RAG serving").
+ *
+ * Cites: P:<n> = /root/reference/PAPER.md line n; S:<n> = SPEC.md line n.
+ *
+ * The problem statement the calls follow (Alg. 1): the executor
+ * "interacts with the Cache Engine to identify reusable prefixes" (pcr_match_prefix),
+ * loads the matched KV from CPU memory layer by layer (pcr_load_layer_kv), computes
+ * the remaining tokens (pcr_prefill_attn_layer), overlapping load(l+1) with compute(l)
+ * on separate CUDA streams (pcr_run_prefill), and commits or drops
+ * the new chunks at the end of the step (pcr_release).
+ *
+ * Conventions
+ *  - C99; no C++/CUDA/torch types cross the ABI. Streams are cudaStream_t passed as void*.
+ *  - Every call returns pcr_status; the message of the last failure is pcr_last_error().
+ *    No exception or abort crosses the ABI.
+ *  - Host-control calls (pcr_submit, pcr_match_prefix, pcr_release) make NO CUDA calls
+ *    and give the strong guarantee: on error nothing changed.
+ *  - Device calls only ENQUEUE work on the given streams and never synchronise (except
+ *    pcr_run_prefill with a non-NULL layer_times_ms, see there). Launch errors return
+ *    PCR_E_CUDA; asynchronous faults surface at the caller's stream synchronisation.
+ *  - A ctx is not thread-safe: one owner thread.
+ *  - Ownership: the library owns the pinned host store, the prefix tree and the per-
+ *    request plan (including its device-side page/slot tables). The caller owns the
+ *    HBM pool, all Q/K/V/out buffers and the streams; the library borrows raw pointers.
+ *  - Lifecycle per request: pcr_submit -> (may appear in other requests' pending ids)
+ *    -> pcr_match_prefix -> device calls -> [caller synchronises] -> pcr_release.
+ *    Calls out of order return PCR_E_STATE; unknown ids PCR_E_NOREQ.
+ *    pcr_release frees the request's pool pages and table region for reuse, so the
+ *    caller must make sure the request's device work has completed before releasing.
+ *
+ * Data layouts (all bf16, row-major, innermost last; "loc" = this rank's slice):
+ *   store slot (one chunk, all layers)  [L][Hkv_loc][2][C][d]       2 = {K, V}
+ *   HBM pool                            [L][n_pages][Hkv_loc][2][S_pg][d]
+ *     token t of a request lives in pool page pages[t / S_pg], row t % S_pg.
+ *   q    (one layer)                    [N2][Hq_loc][d]
+ *   k_new, v_new (one layer)            [N2][Hkv_loc][d]   (post-RoPE)
+ *   out  (one layer)                    [N2][Hq_loc][d]
+ *   *_all (pcr_run_prefill)             [L][...] of the per-layer layouts above
+ * Query head h (local index) uses KV head h / G, G = Hq / Hkv (GQA, HF repeat_kv).
+ * Rank r of `world` owns KV heads [r*Hkv/world, (r+1)*Hkv/world) and the matching Q heads.
+ */
+#ifndef PCR_H_
+#define PCR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCR_ABI_VERSION 1
+
+typedef struct pcr_ctx pcr_ctx;
+
+typedef enum pcr_status {
+  PCR_OK = 0,
+  PCR_E_INVAL = -1,      /* bad argument (null pointer, out-of-range id/layer, short capacity) */
+  PCR_E_NOMEM = -2,      /* pool pages, plan regions or host memory exhausted */
+  PCR_E_CUDA = -3,       /* a CUDA runtime call or kernel launch failed */
+  PCR_E_STATE = -4,      /* call out of lifecycle order, or device call on a host-only ctx */
+  PCR_E_NOREQ = -5,      /* unknown request id */
+  PCR_E_INTERNAL = -6,   /* invariant violated (S:145 InconsistentDrop); a bug */
+  PCR_E_UNSUPPORTED = -7 /* shape the kernels do not implement (see pcr_create) */
+} pcr_status;
+
+/* Model geometry and cache configuration.  Every rank passes the same struct except
+ * `rank`, `device` and `pool`; host decisions are deterministic, so every rank computes
+ * identical slots, pages and evictions without any control traffic. */
+typedef struct pcr_config {
+  int32_t n_layers;      /* L */
+  int32_t n_q_heads;     /* Hq (full model); Hq % Hkv == 0 */
+  int32_t n_kv_heads;    /* Hkv (full model); world divides Hkv */
+  int32_t head_dim;      /* d; the device path implements d in {64, 128} */
+  int32_t rank, world;   /* KV-head sharding */
+  int32_t chunk_tokens;  /* C: tree/store granularity (paper 256) */
+  int32_t page_tokens;   /* S_pg: pool page tokens (paper's vLLM block 16);
+                            S_pg in {16, 32, 64, 128} and S_pg divides C */
+  int64_t store_chunks;  /* DRAM store capacity in chunks (reading R13: capacity unit) */
+  int32_t window;        /* look-ahead window W (paper 4; best 6) */
+  int32_t device;        /* CUDA ordinal; -1 = host-control only (no CUDA calls at all;
+                            the store is ordinary memory; device calls return PCR_E_STATE) */
+  void* pool;            /* caller-owned HBM pool (device pointer, 256-byte aligned) */
+  int64_t pool_bytes;    /* n_pages = pool_bytes / (L*Hkv_loc*2*S_pg*d*2) */
+  int32_t max_inflight;  /* requests planned but not yet released; 0 -> 4 */
+  int32_t max_tokens;    /* max tokens of one request; 0 -> pool capacity in tokens */
+  int32_t gather_ctas;   /* CTAs of the host->HBM gather kernel; 0 -> library default */
+  int32_t reserved0;
+} pcr_config;
+
+/* Create a context.  Allocates the pinned store (mmap + NUMA-local mbind to the GPU's
+ * node + cudaHostRegister, mapped), the device plan arena, events and TMA descriptors
+ * over `pool`.  PCR_E_INVAL: inconsistent geometry; PCR_E_UNSUPPORTED: head_dim or
+ * page_tokens outside what the kernels implement; PCR_E_NOMEM / PCR_E_CUDA: allocation. */
+pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out);
+void pcr_destroy(pcr_ctx* ctx);                 /* NULL is a no-op */
+const char* pcr_last_error(const pcr_ctx* ctx); /* never NULL; "" if no error */
+int32_t pcr_abi_version(void);
+
+/* Derived geometry: pool pages, bytes of one store slot, bytes of one pool page (all layers). */
+int64_t pcr_pool_pages(const pcr_ctx* ctx);
+int64_t pcr_slot_bytes(const pcr_ctx* ctx);
+
+/* ---------------------------------------------------------------- host control ------ */
+
+/* Register a request (it may now appear in pending windows).  tokens[n_tokens] are copied;
+ * chunks are hashed once here (Alg.1 Chunkify/HashPrefix):
+ *   key_i = BLAKE2b-128(key_{i-1} || tokens_i as little-endian uint32), key_{-1} = 0^16,
+ * for the min(n_cacheable / C, (n_tokens-1) / C) cacheable chunks (reading R5: at least
+ * one token is always recomputed).  PCR_E_INVAL: n_tokens < 1 or n_cacheable outside
+ * [0, n_tokens] or null tokens; PCR_E_STATE: id already registered. */
+pcr_status pcr_submit(pcr_ctx* ctx, int64_t req_id, const uint32_t* tokens, int64_t n_tokens,
+                      int64_t n_cacheable);
+
+/* The movement plan of one request (Alg.1: cpu_to_gpu = the n_matched chunks,
+ * gpu_to_cpu = the n_reserved new chunks; AdjustTokens = n1/n2).  Caller-owned arrays
+ * with capacities; if a capacity is short the call fails with PCR_E_INVAL and nothing
+ * changes.  Arrays may be NULL when their capacity is 0 and no entries are produced. */
+typedef struct pcr_plan {
+  int32_t n_matched;     /* chunks reused from the DRAM store (pinned until release) */
+  int32_t n_reserved;    /* new chunks given a store slot (PENDING until release/commit) */
+  int64_t n1_tokens;     /* n_matched * C */
+  int64_t n2_tokens;     /* n_tokens - n1_tokens (>= 1) */
+  int32_t* slots;        /* [n_matched + n_reserved] store slots in chain order */
+  int32_t cap_slots;
+  int32_t* pages;        /* [ceil(n_tokens / S_pg)] pool pages, logical order */
+  int32_t cap_pages;
+  int32_t n_pages;
+  int32_t n_evicted;
+  uint8_t* evicted_keys; /* [n_evicted][16] keys evicted to make room, in eviction order */
+  int32_t* evicted_slots;/* [n_evicted] their freed slots */
+  int32_t cap_evicted;
+  int32_t reserved0;
+} pcr_plan;
+
+/* Plan one request (§4.2; Alg.1), in this order:
+ *  1. look-ahead bump: for each id in Reverse(pending_ids[0 : min(n_pending, window)]),
+ *     walk its chunk chain root-first, touching (moving to MRU) every RESIDENT chunk
+ *     that is a leaf; stop at the first chunk that is not RESIDENT;
+ *  2. match: walk this request's chain while the chunk is RESIDENT (key, parent and
+ *     tokens equal); touch and pin each matched chunk ("until a mismatch occurs");
+ *  3. reserve: for each remaining cacheable chunk: the lowest free slot, else evict the
+ *     first unpinned RESIDENT leaf in LRU order (its parent becomes a leaf at MRU when
+ *     this was its last child); insert a PENDING pinned node at MRU (its parent
+ *     leaves the leaf list).  Stop at the first chunk that cannot get a slot (all leaves
+ *     pinned: SPEC's EvictionStarved is not an error) or whose key exists;
+ *  4. pool pages: ceil(n_tokens / S_pg), lowest free first.
+ * Ids beyond the window are ignored.  PCR_E_NOREQ: unknown req_id or pending id;
+ * PCR_E_STATE: already planned; PCR_E_INVAL: pending ids contain req_id or duplicates,
+ * or a short capacity (slots and evicted need >= the request's cacheable chunk count, pages
+ * >= ceil(n_tokens / S_pg)); PCR_E_NOMEM: not enough free pages or plan regions, or the
+ * request is longer than pcr_config.max_tokens. */
+pcr_status pcr_match_prefix(pcr_ctx* ctx, int64_t req_id, const int64_t* pending_ids,
+                            int32_t n_pending, pcr_plan* out);
+
+/* End of the step (Alg.1).  commit != 0: reserved chunks become RESIDENT
+ * (their slot data must have been written: by offload, or by pcr_store_write);
+ * commit == 0: reserved chunks are dropped deepest-first.  All pins are released and the
+ * pool pages returned.  The request id is then forgotten. */
+pcr_status pcr_release(pcr_ctx* ctx, int64_t req_id, int32_t commit);
+
+/* Copy one chunk record ([L][Hkv_loc][2][C][d] bf16, pcr_slot_bytes bytes) into / out of
+ * the pinned DRAM store.  Host memcpy; PCR_E_INVAL on a bad slot or null pointer. */
+pcr_status pcr_store_write(pcr_ctx* ctx, int32_t slot, const void* src);
+pcr_status pcr_store_read(const pcr_ctx* ctx, int32_t slot, void* dst);
+
+/* Inspection for tests: the leaf list in LRU->MRU order as 16-byte keys. */
+pcr_status pcr_leaf_list(const pcr_ctx* ctx, uint8_t* keys, int32_t cap, int32_t* n_out);
+/* RFC 7693 BLAKE2b (unkeyed when keylen == 0), digest_len in [1, 64]; used by tests to pin
+ * the library's hash against the RFC vectors. */
+pcr_status pcr_blake2b(const void* data, int64_t n, const void* key, int32_t keylen,
+                       int32_t digest_len, uint8_t* out);
+
+/* ---------------------------------------------------------------- device path ------- */
+
+/* a2 — enqueue on load_stream the copy of layer `layer` of every matched chunk from the
+ * pinned host store into the request's pool pages:
+ *   pool[layer][pages[t/S_pg]][h][kv][t%S_pg][:] = store[slots[t/C]][layer][h][kv][t%C][:]
+ * for t < n1.  An sm_100a kernel reads the mapped host memory over PCIe with 16-byte
+ * loads and writes 16-byte stores into the pool pages (no copy engine).  The first
+ * device call of a request also uploads its page/slot tables on its stream. */
+pcr_status pcr_load_layer_kv(pcr_ctx* ctx, int64_t req_id, int32_t layer, void* load_stream);
+
+/* a3 + a4 — enqueue on compute_stream: append k_new/v_new ([N2][Hkv_loc][d]) at tokens
+ * n1..n1+N2-1 of the pool, then suffix-query causal attention:
+ *   out[i][h] = softmax_j( q[i][h] . K[j][h/G] / sqrt(d) ) V[j][h/G],  j <= n1 + i,
+ * bf16 inputs, fp32 accumulation (tcgen05/TMEM), bf16 output.  The caller orders this
+ * after pcr_load_layer_kv(layer) (pcr_run_prefill does so with events). */
+pcr_status pcr_prefill_attn_layer(pcr_ctx* ctx, int64_t req_id, int32_t layer, const void* q,
+                                  const void* k_new, const void* v_new, void* out,
+                                  void* compute_stream);
+
+/* a5 — the whole layer pipeline for one planned request (Alg.1):
+ *   mode 0 OVERLAP: load_stream: gather(l) -> record ev_load[l];
+ *                   compute_stream: wait ev_load[l] -> append(l) -> attn(l)
+ *                   so gather(l+1) overlaps attn(l);
+ *   mode 1 SYNC:    everything in order on compute_stream (load(l), append(l), attn(l)).
+ * compute_stream is the stream the caller synchronises on (load_stream is joined into it
+ * at the end).  layer_times_ms (nullable) = [2L] floats: per-layer gather and
+ * append+attention durations from CUDA events; when non-NULL the call blocks until the
+ * request's device work has completed. */
+pcr_status pcr_run_prefill(pcr_ctx* ctx, int64_t req_id, const void* q_all, const void* k_all,
+                           const void* v_all, void* out_all, void* compute_stream,
+                           void* load_stream, int32_t mode, float* layer_times_ms);
+
+/* Count of kernels launched by this ctx since creation (bench `gpu_launches`). */
+int64_t pcr_kernel_launches(const pcr_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCR_H_ */

@@ -1,0 +1,7 @@
+"""B200-native reuse-prefill hot path of PCR (arXiv 2603.23049).
+
+The product is libpcr.so (include/pcr.h): C++ host control (prefix tree + look-ahead LRU)
+and hand-written sm_100a kernels (16-byte host->HBM gather, suffix append, tcgen05/TMEM/TMA
+suffix attention), driven per layer on two CUDA streams.  `pcr` is the ctypes binding.
+"""
+from .pcr import MODE_OVERLAP, MODE_SYNC, Context, PcrError, blake2b, load_library  # noqa: F401

@@ -1,0 +1,104 @@
+// Host control of the hot path: chunk keys, the prefix tree with a
+// look-ahead leaf-LRU list, store-slot and pool-page allocation.  No CUDA here.
+//
+// Paper: §4.2 P:362-364 (prefix tree, leaf-only LRU eviction, look-ahead priority bump),
+// §5 P:480 (window of waiting requests "update the recency for matched chunks"),
+// Alg.1 P:487-507 (bump over Reverse(prefetch_reqs), then plan cpu_to_gpu/gpu_to_cpu,
+// AdjustTokens), P:518 (computation only on confirmed-present chunks).
+// Policy readings R1-R3, R5, R7-R12 are listed in DESIGN.md.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+namespace pcr {
+
+using Key = std::array<uint8_t, 16>;
+
+struct KeyHash {
+  size_t operator()(const Key& k) const noexcept {
+    uint64_t a;
+    __builtin_memcpy(&a, k.data(), 8);
+    return static_cast<size_t>(a);
+  }
+};
+
+enum : int32_t { kPending = 0, kResident = 1 };
+
+// Status codes mirror pcr_status (include/pcr.h).
+enum : int32_t { kOk = 0, kInval = -1, kNoMem = -2, kState = -4, kNoReq = -5, kInternal = -6 };
+
+struct Node {
+  Key key;
+  int32_t parent = -1;     // node index, -1 = root
+  int32_t slot = -1;
+  int32_t state = kPending;
+  int32_t pins = 0;
+  int32_t n_children = 0;
+  int32_t prev = -1, next = -1;  // intrusive leaf-list links
+  bool in_list = false;
+  bool live = false;
+  std::vector<uint32_t> tokens;
+};
+
+struct Plan {
+  int32_t n_matched = 0, n_reserved = 0;
+  int64_t n1 = 0, n2 = 0;
+  std::vector<int32_t> slots, pages;
+  std::vector<std::pair<Key, int32_t>> evicted;
+  int32_t region = -1;     // device plan-table region
+};
+
+struct Request {
+  std::vector<uint32_t> tokens;
+  std::vector<Key> keys;   // cacheable chunk chain
+  bool planned = false;
+  std::vector<int32_t> matched, reserved;  // node indices
+  Plan plan;
+  bool tables_uploaded = false;
+};
+
+class Planner {
+ public:
+  Planner(int32_t chunk_tokens, int32_t page_tokens, int64_t store_chunks, int64_t n_pages,
+          int32_t window, int32_t max_regions);
+
+  int32_t submit(int64_t id, const uint32_t* tokens, int64_t n, int64_t n_cacheable, std::string* err);
+  // Validates first (strong guarantee); `cap_*` are the caller's capacities (-1 = unchecked).
+  int32_t match_prefix(int64_t id, const int64_t* pending, int32_t n_pending, int64_t cap_slots,
+                       int64_t cap_pages, int64_t cap_evicted, std::string* err);
+  int32_t release(int64_t id, bool commit, std::string* err);
+
+  Request* find(int64_t id) {
+    auto it = reqs_.find(id);
+    return it == reqs_.end() ? nullptr : &it->second;
+  }
+  std::vector<Key> leaf_list() const;
+  int32_t chunk_tokens() const { return C_; }
+  int32_t page_tokens() const { return S_; }
+
+  static Key chunk_key(const Key& parent, const uint32_t* tokens, int32_t n);
+
+ private:
+  int32_t C_, S_, window_;
+  int64_t n_slots_, n_pages_;
+  std::vector<Node> nodes_;
+  std::vector<int32_t> free_nodes_;
+  std::unordered_map<Key, int32_t, KeyHash> index_;
+  int32_t head_ = -1, tail_ = -1;          // leaf list: head = LRU, tail = MRU
+  std::set<int32_t> free_slots_, free_pages_, free_regions_;
+  std::unordered_map<int64_t, Request> reqs_;
+
+  void list_append(int32_t n);
+  void list_remove(int32_t n);
+  void touch(int32_t n);
+  int32_t valid_child(const Key& key, int32_t parent, const uint32_t* toks) const;
+  int32_t new_node();
+  void remove_node(int32_t n);  // unlink from parent/list/index; parent may become a leaf
+};
+
+}  // namespace pcr

@@ -1,0 +1,47 @@
+// Launch interface of the hot-path kernels (internal; the public boundary is include/pcr.h).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace pcr {
+
+// Geometry shared by the copy kernels.  All sizes are in elements (bf16) unless noted.
+struct KvGeom {
+  int32_t L, Hkv, d, C, S;          // layers, local kv heads, head dim, chunk tokens, page tokens
+  int64_t n_pool_pages;             // pages in the pool
+  int64_t slot_elems;               // elements of one store slot = L*Hkv*2*C*d
+};
+
+// a2: pool[layer][pages[t/S]][h][kv][t%S] = store[slots[t/C]][layer][h][kv][t%C], t < n_matched*C.
+// `store` is the device (UVA) view of the mapped pinned host store; 16-byte loads/stores.
+cudaError_t launch_kv_gather(const void* store, void* pool, const int32_t* d_slots, const int32_t* d_pages,
+                             int32_t n_matched, int32_t layer, const KvGeom& g, int32_t target_ctas,
+                             cudaStream_t stream);
+
+// a3: suffix token i -> pool token n1+i for K and V; zero-fills rows [n1+n2, n_pages*S) of the
+// request's last page so the attention never reads uninitialised (possibly NaN) bits.
+cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool, const int32_t* d_pages,
+                             int64_t n1, int64_t n2, int32_t n_req_pages, int32_t layer, const KvGeom& g,
+                             cudaStream_t stream);
+
+struct AttnParams {
+  const uint16_t* q;      // [N2][Hq_loc][d]
+  uint16_t* out;          // [N2][Hq_loc][d]
+  const int32_t* pages;   // [n_req_pages] device page table of the request
+  int32_t n1, n2;
+  int32_t hq, hkv;        // local heads
+  int32_t layer;
+  int32_t S;              // page tokens
+  int32_t n_req_pages;
+  int64_t n_pool_pages;
+  float scale_log2;       // log2(e) / sqrt(d)
+};
+
+// a4: suffix-query causal attention over the request's pool pages (tcgen05 + TMEM + TMA).
+// `tmap_pool` is a 2D tensor map over the pool viewed as [rows][d] (rows = L*pages*Hkv*2*S),
+// box {64, S}, SWIZZLE_128B.
+cudaError_t launch_suffix_attn(const CUtensorMap* tmap_pool, const AttnParams& p, int32_t d,
+                               cudaStream_t stream);
+
+}  // namespace pcr

@@ -1,0 +1,457 @@
+// libpcr.so — the C-ABI of include/pcr.h: context, pinned DRAM store, device plan tables,
+// TMA descriptor over the pool, and the per-layer stream/event pipeline.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../../include/pcr.h"
+#include "../host/blake2b.h"
+#include "../host/planner.h"
+#include "../kernels/kernels.h"
+
+using pcr::Planner;
+using pcr::Request;
+
+struct pcr_ctx {
+  pcr_config cfg{};
+  int32_t hkv = 0, hq = 0, G = 0;
+  int64_t slot_elems = 0, slot_bytes = 0, page_elems_all_layers = 0, n_pool_pages = 0;
+  std::unique_ptr<Planner> planner;
+  bool device = false;
+  // pinned DRAM store (library-owned)
+  void* store = nullptr;
+  size_t store_bytes = 0;
+  bool registered = false;
+  void* store_dev = nullptr;
+  // device plan arena: max_inflight regions of [pages | slots] int32
+  int32_t max_regions = 0;
+  int64_t region_words = 0, region_page_cap = 0;
+  int32_t* h_arena = nullptr;
+  int32_t* d_arena = nullptr;
+  std::vector<cudaEvent_t> region_ev;
+  CUtensorMap tmap{};
+  std::vector<cudaEvent_t> ev_load;
+  cudaEvent_t ev_join = nullptr;
+  std::vector<cudaEvent_t> ev_t;  // timing: 4 per layer
+  std::string err;
+  int64_t launches = 0;
+  pcr::KvGeom geom{};
+  int32_t gather_ctas = 16;
+};
+
+namespace {
+
+pcr_status fail(const pcr_ctx* c, pcr_status s, const std::string& msg) {
+  if (c) const_cast<pcr_ctx*>(c)->err = msg;
+  return s;
+}
+
+pcr_status cuda_fail(const pcr_ctx* c, cudaError_t e, const char* what) {
+  return fail(c, PCR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(ctx, call)                                   \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);  \
+  } while (0)
+
+bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+
+// NUMA node of the GPU from sysfs (-1 if unknown) and MPOL_PREFERRED placement of the store.
+int gpu_numa_node(int dev) {
+  char bus[64] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof(bus), dev) != cudaSuccess) return -1;
+  for (char* p = bus; *p; ++p) *p = static_cast<char>(tolower(*p));
+  std::string path = std::string("/sys/bus/pci/devices/") + bus + "/numa_node";
+  FILE* f = fopen(path.c_str(), "r");
+  if (!f) return -1;
+  int node = -1;
+  if (fscanf(f, "%d", &node) != 1) node = -1;
+  fclose(f);
+  return node;
+}
+
+void bind_to_node(void* p, size_t bytes, int node) {
+  if (node < 0 || node >= 64) return;
+  unsigned long mask = 1UL << node;
+  const int kMpolPreferred = 1;
+  syscall(SYS_mbind, p, bytes, kMpolPreferred, &mask, 64, 0);
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+pcr_status make_pool_tmap(pcr_ctx* c) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CUDA_TRY(c, cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) return fail(c, PCR_E_CUDA, "cuTensorMapEncodeTiled not found");
+  const int64_t rows = int64_t(c->cfg.n_layers) * c->n_pool_pages * c->hkv * 2 * c->cfg.page_tokens;
+  if (rows >= (int64_t(1) << 31)) return fail(c, PCR_E_INVAL, "pool too large for 32-bit TMA row coordinates");
+  cuuint64_t dims[2] = {cuuint64_t(c->cfg.head_dim), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(c->cfg.head_dim) * 2};
+  cuuint32_t box[2] = {64, cuuint32_t(c->cfg.page_tokens)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = reinterpret_cast<EncodeTiledFn>(fn)(
+      &c->tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, c->cfg.pool, dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, PCR_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return PCR_OK;
+}
+
+Request* planned_request(pcr_ctx* c, int64_t id, pcr_status* st) {
+  Request* r = c->planner->find(id);
+  if (!r) { *st = fail(c, PCR_E_NOREQ, "unknown request"); return nullptr; }
+  if (!r->planned) { *st = fail(c, PCR_E_STATE, "request not planned (call pcr_match_prefix first)"); return nullptr; }
+  *st = PCR_OK;
+  return r;
+}
+
+int32_t* d_pages_of(pcr_ctx* c, const Request* r) { return c->d_arena + r->plan.region * c->region_words; }
+int32_t* d_slots_of(pcr_ctx* c, const Request* r) { return d_pages_of(c, r) + c->region_page_cap; }
+
+// First device call of a request uploads its page/slot tables; later calls (on any stream)
+// are ordered after that upload by an event.
+pcr_status ensure_tables(pcr_ctx* c, Request* r, cudaStream_t s) {
+  const int32_t reg = r->plan.region;
+  if (!r->tables_uploaded) {
+    int32_t* h = c->h_arena + reg * c->region_words;
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_arena + reg * c->region_words, h, sizeof(int32_t) * c->region_words,
+                                cudaMemcpyHostToDevice, s));
+    CUDA_TRY(c, cudaEventRecord(c->region_ev[reg], s));
+    r->tables_uploaded = true;
+  } else {
+    CUDA_TRY(c, cudaStreamWaitEvent(s, c->region_ev[reg], 0));
+  }
+  return PCR_OK;
+}
+
+pcr_status device_ready(pcr_ctx* c) {
+  if (!c->device) return fail(c, PCR_E_STATE, "device call on a host-control-only context (device = -1)");
+  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  return PCR_OK;
+}
+
+pcr_status enqueue_gather(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s) {
+  if (r->plan.n_matched == 0) return PCR_OK;
+  CUDA_TRY(c, pcr::launch_kv_gather(c->store_dev, c->cfg.pool, d_slots_of(c, r), d_pages_of(c, r),
+                                    r->plan.n_matched, layer, c->geom, c->gather_ctas, s));
+  c->launches += 1;
+  return PCR_OK;
+}
+
+pcr_status enqueue_attn(pcr_ctx* c, Request* r, int32_t layer, const void* q, const void* k, const void* v,
+                        void* out, cudaStream_t s) {
+  const int64_t n1 = r->plan.n1, n2 = r->plan.n2;
+  const int32_t n_pages = static_cast<int32_t>(r->plan.pages.size());
+  CUDA_TRY(c, pcr::launch_kv_append(k, v, c->cfg.pool, d_pages_of(c, r), n1, n2, n_pages, layer, c->geom, s));
+  pcr::AttnParams p{};
+  p.q = static_cast<const uint16_t*>(q);
+  p.out = static_cast<uint16_t*>(out);
+  p.pages = d_pages_of(c, r);
+  p.n1 = static_cast<int32_t>(n1);
+  p.n2 = static_cast<int32_t>(n2);
+  p.hq = c->hq;
+  p.hkv = c->hkv;
+  p.layer = layer;
+  p.S = c->cfg.page_tokens;
+  p.n_req_pages = n_pages;
+  p.n_pool_pages = c->n_pool_pages;
+  p.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(c->cfg.head_dim));
+  CUDA_TRY(c, pcr::launch_suffix_attn(&c->tmap, p, c->cfg.head_dim, s));
+  c->launches += 2;
+  return PCR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t pcr_abi_version(void) { return PCR_ABI_VERSION; }
+
+const char* pcr_last_error(const pcr_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t pcr_pool_pages(const pcr_ctx* ctx) { return ctx ? ctx->n_pool_pages : -1; }
+int64_t pcr_slot_bytes(const pcr_ctx* ctx) { return ctx ? ctx->slot_bytes : -1; }
+int64_t pcr_kernel_launches(const pcr_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
+  if (!cfg || !out) return PCR_E_INVAL;
+  *out = nullptr;
+  const pcr_config& k = *cfg;
+  if (k.n_layers < 1 || k.n_q_heads < 1 || k.n_kv_heads < 1 || k.n_q_heads % k.n_kv_heads ||
+      k.head_dim < 8 || k.head_dim % 8 || k.world < 1 || k.rank < 0 || k.rank >= k.world ||
+      k.n_kv_heads % k.world || k.chunk_tokens < 1 || k.page_tokens < 1 || k.chunk_tokens % k.page_tokens ||
+      k.store_chunks < 1 || k.window < 0 || k.pool_bytes < 0 || k.max_inflight < 0 || k.max_tokens < 0 ||
+      k.gather_ctas < 0)
+    return PCR_E_INVAL;
+  auto c = std::make_unique<pcr_ctx>();
+  c->cfg = k;
+  c->device = k.device >= 0;
+  c->hkv = k.n_kv_heads / k.world;
+  c->hq = k.n_q_heads / k.world;
+  c->G = c->hq / c->hkv;
+  c->slot_elems = int64_t(k.n_layers) * c->hkv * 2 * k.chunk_tokens * k.head_dim;
+  c->slot_bytes = c->slot_elems * 2;
+  c->page_elems_all_layers = int64_t(k.n_layers) * c->hkv * 2 * k.page_tokens * k.head_dim;
+  c->n_pool_pages = k.pool_bytes / (c->page_elems_all_layers * 2);
+  if (c->device) {
+    if (!(k.head_dim == 64 || k.head_dim == 128) ||
+        !(k.page_tokens == 16 || k.page_tokens == 32 || k.page_tokens == 64 || k.page_tokens == 128) ||
+        !is_pow2(k.chunk_tokens) || 128 % c->G != 0)
+      return PCR_E_UNSUPPORTED;
+    if (!k.pool || c->n_pool_pages < 1 || (reinterpret_cast<uintptr_t>(k.pool) & 255)) return PCR_E_INVAL;
+  }
+  const int64_t max_tokens = k.max_tokens > 0 ? k.max_tokens : std::max<int64_t>(1, c->n_pool_pages * k.page_tokens);
+  c->max_regions = k.max_inflight > 0 ? k.max_inflight : 4;
+  c->region_page_cap = (max_tokens + k.page_tokens - 1) / k.page_tokens;
+  c->region_words = c->region_page_cap + (max_tokens + k.chunk_tokens - 1) / k.chunk_tokens;
+  c->region_words = (c->region_words + 63) / 64 * 64;
+  c->planner = std::make_unique<Planner>(k.chunk_tokens, k.page_tokens, k.store_chunks, c->n_pool_pages, k.window,
+                                         c->max_regions);
+  c->geom = pcr::KvGeom{k.n_layers, c->hkv, k.head_dim, k.chunk_tokens, k.page_tokens, c->n_pool_pages,
+                        c->slot_elems};
+  if (k.gather_ctas > 0) c->gather_ctas = k.gather_ctas;
+
+  // DRAM store: anonymous mapping, NUMA-local to the GPU, pinned + mapped for zero-copy reads.
+  c->store_bytes = static_cast<size_t>(k.store_chunks) * static_cast<size_t>(c->slot_bytes);
+  void* p = mmap(nullptr, c->store_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+  if (p == MAP_FAILED) return PCR_E_NOMEM;
+  c->store = p;
+  madvise(p, c->store_bytes, MADV_HUGEPAGE);
+  c->h_arena = nullptr;
+  if (c->device) {
+    pcr_ctx* cp = c.get();
+    cudaError_t e = cudaSetDevice(k.device);
+    if (e == cudaSuccess) bind_to_node(p, c->store_bytes, gpu_numa_node(k.device));
+    if (e == cudaSuccess) e = cudaHostRegister(p, c->store_bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e == cudaSuccess) { cp->registered = true; e = cudaHostGetDevicePointer(&cp->store_dev, p, 0); }
+    if (e == cudaSuccess)
+      e = cudaHostAlloc(reinterpret_cast<void**>(&cp->h_arena), sizeof(int32_t) * c->region_words * c->max_regions,
+                        cudaHostAllocDefault);
+    if (e == cudaSuccess)
+      e = cudaMalloc(reinterpret_cast<void**>(&cp->d_arena), sizeof(int32_t) * c->region_words * c->max_regions);
+    for (int i = 0; e == cudaSuccess && i < c->max_regions; ++i) {
+      cudaEvent_t ev;
+      e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e == cudaSuccess) cp->region_ev.push_back(ev);
+    }
+    for (int l = 0; e == cudaSuccess && l < k.n_layers; ++l) {
+      cudaEvent_t ev;
+      e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e == cudaSuccess) cp->ev_load.push_back(ev);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cp->ev_join, cudaEventDisableTiming);
+    for (int l = 0; e == cudaSuccess && l < 4 * k.n_layers; ++l) {
+      cudaEvent_t ev;
+      e = cudaEventCreate(&ev);
+      if (e == cudaSuccess) cp->ev_t.push_back(ev);
+    }
+    if (e != cudaSuccess) {
+      std::fprintf(stderr, "pcr_create: %s\n", cudaGetErrorString(e));
+      pcr_destroy(c.release());
+      return PCR_E_CUDA;
+    }
+    if (make_pool_tmap(cp) != PCR_OK) {
+      std::fprintf(stderr, "pcr_create: %s\n", cp->err.c_str());
+      pcr_destroy(c.release());
+      return PCR_E_CUDA;
+    }
+  } else {
+    c->h_arena = static_cast<int32_t*>(std::calloc(c->region_words * c->max_regions, sizeof(int32_t)));
+    if (!c->h_arena) { pcr_destroy(c.release()); return PCR_E_NOMEM; }
+  }
+  *out = c.release();
+  return PCR_OK;
+}
+
+void pcr_destroy(pcr_ctx* c) {
+  if (!c) return;
+  if (c->device) {
+    cudaSetDevice(c->cfg.device);
+    cudaDeviceSynchronize();
+    for (auto e : c->region_ev) cudaEventDestroy(e);
+    for (auto e : c->ev_load) cudaEventDestroy(e);
+    for (auto e : c->ev_t) cudaEventDestroy(e);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->d_arena) cudaFree(c->d_arena);
+    if (c->h_arena) cudaFreeHost(c->h_arena);
+    if (c->registered) cudaHostUnregister(c->store);
+  } else {
+    std::free(c->h_arena);
+  }
+  if (c->store) munmap(c->store, c->store_bytes);
+  delete c;
+}
+
+pcr_status pcr_submit(pcr_ctx* c, int64_t req_id, const uint32_t* tokens, int64_t n_tokens, int64_t n_cacheable) {
+  if (!c) return PCR_E_INVAL;
+  std::string err;
+  int32_t s = c->planner->submit(req_id, tokens, n_tokens, n_cacheable, &err);
+  if (s != 0) return fail(c, static_cast<pcr_status>(s), err);
+  return PCR_OK;
+}
+
+pcr_status pcr_match_prefix(pcr_ctx* c, int64_t req_id, const int64_t* pending, int32_t n_pending, pcr_plan* out) {
+  if (!c || !out) return c ? fail(c, PCR_E_INVAL, "pcr_match_prefix: null plan") : PCR_E_INVAL;
+  Request* r = c->planner->find(req_id);
+  if (r && !r->planned) {
+    const int64_t need_pages = (static_cast<int64_t>(r->tokens.size()) + c->cfg.page_tokens - 1) / c->cfg.page_tokens;
+    if (need_pages > c->region_page_cap)
+      return fail(c, PCR_E_NOMEM, "pcr_match_prefix: request longer than pcr_config.max_tokens");
+  }
+  if ((out->cap_slots > 0 && !out->slots) || (out->cap_pages > 0 && !out->pages) ||
+      (out->cap_evicted > 0 && (!out->evicted_keys || !out->evicted_slots)))
+    return fail(c, PCR_E_INVAL, "pcr_match_prefix: null output array with nonzero capacity");
+  std::string err;
+  int32_t s = c->planner->match_prefix(req_id, pending, n_pending, out->cap_slots, out->cap_pages,
+                                       out->cap_evicted, &err);
+  if (s != 0) return fail(c, static_cast<pcr_status>(s), err);
+  const pcr::Plan& pl = r->plan;
+  out->n_matched = pl.n_matched;
+  out->n_reserved = pl.n_reserved;
+  out->n1_tokens = pl.n1;
+  out->n2_tokens = pl.n2;
+  out->n_pages = static_cast<int32_t>(pl.pages.size());
+  out->n_evicted = static_cast<int32_t>(pl.evicted.size());
+  std::copy(pl.slots.begin(), pl.slots.end(), out->slots);
+  std::copy(pl.pages.begin(), pl.pages.end(), out->pages);
+  for (size_t i = 0; i < pl.evicted.size(); ++i) {
+    std::memcpy(out->evicted_keys + 16 * i, pl.evicted[i].first.data(), 16);
+    out->evicted_slots[i] = pl.evicted[i].second;
+  }
+  // Stage the device tables (host memory only; uploaded by the first device call).
+  int32_t* h = c->h_arena + pl.region * c->region_words;
+  std::copy(pl.pages.begin(), pl.pages.end(), h);
+  std::copy(pl.slots.begin(), pl.slots.begin() + pl.n_matched, h + c->region_page_cap);
+  return PCR_OK;
+}
+
+pcr_status pcr_release(pcr_ctx* c, int64_t req_id, int32_t commit) {
+  if (!c) return PCR_E_INVAL;
+  std::string err;
+  int32_t s = c->planner->release(req_id, commit != 0, &err);
+  if (s != 0) return fail(c, static_cast<pcr_status>(s), err);
+  return PCR_OK;
+}
+
+pcr_status pcr_store_write(pcr_ctx* c, int32_t slot, const void* src) {
+  if (!c || !src) return c ? fail(c, PCR_E_INVAL, "pcr_store_write: null source") : PCR_E_INVAL;
+  if (slot < 0 || slot >= c->cfg.store_chunks) return fail(c, PCR_E_INVAL, "pcr_store_write: slot out of range");
+  std::memcpy(static_cast<uint8_t*>(c->store) + static_cast<size_t>(slot) * c->slot_bytes, src, c->slot_bytes);
+  return PCR_OK;
+}
+
+pcr_status pcr_store_read(const pcr_ctx* c, int32_t slot, void* dst) {
+  if (!c || !dst) return c ? fail(c, PCR_E_INVAL, "pcr_store_read: null destination") : PCR_E_INVAL;
+  if (slot < 0 || slot >= c->cfg.store_chunks) return fail(c, PCR_E_INVAL, "pcr_store_read: slot out of range");
+  std::memcpy(dst, static_cast<const uint8_t*>(c->store) + static_cast<size_t>(slot) * c->slot_bytes, c->slot_bytes);
+  return PCR_OK;
+}
+
+pcr_status pcr_leaf_list(const pcr_ctx* c, uint8_t* keys, int32_t cap, int32_t* n_out) {
+  if (!c || !n_out || (cap > 0 && !keys)) return PCR_E_INVAL;
+  auto leaves = c->planner->leaf_list();
+  *n_out = static_cast<int32_t>(leaves.size());
+  if (static_cast<int64_t>(leaves.size()) > cap) return fail(c, PCR_E_INVAL, "pcr_leaf_list: capacity too small");
+  for (size_t i = 0; i < leaves.size(); ++i) std::memcpy(keys + 16 * i, leaves[i].data(), 16);
+  return PCR_OK;
+}
+
+pcr_status pcr_blake2b(const void* data, int64_t n, const void* key, int32_t keylen, int32_t digest_len,
+                       uint8_t* out) {
+  if ((n > 0 && !data) || !out || n < 0 || keylen < 0 || (keylen > 0 && !key)) return PCR_E_INVAL;
+  return pcr::blake2b(out, static_cast<size_t>(digest_len), key, static_cast<size_t>(keylen), data,
+                      static_cast<size_t>(n))
+             ? PCR_OK
+             : PCR_E_INVAL;
+}
+
+pcr_status pcr_load_layer_kv(pcr_ctx* c, int64_t req_id, int32_t layer, void* load_stream) {
+  if (!c) return PCR_E_INVAL;
+  pcr_status st = device_ready(c);
+  if (st != PCR_OK) return st;
+  Request* r = planned_request(c, req_id, &st);
+  if (!r) return st;
+  if (layer < 0 || layer >= c->cfg.n_layers) return fail(c, PCR_E_INVAL, "layer out of range");
+  cudaStream_t s = static_cast<cudaStream_t>(load_stream);
+  if ((st = ensure_tables(c, r, s)) != PCR_OK) return st;
+  return enqueue_gather(c, r, layer, s);
+}
+
+pcr_status pcr_prefill_attn_layer(pcr_ctx* c, int64_t req_id, int32_t layer, const void* q, const void* k_new,
+                                  const void* v_new, void* out, void* compute_stream) {
+  if (!c) return PCR_E_INVAL;
+  pcr_status st = device_ready(c);
+  if (st != PCR_OK) return st;
+  Request* r = planned_request(c, req_id, &st);
+  if (!r) return st;
+  if (layer < 0 || layer >= c->cfg.n_layers) return fail(c, PCR_E_INVAL, "layer out of range");
+  if (!q || !k_new || !v_new || !out) return fail(c, PCR_E_INVAL, "null q/k/v/out");
+  cudaStream_t s = static_cast<cudaStream_t>(compute_stream);
+  if ((st = ensure_tables(c, r, s)) != PCR_OK) return st;
+  return enqueue_attn(c, r, layer, q, k_new, v_new, out, s);
+}
+
+pcr_status pcr_run_prefill(pcr_ctx* c, int64_t req_id, const void* q_all, const void* k_all, const void* v_all,
+                           void* out_all, void* compute_stream, void* load_stream, int32_t mode,
+                           float* layer_times_ms) {
+  if (!c) return PCR_E_INVAL;
+  pcr_status st = device_ready(c);
+  if (st != PCR_OK) return st;
+  Request* r = planned_request(c, req_id, &st);
+  if (!r) return st;
+  if (!q_all || !k_all || !v_all || !out_all) return fail(c, PCR_E_INVAL, "null q/k/v/out");
+  if (mode != 0 && mode != 1) return fail(c, PCR_E_INVAL, "mode must be 0 (OVERLAP) or 1 (SYNC)");
+  cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
+  cudaStream_t ls = mode == 0 ? static_cast<cudaStream_t>(load_stream) : cs;
+  if (mode == 0 && load_stream == compute_stream)
+    return fail(c, PCR_E_INVAL, "OVERLAP mode needs two distinct streams");
+  const int64_t n2 = r->plan.n2;
+  const int64_t q_layer = n2 * c->hq * c->cfg.head_dim, kv_layer = n2 * c->hkv * c->cfg.head_dim;
+  const bool timed = layer_times_ms != nullptr;
+  if ((st = ensure_tables(c, r, ls)) != PCR_OK) return st;
+  if (mode == 0) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->region_ev[r->plan.region], 0));
+  for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
+    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 0], ls));
+    if ((st = enqueue_gather(c, r, l, ls)) != PCR_OK) return st;
+    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 1], ls));
+    if (mode == 0) {
+      CUDA_TRY(c, cudaEventRecord(c->ev_load[l], ls));
+      CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_load[l], 0));
+    }
+    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 2], cs));
+    st = enqueue_attn(c, r, l, static_cast<const uint16_t*>(q_all) + l * q_layer,
+                      static_cast<const uint16_t*>(k_all) + l * kv_layer,
+                      static_cast<const uint16_t*>(v_all) + l * kv_layer, static_cast<uint16_t*>(out_all) + l * q_layer,
+                      cs);
+    if (st != PCR_OK) return st;
+    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 3], cs));
+  }
+  if (mode == 0) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_join, ls));
+    CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_join, 0));
+  }
+  if (timed) {
+    CUDA_TRY(c, cudaStreamSynchronize(cs));
+    for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
+      CUDA_TRY(c, cudaEventElapsedTime(&layer_times_ms[2 * l], c->ev_t[4 * l + 0], c->ev_t[4 * l + 1]));
+      CUDA_TRY(c, cudaEventElapsedTime(&layer_times_ms[2 * l + 1], c->ev_t[4 * l + 2], c->ev_t[4 * l + 3]));
+    }
+  }
+  return PCR_OK;
+}
+
+}  // extern "C"
