@@ -1,0 +1,427 @@
+"""bench.py — reuse-prefill throughput of the PCR hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload L8|M7|L70|T] [--ratio r]
+                    [--mode overlap|sync] [--impl ours|reference]
+
+One STEP = one RAG request through the whole hot path:
+pcr_submit -> pcr_match_prefix (host plan, look-ahead LRU) -> pcr_run_prefill (per layer:
+host->HBM gather of the cached prefix KV, suffix append, tcgen05 suffix attention; load(l+1)
+overlapping attn(l) on two streams) -> pcr_release(commit).  Default workload = configs[1]
+(L8: Llama-3-8B shape, 32 layers, 32/8 heads, d=128, 4 docs x 1k cached + 128-token query,
+100% prefix hit, B=1).  value = context tokens (N1+N2) per second over K steps, whole job.
+
+N > 1 (torchrun): KV heads are sharded across ranks (rank r owns heads [r*Hkv/N, (r+1)*Hkv/N),
+its own store slice and host link); outputs are re-assembled by an NCCL all-gather.  The same
+request is processed by all ranks, so per-GPU work shrinks with N: scaling = "strong".
+
+--impl reference runs the fp64 CPU oracle (oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (geometry preset, N1 docs tokens, query tokens)
+    "L8": ("L8", 4096, 128),
+    "M7": ("M7", 8192, 128),
+    "L70": ("L70", 16384, 128),
+    "T": ("T", 256, 64),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="L8", choices=list(WORKLOADS))
+    ap.add_argument("--ratio", type=float, default=1.0, help="prefix hit ratio of the doc tokens (M7 sweep)")
+    ap.add_argument("--mode", default="overlap", choices=["overlap", "sync"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def geometry(name):
+    from pcrgen import PRESETS
+    return PRESETS[name]
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ oracle leg
+def oracle_sample(geo, N1, N2, hkv_loc, hq_loc, budget_s=15.0, seed=0, max_layers=None):
+    """Time the oracle (as it stands) on a bounded sample of the workload: whole layers of
+    load + append + fp64 suffix attention, until the budget is spent.  Returns
+    (seconds per layer, layers sampled)."""
+    from oracle.attention import bf16_bits_to_f64, suffix_attention_blocked
+    from oracle.kvload import append_layer, load_layer
+    from pcrgen import make_rng, randn_bf16
+    rng = make_rng(seed)
+    C, S, d = geo["C"], geo["S_pg"], geo["d"]
+    N = N1 + N2
+    n_chunks = N1 // C
+    n_pages = -(-N // S)
+    store = randn_bf16(rng, (n_chunks, 1, hkv_loc, 2, C, d))
+    pool = np.zeros((1, n_pages, hkv_loc, 2, S, d), np.uint16)
+    q = randn_bf16(rng, (N2, hq_loc, d))
+    kn = randn_bf16(rng, (N2, hkv_loc, d))
+    vn = randn_bf16(rng, (N2, hkv_loc, d))
+    slots, pages = list(range(n_chunks)), list(range(n_pages))
+    t0 = time.perf_counter()
+    layers = 0
+    while True:
+        load_layer(pool, store, slots, pages, 0, N1, C, S)
+        append_layer(pool, kn, vn, pages, 0, N1, S)
+        kc = np.concatenate([store[c, 0, :, 0].transpose(1, 0, 2) for c in range(n_chunks)] + [kn]) if n_chunks else kn
+        vc = np.concatenate([store[c, 0, :, 1].transpose(1, 0, 2) for c in range(n_chunks)] + [vn]) if n_chunks else vn
+        suffix_attention_blocked(bf16_bits_to_f64(q), bf16_bits_to_f64(kc), bf16_bits_to_f64(vc), N1)
+        layers += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or (max_layers and layers >= max_layers) or layers >= geo["L"]:
+            return el / layers, layers
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    wl_geo, n_doc, n_query = WORKLOADS[args.workload]
+    geo = geometry(wl_geo)
+    N1 = int(round(args.ratio * (n_doc // geo["C"]))) * geo["C"]
+    N2 = n_doc - N1 + n_query
+    per_step_budget = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        oracle_sample(geo, N1, N2, geo["Hkv"], geo["Hq"], budget_s=0.0, max_layers=1)
+    times = []
+    for _ in range(args.steps):
+        t_layer, _ = oracle_sample(geo, N1, N2, geo["Hkv"], geo["Hq"], budget_s=per_step_budget, max_layers=1)
+        times.append(t_layer * geo["L"])
+    t_step = statistics.mean(times)
+    value = (N1 + N2) / t_step
+    line = {
+        "impl": "reference", "metric": f"reuse-prefill tokens/s ({args.workload})", "value": value,
+        "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {geo['L']}L {geo['Hq']}/{geo['Hkv']} heads d={geo['d']}, "
+                               f"N1={N1} cached + N2={N2} computed", "N1": N1, "N2": N2},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+                         "sample": "1 of L layers per step (load + append + fp64 suffix attention, all heads), "
+                                   "time x L"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ our arm
+def h2d_peak_gbs(torch, nbytes=256 << 20, reps=5):
+    """Measured host->HBM copy-engine peak from pinned memory (the host-link roofline)."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h.fill_(1)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    best = 1e9
+    with torch.cuda.stream(s):
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            d.copy_(h, non_blocking=True)
+            b.record(s)
+            b.synchronize()
+            best = min(best, a.elapsed_time(b))
+    del h, d
+    return nbytes / (best * 1e-3) / 1e9
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_23049_b200 import MODE_OVERLAP, MODE_SYNC, Context
+    from pcrgen import make_rng, randn_bf16
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl_geo, n_doc, n_query = WORKLOADS[args.workload]
+    geo = geometry(wl_geo)
+    L, Hq, Hkv, d, C, S = geo["L"], geo["Hq"], geo["Hkv"], geo["d"], geo["C"], geo["S_pg"]
+    assert Hkv % world == 0, "KV-head sharding needs world | Hkv"
+    hkv, hq = Hkv // world, Hq // world
+    N1 = int(round(args.ratio * (n_doc // C))) * C
+    N = n_doc + n_query
+    N2 = N - N1
+    n_chunks = N1 // C
+    rng = make_rng(1000 + rank)
+
+    # pool: room for 2 requests; store: the doc chunks (+ slack)
+    pages_req = -(-N // S)
+    n_pool_pages = 2 * pages_req + 8
+    page_elems = L * hkv * 2 * S * d
+    pool = torch.empty(n_pool_pages * page_elems, dtype=torch.int16, device="cuda")
+    store_chunks = n_doc // C + 4
+    ctx = Context(L, Hq, Hkv, d, C, S, store_chunks, 4, device=local, pool=pool, rank=rank, world=world)
+
+    # warm the DRAM store: commit a request whose first n_chunks chunks are the cached docs
+    doc = make_rng(7).integers(0, 128256, n_doc, dtype=np.uint32)       # same tokens on every rank
+    if n_chunks:
+        ctx.submit(-1, np.concatenate([doc[:N1], [1]]).astype(np.uint32))
+        warm = ctx.match_prefix(-1, [])
+        assert warm["n_reserved"] == n_chunks
+        for s in warm["slots"]:
+            ctx.store_write(s, randn_bf16(rng, (ctx.slot_bytes // 2,)))
+        ctx.release(-1, True)
+    query = make_rng(8).integers(0, 128256, n_query, dtype=np.uint32)
+    toks = np.concatenate([doc, query])
+
+    # suffix Q/K/V (device-resident for `value`; pinned host copies for `e2e`)
+    def dev(a):
+        return torch.from_numpy(a.view(np.int16)).cuda()
+    q_h = randn_bf16(rng, (L, N2, hq, d))
+    k_h = randn_bf16(rng, (L, N2, hkv, d))
+    v_h = randn_bf16(rng, (L, N2, hkv, d))
+    q_d, k_d, v_d = dev(q_h), dev(k_h), dev(v_h)
+    out_d = torch.empty_like(q_d)
+    gathered = torch.empty((world,) + tuple(out_d.shape), dtype=out_d.dtype, device="cuda") if world > 1 else None
+    cs, ls = torch.cuda.Stream(), torch.cuda.Stream()
+    mode = MODE_OVERLAP if args.mode == "overlap" else MODE_SYNC
+    req_counter = [0]
+    match_us = []
+
+    def step(q, k, v, out, times=True):
+        rid = req_counter[0]
+        req_counter[0] += 1
+        t0 = time.perf_counter()
+        ctx.submit(rid, toks, n_cacheable=n_doc)
+        plan = ctx.match_prefix(rid, [])
+        match_us.append((time.perf_counter() - t0) * 1e6)
+        assert plan["n1"] == N1, plan["n1"]
+        t = ctx.run_prefill(rid, q, k, v, out, cs, ls, mode=mode, layer_times=times)
+        if world > 1:
+            with torch.cuda.stream(cs):
+                dist.all_gather_into_tensor(gathered, out)
+            cs.synchronize()
+        elif not times:
+            cs.synchronize()
+        ctx.release(rid, True)
+        return t
+
+    for _ in range(args.warmup):
+        step(q_d, k_d, v_d, out_d)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = ctx.kernel_launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(cs)
+    ls.wait_event(ev0)
+    layer_times = []
+    step_ms = []
+    for _ in range(args.steps):
+        e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_a.record(cs)
+        ls.wait_event(e_a)
+        layer_times.append(step(q_d, k_d, v_d, out_d))
+        e_b.record(cs)
+        e_b.synchronize()
+        step_ms.append(e_a.elapsed_time(e_b))
+    ev1.record(cs)
+    torch.cuda.synchronize()
+    total_ms = ev0.elapsed_time(ev1)
+    launches = ctx.kernel_launches - launches0
+    clk = clocks.stop()
+    if world > 1:
+        tt = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+        dist.barrier()
+
+    # e2e: the same step through the C-ABI with HOST buffers (H2D of q/k/v, D2H of out, per step)
+    e2e = None
+    if not args.no_e2e:
+        q_p = torch.from_numpy(q_h.view(np.int16)).pin_memory()
+        k_p = torch.from_numpy(k_h.view(np.int16)).pin_memory()
+        v_p = torch.from_numpy(v_h.view(np.int16)).pin_memory()
+        o_p = torch.empty(q_p.shape, dtype=torch.int16).pin_memory()
+        q2, k2, v2, o2 = (torch.empty_like(q_d), torch.empty_like(k_d), torch.empty_like(v_d),
+                          torch.empty_like(out_d))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_e2e = max(3, min(args.steps, 20))
+        a.record(cs)
+        for _ in range(n_e2e):
+            with torch.cuda.stream(cs):
+                q2.copy_(q_p, non_blocking=True)
+                k2.copy_(k_p, non_blocking=True)
+                v2.copy_(v_p, non_blocking=True)
+            ls.wait_stream(cs)
+            step(q2, k2, v2, o2, times=False)
+            with torch.cuda.stream(cs):
+                o_p.copy_(o2, non_blocking=True)
+            cs.synchronize()
+        b.record(cs)
+        b.synchronize()
+        e2e_ms = a.elapsed_time(b)
+        if world > 1:
+            tt = torch.tensor([e2e_ms], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt.item())
+        e2e = {"value": n_e2e * N / (e2e_ms * 1e-3), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(q_p.nbytes + k_p.nbytes + v_p.nbytes),
+               "d2h_bytes_per_step": int(o_p.nbytes), "steps": n_e2e}
+
+    # roofline of the dominant kernel (the host->HBM gather), from the live per-layer events
+    lt = np.array(layer_times)                      # [K][L][2] ms: gather, append+attn
+    gather_ms = float(lt[:, :, 0].mean())
+    attn_ms = float(lt[:, :, 1].mean())
+    load_bytes = 2 * N1 * hkv * d * 2               # algorithmic bytes per launch (one layer)
+    attn_flops = 4 * hq * d * (N2 * N1 + N2 * (N2 + 1) // 2)
+    peak_h2d = h2d_peak_gbs(torch)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    bf16_peak = peaks.get("bf16_tflops", 1590.0)
+    gather_gbs = load_bytes / (gather_ms * 1e-3) / 1e9 if N1 else 0.0
+    attn_tflops = attn_flops / (attn_ms * 1e-3) / 1e12
+    # pipelined bound T* from the measured per-layer times (O6) and the SYNC bound
+    # two in-order streams, identical layers: T* = t_ld + (L-1) max(t_ld, t_at) + t_at
+    ttft_pred = gather_ms + (L - 1) * max(gather_ms, attn_ms) + attn_ms
+    value = args.steps * N / (total_ms * 1e-3)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t_layer, n_l = oracle_sample(geo, N1, N2, hkv, hq, budget_s=15.0)
+        cpu = {"value": N / (t_layer * L), "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": f"{n_l} of {L} layers (pool load + append + fp64 suffix attention over all heads), "
+                         f"extrapolated x{L}/{n_l}"}
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    dominant = "kv_gather" if gather_ms >= attn_ms else "suffix_attn"
+    line = {
+        "metric": f"reuse-prefill tokens/s ({args.workload}: context tokens N1+N2 per second, TTFT in ttft_ms)",
+        "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) bf16 KV/Q, random token ids)",
+        "config": {"workload": f"{args.workload}: {L}L {Hq}/{Hkv} heads d={d}, N1={N1} cached (host DRAM) + "
+                               f"N2={N2} computed, B=1, C={C}, S_pg={S}, mode={args.mode}",
+                   "N1": N1, "N2": N2, "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
+                   "l2": f"inputs > L2: {L * load_bytes / 2**20:.0f} MiB of prefix KV streamed from host per step"},
+        "ttft_ms": statistics.median(step_ms), "ttft_ms_p90": float(np.percentile(step_ms, 90)),
+        "ttft_pred_ms": ttft_pred, "sync_bound_ms": L * (gather_ms + attn_ms),
+        "match_prefix_us": statistics.median(match_us),
+        "gpu_launches": launches,
+        "roofline": ({"bound": "host-link", "kernel": "kv_gather", "achieved": gather_gbs, "peak": peak_h2d,
+                      "unit": "GB/s", "frac": gather_gbs / peak_h2d, "traffic": None,
+                      "peak_source": "live: cudaMemcpyAsync H2D from pinned host, 256 MiB, best of 5",
+                      "algorithmic_bytes_per_launch": load_bytes, "avg_launch_ms": gather_ms}
+                     if dominant == "kv_gather" else
+                     {"bound": "tensor", "kernel": "suffix_attn(+append)", "achieved": attn_tflops,
+                      "peak": bf16_peak, "unit": "TFLOP/s", "frac": attn_tflops / bf16_peak, "traffic": None,
+                      "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)",
+                      "algorithmic_flops_per_launch": attn_flops, "avg_launch_ms": attn_ms}),
+        "roofline_attn": {"bound": "tensor", "achieved": attn_tflops, "peak": bf16_peak, "unit": "TFLOP/s",
+                          "frac": attn_tflops / bf16_peak, "avg_launch_ms": attn_ms,
+                          "note": "append + attention per layer, CUDA events on the compute stream"},
+        "host_link": {"gather_GBps": gather_gbs, "h2d_peak_GBps": peak_h2d},
+        "clocks": clk,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -213,8 +213,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int c = 0; c < kBlockN; c += 2) {
         const float e0 = ex2(s[c] - m_use), e1 = ex2(s[c + 1] - m_use);
-        rowsum += e0 + e1;
         __nv_bfloat162 b = __floats2bfloat162_rn(e0, e1);
+        // l sums the SAME bf16-rounded weights the PV product uses, so out = sum(w v)/sum(w)
+        // is an exact convex combination of V rows (no numerator/denominator mismatch).
+        rowsum += __low2float(b) + __high2float(b);
         pk[c / 2] = *reinterpret_cast<uint32_t*>(&b);
       }
       l = l * alpha + rowsum;

@@ -1,0 +1,220 @@
+"""GPU parity: libpcr.so (sm_100a kernels, through the C-ABI) vs the fp64 oracle on the same
+seeded inputs.  Pool contents bit-exact (O3), attention within the north_star tolerance
+(rel-L2 <= 5e-3, max-abs <= 2e-2, O4), plans bit-exact (O2)."""
+import zlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.tree import PlanOracle  # noqa: E402
+from oracle.tiny_model import TinyModel  # noqa: E402
+from pcrgen import (appendix_c_trace, f32_to_bf16_bits, make_rng, pack_store_slots,  # noqa: E402
+                    stress_values)
+from tests._gpu_harness import (TOL_MAX_ABS, TOL_REL_L2, Rig, check_attention, sample_rows,  # noqa: E402
+                                to_dev, to_host)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+
+
+def _warm_prefix(rig, req_id, doc_tokens, k_ctx, v_ctx, n_chunks):
+    """Commit a request whose first n_chunks chunks are `doc_tokens`, writing their KV."""
+    toks = np.concatenate([doc_tokens, np.array([7], np.uint32)])
+    rig.ctx.submit(req_id, toks)
+    plan = rig.ctx.match_prefix(req_id, [])
+    assert plan["n_matched"] == 0 and plan["n_reserved"] == n_chunks
+    recs = pack_store_slots(k_ctx, v_ctx, n_chunks, rig.C)
+    for c, s in enumerate(plan["slots"]):
+        rig.write_slot(s, recs[c])
+    rig.ctx.release(req_id, True)
+
+
+def _single_request(kind, L, Hq, Hkv, d, C, S, N1, N2, seed, mode=0, world=1, rank=0):
+    """Warm N1 tokens, then run one request [doc | query] and return everything to compare."""
+    rng = make_rng(seed)
+    Hkv_l, Hq_l = Hkv // world, Hq // world
+    q, k, v = [], [], []
+    for l in range(L):
+        ql, kl, vl = stress_values(kind, seed * 100 + l, N1, N2, Hq, Hkv, d)
+        q.append(ql)
+        k.append(kl)
+        v.append(vl)
+    q, k, v = np.stack(q), np.stack(k), np.stack(v)       # [L][N2][Hq][d], [L][N][Hkv][d]
+    hs = slice(rank * Hkv_l, (rank + 1) * Hkv_l)
+    qs = slice(rank * Hq_l, (rank + 1) * Hq_l)
+    q, k, v = q[:, :, qs], k[:, :, hs], v[:, :, hs]
+    n_pages = (N1 + N2) // S + 8
+    rig = Rig(L, Hq, Hkv, d, C, S, store_chunks=max(1, N1 // C) + 2, n_pool_pages=n_pages + N1 // S + 2,
+              rank=rank, world=world)
+    doc = rng.integers(0, 1000, N1, dtype=np.uint32)
+    if N1:
+        _warm_prefix(rig, 1000, doc, k[:, :N1], v[:, :N1], N1 // C)
+    toks = np.concatenate([doc, rng.integers(0, 1000, N2, dtype=np.uint32)])
+    rig.ctx.submit(1, toks, n_cacheable=N1)
+    plan = rig.ctx.match_prefix(1, [])
+    assert plan["n1"] == N1 and plan["n2"] == N2
+    out, _ = rig.run(1, q, k[:, N1:], v[:, N1:], mode=mode)
+    return rig, plan, q, k, v, out
+
+
+CASES = [
+    # (L, Hq, Hkv, d, C, S, N1, N2)
+    (2, 32, 8, 128, 256, 64, 1024, 128),   # L8 geometry, short
+    (2, 32, 8, 128, 256, 16, 512, 200),    # ragged N2, paper's 16-token pages
+    (2, 64, 8, 128, 256, 64, 768, 77),     # G = 8 (Llama-3-70B shape)
+    (2, 8, 8, 128, 128, 32, 256, 300),     # G = 1 (MHA), several M tiles
+    (2, 4, 2, 64, 64, 16, 256, 64),        # preset T geometry
+    (1, 32, 8, 128, 256, 128, 0, 333),     # N1 = 0: plain causal self-attention
+    (1, 32, 8, 128, 256, 64, 2048, 1),     # N2 = 1: decode-like row
+]
+
+
+@pytest.mark.parametrize("kind", ["iid", "q4", "kout", "advfuture"])
+@pytest.mark.parametrize("case", CASES, ids=[f"L{c[0]}H{c[1]}/{c[2]}d{c[3]}S{c[5]}N{c[6]}+{c[7]}" for c in CASES])
+def test_attention_and_pool_vs_oracle(kind, case):
+    L, Hq, Hkv, d, C, S, N1, N2 = case
+    rig, plan, q, k, v, out = _single_request(kind, L, Hq, Hkv, d, C, S, N1, N2, seed=zlib.crc32(repr((kind,) + case).encode()) % 1000)
+    pool = rig.pool_np()
+    for l in range(L):
+        exp_pool = rig.expected_pool(plan, k[:, N1:], v[:, N1:], l)
+        pg = plan["pages"]
+        for t in range(N1 + N2):                   # O3: bit-exact at every token position
+            assert np.array_equal(pool[l, pg[t // S], :, :, t % S], exp_pool[l, pg[t // S], :, :, t % S]), (l, t)
+        tail = [(t, pg[t // S]) for t in range(N1 + N2, len(pg) * S)]
+        for t, p in tail:                          # kernel property: tail rows are zero (finite)
+            assert not pool[l, p, :, :, t % S].any()
+        kc, vc = rig.expected_context(plan, k[:, N1:], v[:, N1:], l)
+        assert np.array_equal(kc, k[l]) and np.array_equal(vc, v[l])
+        r, m = check_attention(out[l], q[l], kc, vc, N1, blocked=True)
+        assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (l, r, m)
+
+
+def test_overlap_sync_and_per_layer_api_are_bitwise_identical():
+    rig, plan, q, k, v, out = _single_request("iid", 3, 32, 8, 128, 256, 64, 1024, 130, seed=5)
+    rig.ctx.release(1, True)
+    toks_plan = rig.ctx
+    # same request again: SYNC mode
+    rng = make_rng(5)
+    doc = rng.integers(0, 1000, 1024, dtype=np.uint32)
+    toks = np.concatenate([doc, rng.integers(0, 1000, 130, dtype=np.uint32)])
+    toks_plan.submit(2, toks, n_cacheable=1024)
+    p2 = toks_plan.match_prefix(2, [])
+    assert p2["n1"] == 1024
+    out_sync, _ = rig.run(2, q, k[:, 1024:], v[:, 1024:], mode=1)
+    assert np.array_equal(out_sync, out)
+    # per-layer API on two streams, ordered by the caller
+    toks_plan.release(2, True)
+    toks_plan.submit(3, toks, n_cacheable=1024)
+    toks_plan.match_prefix(3, [])
+    qd, kd, vd = to_dev(q), to_dev(k[:, 1024:]), to_dev(v[:, 1024:])
+    o = torch.empty_like(qd)
+    for l in range(3):
+        rig.ctx.load_layer_kv(3, l, rig.ls)
+        ev = torch.cuda.Event()
+        ev.record(rig.ls)
+        rig.cs.wait_event(ev)
+        rig.ctx.prefill_attn_layer(3, l, qd[l], kd[l], vd[l], o[l], rig.cs)
+    rig.cs.synchronize()
+    assert np.array_equal(to_host(o), out)
+
+
+def test_page_size_does_not_change_results():
+    outs = []
+    for S in (16, 32, 64, 128):
+        _, _, _, _, _, out = _single_request("kout", 1, 32, 8, 128, 256, S, 1024, 96, seed=9)
+        outs.append(out)
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+def test_full_context_self_consistency():
+    """suffix_attn with N1 = 0 over the whole context, last N2 rows == the reuse
+    path's output (the kernel's per-row math does not depend on the M-tile split)."""
+    L, Hq, Hkv, d, C, S, N1, N2 = 1, 32, 8, 128, 256, 64, 512, 128
+    rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, N1, N2, seed=3)
+    # full-context run: queries for all N tokens (prefix rows random, suffix rows = q)
+    rng = make_rng(4)
+    qfull = np.concatenate([f32_to_bf16_bits(rng.standard_normal((L, N1, Hq, d), dtype=np.float32)), q], axis=1)
+    rig2 = Rig(L, Hq, Hkv, d, C, S, store_chunks=2, n_pool_pages=(N1 + N2) // S + 4)
+    rig2.ctx.submit(5, rng.integers(0, 1000, N1 + N2, dtype=np.uint32), n_cacheable=0)
+    p = rig2.ctx.match_prefix(5, [])
+    assert p["n1"] == 0
+    full, _ = rig2.run(5, qfull, k, v)
+    a, b = full[:, N1:], out
+    from tests._gpu_harness import rel_l2
+    from oracle.attention import bf16_bits_to_f64
+    assert rel_l2(bf16_bits_to_f64(a), bf16_bits_to_f64(b)) <= TOL_REL_L2
+    print("full-context vs reuse bitwise equal:", np.array_equal(a, b))
+
+
+def test_kv_head_sharding_concat_equals_single_gpu():
+    """SURVEY §8(e)/O7 on one GPU: rank r's context owns kv heads [r*Hkv/P, (r+1)*Hkv/P);
+    concatenating the P ranks' outputs by head equals the P=1 output bit for bit, and each
+    rank's pool holds exactly its head slice."""
+    full = _single_request("iid", 2, 32, 8, 128, 256, 64, 512, 100, seed=21)[5]
+    for P in (2, 4, 8):
+        parts = [_single_request("iid", 2, 32, 8, 128, 256, 64, 512, 100, seed=21, world=P, rank=r)[5]
+                 for r in range(P)]
+        assert np.array_equal(np.concatenate(parts, axis=2), full)
+
+
+def test_appendix_c_trace_tiny_model():
+    """Preset T end to end: the Appendix C trace with realistic (tiny-transformer) Q/K/V,
+    look-ahead W=2: plans bit-exact vs the oracle planner, pool bit-exact, attention in tol."""
+    g = dict(L=2, Hq=4, Hkv=2, d=64, C=64, S=16)
+    docs, order, reqs = appendix_c_trace(0)
+    model = TinyModel(L=2, Hq=4, Hkv=2, d=64, d_model=96, d_ff=128, vocab=1 << 17, seed=0)
+    W = 2
+    rig = Rig(g["L"], g["Hq"], g["Hkv"], g["d"], g["C"], g["S"], store_chunks=10, n_pool_pages=64, window=W)
+    orc = PlanOracle(C=64, S_pg=16, store_chunks=10, n_pages=64, window=W)
+    for i, t in enumerate(reqs):
+        rig.ctx.submit(i, t)
+        orc.submit(i, t)
+    for i, toks in enumerate(reqs):
+        pend = list(range(i + 1, min(len(reqs), i + 1 + W)))
+        plan = rig.ctx.match_prefix(i, pend)
+        po = orc.match_prefix(i, pend)
+        for f in ("n_matched", "n_reserved", "n1", "n2", "slots", "pages"):
+            assert plan[f] == po[f]
+        assert plan["evicted"] == po["evicted"]
+        _, kv, qs = model.forward(toks)
+        N1, N = plan["n1"], len(toks)
+        q = np.stack([f32_to_bf16_bits(qs[l][N1:].astype(np.float32)) for l in range(2)])
+        k = np.stack([f32_to_bf16_bits(kv[l][0].astype(np.float32)) for l in range(2)])
+        v = np.stack([f32_to_bf16_bits(kv[l][1].astype(np.float32)) for l in range(2)])
+        out, _ = rig.run(i, q, k[:, N1:], v[:, N1:])
+        pool = rig.pool_np()
+        for l in range(2):
+            exp_pool = rig.expected_pool(plan, k[:, N1:], v[:, N1:], l, pool_before=pool)
+            assert np.array_equal(pool[l], exp_pool[l])
+            kc, vc = rig.expected_context(plan, k[:, N1:], v[:, N1:], l)
+            r, m = check_attention(out[l], q[l], kc, vc, N1)
+            assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (i, l, r, m)
+        # "offload": the reserved chunks' KV as computed by this request
+        recs = pack_store_slots(k, v, plan["n_matched"] + plan["n_reserved"], 64)
+        for c in range(plan["n_matched"], plan["n_matched"] + plan["n_reserved"]):
+            rig.write_slot(plan["slots"][c], recs[c])
+        rig.ctx.release(i, True)
+        orc.release(i, True)
+
+
+def test_l8_full_size_sampled():
+    """configs[1] at full size in the bench's launch configuration (OVERLAP, 32 layers,
+    4096 cached + 128 query): sampled rows vs the oracle on layers 0, 15, 31; pool bit-exact
+    on those layers."""
+    L, Hq, Hkv, d, C, S, N1, N2 = 32, 32, 8, 128, 256, 64, 4096, 128
+    rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, N1, N2, seed=1)
+    rows = sample_rows(N2, N1, C, S, k=64, seed=1)
+    pool = rig.pool_np()
+    for l in (0, 15, 31):
+        exp_pool = rig.expected_pool(plan, k[:, N1:], v[:, N1:], l)
+        assert np.array_equal(pool[l][plan["pages"]], exp_pool[l][plan["pages"]])
+        kc, vc = rig.expected_context(plan, k[:, N1:], v[:, N1:], l)
+        r, m = check_attention(out[l], q[l], kc, vc, N1, rows=rows)
+        assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (l, r, m)
