@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gather-ctas", type=int, default=0, help="CTAs of the host->HBM gather (0 = library default)")
+    ap.add_argument("--profile-steps", type=int, default=5, help="extra steps with per-layer events (after timing)")
     return ap.parse_args()
 
 
@@ -234,7 +236,8 @@ def run_ours(args):
     page_elems = L * hkv * 2 * S * d
     pool = torch.empty(n_pool_pages * page_elems, dtype=torch.int16, device="cuda")
     store_chunks = n_doc // C + 4
-    ctx = Context(L, Hq, Hkv, d, C, S, store_chunks, 4, device=local, pool=pool, rank=rank, world=world)
+    ctx = Context(L, Hq, Hkv, d, C, S, store_chunks, 4, device=local, pool=pool, rank=rank, world=world,
+                  gather_ctas=args.gather_ctas)
 
     # warm the DRAM store: commit a request whose first n_chunks chunks are the cached docs
     doc = make_rng(7).integers(0, 128256, n_doc, dtype=np.uint32)       # same tokens on every rank
@@ -257,12 +260,15 @@ def run_ours(args):
     q_d, k_d, v_d = dev(q_h), dev(k_h), dev(v_h)
     out_d = torch.empty_like(q_d)
     gathered = torch.empty((world,) + tuple(out_d.shape), dtype=out_d.dtype, device="cuda") if world > 1 else None
-    cs, ls = torch.cuda.Stream(), torch.cuda.Stream()
+    # the load stream gets the highest priority: its few gather CTAs are scheduled ahead of the
+    # attention grid's CTAs whenever an SM slot frees up
+    cs, ls = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
     mode = MODE_OVERLAP if args.mode == "overlap" else MODE_SYNC
     req_counter = [0]
     match_us = []
 
-    def step(q, k, v, out, times=True):
+    def step(q, k, v, out, times=False, load_events=None):
+        """One request.  The caller's stream sync precedes pcr_release (pages are reused)."""
         rid = req_counter[0]
         req_counter[0] += 1
         t0 = time.perf_counter()
@@ -270,14 +276,18 @@ def run_ours(args):
         plan = ctx.match_prefix(rid, [])
         match_us.append((time.perf_counter() - t0) * 1e6)
         assert plan["n1"] == N1, plan["n1"]
+        if load_events:
+            load_events[0].record(ls)
         t = ctx.run_prefill(rid, q, k, v, out, cs, ls, mode=mode, layer_times=times)
+        if load_events:
+            load_events[1].record(ls)
         if world > 1:
             with torch.cuda.stream(cs):
                 dist.all_gather_into_tensor(gathered, out)
-            cs.synchronize()
-        elif not times:
-            cs.synchronize()
-        ctx.release(rid, True)
+        cs.synchronize()
+        # No offload stream yet: the request's newly reserved chunks have no KV
+        # written, so they are dropped instead of committed; the cached prefix stays resident.
+        ctx.release(rid, False)
         return t
 
     for _ in range(args.warmup):
@@ -292,16 +302,17 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev0.record(cs)
     ls.wait_event(ev0)
-    layer_times = []
-    step_ms = []
+    step_ms, load_ms = [], []
     for _ in range(args.steps):
         e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l_a, l_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e_a.record(cs)
         ls.wait_event(e_a)
-        layer_times.append(step(q_d, k_d, v_d, out_d))
+        step(q_d, k_d, v_d, out_d, load_events=(l_a, l_b))
         e_b.record(cs)
         e_b.synchronize()
         step_ms.append(e_a.elapsed_time(e_b))
+        load_ms.append(l_a.elapsed_time(l_b))
     ev1.record(cs)
     torch.cuda.synchronize()
     total_ms = ev0.elapsed_time(ev1)
@@ -312,6 +323,15 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
         dist.barrier()
+
+    # Per-kernel durations.  gather: inside a step the load stream runs the L gather launches
+    # back to back (it never waits), so its busy time per step / L is the average launch
+    # duration, measured over the timed steps with two events per step on that stream.
+    # append+attention: per-layer events on the compute stream, in extra profiling steps.
+    gather_ms = float(np.mean(load_ms)) / L
+    lt = np.array([step(q_d, k_d, v_d, out_d, times=True) for _ in range(max(1, args.profile_steps))])
+    attn_ms = float(lt[:, :, 1].mean())
+    gather_ms_evented = float(lt[:, :, 0].mean())
 
     # e2e: the same step through the C-ABI with HOST buffers (H2D of q/k/v, D2H of out, per step)
     e2e = None
@@ -334,7 +354,7 @@ def run_ours(args):
                 k2.copy_(k_p, non_blocking=True)
                 v2.copy_(v_p, non_blocking=True)
             ls.wait_stream(cs)
-            step(q2, k2, v2, o2, times=False)
+            step(q2, k2, v2, o2)
             with torch.cuda.stream(cs):
                 o_p.copy_(o2, non_blocking=True)
             cs.synchronize()
@@ -349,11 +369,7 @@ def run_ours(args):
                "h2d_bytes_per_step": int(q_p.nbytes + k_p.nbytes + v_p.nbytes),
                "d2h_bytes_per_step": int(o_p.nbytes), "steps": n_e2e}
 
-    # roofline of the dominant kernel (the host->HBM gather), from the live per-layer events
-    lt = np.array(layer_times)                      # [K][L][2] ms: gather, append+attn
-    gather_ms = float(lt[:, :, 0].mean())
-    attn_ms = float(lt[:, :, 1].mean())
-    load_bytes = 2 * N1 * hkv * d * 2               # algorithmic bytes per launch (one layer)
+    load_bytes = 2 * N1 * hkv * d * 2               # algorithmic bytes per gather launch (one layer)
     attn_flops = 4 * hq * d * (N2 * N1 + N2 * (N2 + 1) // 2)
     peak_h2d = h2d_peak_gbs(torch)
     peaks = {}
@@ -362,9 +378,9 @@ def run_ours(args):
     except Exception:
         pass
     bf16_peak = peaks.get("bf16_tflops", 1590.0)
+    bf16_src = "MEASURED_PEAKS.json bf16_tflops (burst)" if "bf16_tflops" in peaks else "fallback 1590 (B200_PROFILING.md)"
     gather_gbs = load_bytes / (gather_ms * 1e-3) / 1e9 if N1 else 0.0
     attn_tflops = attn_flops / (attn_ms * 1e-3) / 1e12
-    # pipelined bound T* from the measured per-layer times (O6) and the SYNC bound
     # two in-order streams, identical layers: T* = t_ld + (L-1) max(t_ld, t_at) + t_at
     ttft_pred = gather_ms + (L - 1) * max(gather_ms, attn_ms) + attn_ms
     value = args.steps * N / (total_ms * 1e-3)
@@ -379,9 +395,16 @@ def run_ours(args):
         if world > 1:
             dist.destroy_process_group()
         return
-    dominant = "kv_gather" if gather_ms >= attn_ms else "suffix_attn"
+    dominant = "kv_gather" if N1 and gather_ms >= attn_ms else "suffix_attn"
+    rl_gather = {"bound": "host-link", "kernel": "kv_gather", "achieved": gather_gbs, "peak": peak_h2d,
+                 "unit": "GB/s", "frac": gather_gbs / peak_h2d, "traffic": None,
+                 "peak_source": "live: cudaMemcpyAsync H2D from pinned host, 256 MiB, best of 5",
+                 "algorithmic_bytes_per_launch": load_bytes, "avg_launch_ms": gather_ms}
+    rl_attn = {"bound": "tensor", "kernel": "kv_append+suffix_attn", "achieved": attn_tflops, "peak": bf16_peak,
+               "unit": "TFLOP/s", "frac": attn_tflops / bf16_peak, "traffic": None, "peak_source": bf16_src,
+               "algorithmic_flops_per_launch": attn_flops, "avg_launch_ms": attn_ms}
     line = {
-        "metric": f"reuse-prefill tokens/s ({args.workload}: context tokens N1+N2 per second, TTFT in ttft_ms)",
+        "metric": f"reuse-prefill tokens/s ({args.workload}: context tokens N1+N2 per second; TTFT in ttft_ms)",
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) bf16 KV/Q, random token ids)",
@@ -391,21 +414,12 @@ def run_ours(args):
                    "l2": f"inputs > L2: {L * load_bytes / 2**20:.0f} MiB of prefix KV streamed from host per step"},
         "ttft_ms": statistics.median(step_ms), "ttft_ms_p90": float(np.percentile(step_ms, 90)),
         "ttft_pred_ms": ttft_pred, "sync_bound_ms": L * (gather_ms + attn_ms),
+        "gather_ms_per_layer": gather_ms, "gather_ms_per_layer_evented": gather_ms_evented,
+        "attn_ms_per_layer": attn_ms, "gather_ctas": args.gather_ctas or 16,
         "match_prefix_us": statistics.median(match_us),
         "gpu_launches": launches,
-        "roofline": ({"bound": "host-link", "kernel": "kv_gather", "achieved": gather_gbs, "peak": peak_h2d,
-                      "unit": "GB/s", "frac": gather_gbs / peak_h2d, "traffic": None,
-                      "peak_source": "live: cudaMemcpyAsync H2D from pinned host, 256 MiB, best of 5",
-                      "algorithmic_bytes_per_launch": load_bytes, "avg_launch_ms": gather_ms}
-                     if dominant == "kv_gather" else
-                     {"bound": "tensor", "kernel": "suffix_attn(+append)", "achieved": attn_tflops,
-                      "peak": bf16_peak, "unit": "TFLOP/s", "frac": attn_tflops / bf16_peak, "traffic": None,
-                      "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)",
-                      "algorithmic_flops_per_launch": attn_flops, "avg_launch_ms": attn_ms}),
-        "roofline_attn": {"bound": "tensor", "achieved": attn_tflops, "peak": bf16_peak, "unit": "TFLOP/s",
-                          "frac": attn_tflops / bf16_peak, "avg_launch_ms": attn_ms,
-                          "note": "append + attention per layer, CUDA events on the compute stream"},
-        "host_link": {"gather_GBps": gather_gbs, "h2d_peak_GBps": peak_h2d},
+        "roofline": rl_gather if dominant == "kv_gather" else rl_attn,
+        "roofline_attn": rl_attn,
         "clocks": clk,
         "e2e": e2e,
         "cpu_baseline": cpu,

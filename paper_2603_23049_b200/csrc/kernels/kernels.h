@@ -36,12 +36,17 @@ struct AttnParams {
   int32_t n_req_pages;
   int64_t n_pool_pages;
   float scale_log2;       // log2(e) / sqrt(d)
+  int32_t n_splits;       // set by the launcher (split-KV count)
+  float* ws_o;            // split-KV workspace [splits][N2*hq][d] fp32 (nullable: no split-KV)
+  float* ws_lse;          // [splits][N2*hq] log2-domain LSE
+  int64_t ws_bytes;       // bytes available in ws_o
 };
 
 // a4: suffix-query causal attention over the request's pool pages (tcgen05 + TMEM + TMA).
 // `tmap_pool` is a 2D tensor map over the pool viewed as [rows][d] (rows = L*pages*Hkv*2*S),
 // box {64, S}, SWIZZLE_128B.
+// `launches` is incremented by the number of kernels enqueued (attention [+ split-KV combine]).
 cudaError_t launch_suffix_attn(const CUtensorMap* tmap_pool, const AttnParams& p, int32_t d,
-                               cudaStream_t stream);
+                               cudaStream_t stream, int* launches);
 
 }  // namespace pcr

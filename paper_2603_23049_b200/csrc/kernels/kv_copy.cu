@@ -12,7 +12,10 @@
 namespace pcr {
 namespace {
 
-constexpr int kThreads = 512;
+// 256 threads x <= 40 registers (10K registers, no shared memory) lets a gather CTA co-reside
+// with an attention CTA (256 threads, ~47K registers, ~195 KB smem) on the same SM, so loads of
+// layer l+1 are never queued behind the attention grid of layer l.
+constexpr int kThreads = 256;
 constexpr int kUnroll = 4;
 
 __device__ __forceinline__ uint4 ld_host_stream(const uint4* p) {
@@ -25,7 +28,7 @@ __device__ __forceinline__ uint4 ld_host_stream(const uint4* p) {
 
 // grid = (ctas_per_chunk, n_matched).  Chunk c's layer block in the store is contiguous:
 // [Hkv][2][C][d] starting at store + slot*slot_elems + layer*Hkv*2*C*d.
-__global__ void __launch_bounds__(kThreads) kv_gather_kernel(const uint4* __restrict__ store,
+__global__ void __launch_bounds__(kThreads, 6) kv_gather_kernel(const uint4* __restrict__ store,
                                                              uint4* __restrict__ pool,
                                                              const int32_t* __restrict__ slots,
                                                              const int32_t* __restrict__ pages, int32_t layer,

@@ -1,24 +1,34 @@
 // a4 — suffix-query causal attention over the paged pool (prefix + suffix KV), sm_100a.
 //
-// What it computes (R2/R3): for local query head h (kv head g = h / G) and
-// suffix row i at absolute position p = n1 + i,
-//     out[i][h] = sum_{j<=p} exp(s_j - m) V[j][g] / sum_{j<=p} exp(s_j - m),  s_j = q[i][h].K[j][g]/sqrt(d)
-// with bf16 inputs, fp32 accumulation and bf16 output.
+// What it computes (R2/R3/R18): for local query head h (kv head g = h / G)
+// and suffix row i at absolute position p = n1 + i,
+//     out[i][h] = sum_{j<=p} w_j V[j][g] / sum_{j<=p} w_j,   w_j = bf16(exp(s_j - m)),
+//     s_j = q[i][h] . K[j][g] / sqrt(d),
+// bf16 inputs, fp32 accumulation (TMEM), bf16 output.
 //
-// B200 design: one CTA per (128-row M tile, kv head).  M rows pack
-// (token, head-in-group) pairs, row r = t*G + gg, so one K/V tile read serves all G query heads
-// of the group.  Keys are processed in tiles of 128:
-//   warp 0  TMA producer: K and V pages of the tile -> smem (2D tensor map over the pool,
-//           one box of {64 dims, S_pg rows} per page-half, SWIZZLE_128B), 2-stage ring;
-//   warp 1  MMA issuer (one thread): S = Q K^T into TMEM (double-buffered, 2 x 128 columns),
-//           then O += P V into TMEM (D columns), tcgen05.commit -> mbarriers;
-//   warp 2  TMEM allocator (512 columns);
-//   warps 4-7 softmax / correction / epilogue, one thread per M row (TMEM lane): tcgen05.ld of
-//           its S row, causal mask on the diagonal tiles only, online softmax in the log2
-//           domain with lazy rescaling of O (only when the running max grows by > 8, so P <= 256),
-//           P as bf16 into smem in the UMMA K-major SWIZZLE_128B layout, final O / l -> bf16.
+// B200 design (DESIGN.md §6 "suffix_attn"):
+//  * GQA packing: M rows are (token, head-in-group) pairs, r = t*G + gg, so one K/V tile read
+//    serves all G query heads of the group.  A CTA owns NQ = 2 Q tiles of 128 rows (256 rows)
+//    of one kv head and one range of 128-key tiles (split-KV when the grid is small).
+//  * warp 0: TMA producer — Q tiles once (3D tensor map over q [N2][Hq][d], box {64, G, 128/G},
+//    rows past N2 zero-filled), then K and V pages of every key tile (2D tensor map over the
+//    pool, one box {64 dims, S_pg rows} per page and 64-column half, SWIZZLE_128B), 2 stages.
+//  * warp 1: one thread issues tcgen05.mma (kind::f16, fp32 accumulate):
+//        S_t = Q_t K^T      (A, B from smem, K-major; D -> TMEM S_t, 128 columns)
+//        O_t += P_t V       (A = P_t from TMEM, B = V from smem MN-major; D -> TMEM O_t)
+//    ping-ponging the two Q tiles so the tensor pipe works on one tile while the other tile's
+//    softmax runs.  tcgen05 MMAs of one thread complete in issue order, so the commit that
+//    signals "S_t(j+1) ready" also certifies that O_t(j) += P_t(j) V(j) finished.
+//  * warp 2: tcgen05.alloc of all 512 TMEM columns: S_0, S_1 (128 each, P_t aliases S_t as
+//    packed bf16x2), O_0, O_1 (d each).
+//  * warps 4-7 / 8-11: softmax of Q tile 0 / 1, one thread per M row (= TMEM lane): tcgen05.ld
+//    of its S row, causal mask only on tiles crossing the diagonal, online softmax in the log2
+//    domain (one FFMA + ex2.approx per score) with lazy rescaling of O in TMEM (only when the
+//    running max grows by > 8, so P <= 256 in bf16), P -> TMEM with tcgen05.st, row sum of the
+//    same bf16-rounded weights (R18).  Epilogue: O / l -> bf16 (or fp32 partial + LSE per split).
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdio>
 
 #include "kernels.h"
@@ -29,9 +39,10 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kBlockM = 128;
-constexpr int kBlockN = 128;
-constexpr int kThreads = 256;
+constexpr int kBlockM = 128;   // rows per Q tile (= TMEM lanes)
+constexpr int kBlockN = 128;   // keys per tile
+constexpr int kNQ = 2;         // Q tiles per CTA
+constexpr int kThreads = 128 + kNQ * 128;
 constexpr int kHalfBytes = 128 * 128;  // 128 rows x 128 bytes (64 bf16) per swizzle column block
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
@@ -39,26 +50,52 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 template <int D>
 struct Layout {
   static constexpr int kHalves = D / 64;
-  static constexpr int kQ = 0;
-  static constexpr int kQBytes = kHalves * kHalfBytes;
-  static constexpr int kTileBytes = kHalves * kHalfBytes;  // one K or V tile of 128 keys
-  static constexpr int kK0 = kQ + kQBytes;
+  static constexpr int kTileBytes = kHalves * kHalfBytes;  // one Q tile, or one K or V tile
+  static constexpr int kQ0 = 0;
+  static constexpr int kK0 = kQ0 + kNQ * kTileBytes;
   static constexpr int kV0 = kK0 + 2 * kTileBytes;
-  static constexpr int kP = kV0 + 2 * kTileBytes;
-  static constexpr int kPBytes = 2 * kHalfBytes;           // 128 rows x 128 keys
-  static constexpr int kBar = kP + kPBytes;
+  static constexpr int kBar = kV0 + 2 * kTileBytes;
   static constexpr int kBytes = kBar + 256;
-  static constexpr int kAlloc = kBytes + 1024;              // slack for 1024-byte alignment
+  static constexpr int kAlloc = kBytes + 1024;  // slack for 1024-byte alignment
+  static constexpr uint32_t kColS = 0;          // S_t at t*128
+  static constexpr uint32_t kColO = kNQ * kBlockN;  // O_t at kColO + t*D
 };
 
 struct Bars {
-  uint64_t k_full[2], v_full[2], kv_empty[2], s_full[2], s_empty[2], p_full, o_done, q_full;
+  uint64_t q_full, k_full[2], v_full[2], kv_empty[2], s_full[kNQ], p_full[kNQ], o_full;
   uint32_t tmem_base;
 };
 
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m, int32_t c0, int32_t c1,
+                                            int32_t c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// D[tmem] (+)= A[tmem] * B[smem]  (kind::f16; A is M x K bf16 packed two per 32-bit column).
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b, float& sum) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  sum += __low2float(v) + __high2float(v);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
-    suffix_attn_kernel(const __grid_constant__ CUtensorMap tmap, const AttnParams p) {
+    suffix_attn_kernel(const __grid_constant__ CUtensorMap tmap_pool, const __grid_constant__ CUtensorMap tmap_q,
+                       const AttnParams p) {
   using Lay = Layout<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -66,27 +103,33 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int g = blockIdx.y;                 // local kv head
+  const int g = blockIdx.y;  // local kv head
   const int G = p.hq / p.hkv;
   const int tok_per_tile = kBlockM / G;
-  const int i0 = blockIdx.x * tok_per_tile;
-  const int i_end = min(i0 + tok_per_tile, p.n2);
-  const int n_tiles = (p.n1 + i_end + kBlockN - 1) / kBlockN;
+  const int i0 = blockIdx.x * kNQ * tok_per_tile;
+  const int i_end = min(i0 + kNQ * tok_per_tile, p.n2);
+  const int n_tiles_all = (p.n1 + i_end + kBlockN - 1) / kBlockN;
+  const int per_split = (n_tiles_all + p.n_splits - 1) / p.n_splits;
+  const int j_begin = blockIdx.z * per_split;
+  const int j_end = min(j_begin + per_split, n_tiles_all);
+  const int n_iter = max(0, j_end - j_begin);
   const int pages_per_tile = kBlockN / p.S;
 
   if (threadIdx.x == 0) {
+    mbar_init(&bars->q_full, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bars->k_full[s], 1);
       mbar_init(&bars->v_full[s], 1);
       mbar_init(&bars->kv_empty[s], 1);
-      mbar_init(&bars->s_full[s], 1);
-      mbar_init(&bars->s_empty[s], 128);
     }
-    mbar_init(&bars->p_full, 128);
-    mbar_init(&bars->o_done, 1);
-    mbar_init(&bars->q_full, 128);
+    for (int t = 0; t < kNQ; ++t) {
+      mbar_init(&bars->s_full[t], 1);
+      mbar_init(&bars->p_full[t], 128);
+    }
+    mbar_init(&bars->o_full, 1);
     fence_mbar_init();
-    tma_prefetch_desc(&tmap);
+    tma_prefetch_desc(&tmap_pool);
+    tma_prefetch_desc(&tmap_q);
   }
   if (warp == 2) tmem_alloc<kTmemCols>(&bars->tmem_base);
   tc_fence_before();
@@ -96,11 +139,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
-    if (lane == 0) {
+    if (lane == 0 && n_iter > 0) {
+      mbar_arrive_expect_tx(&bars->q_full, kNQ * Lay::kTileBytes);
+      for (int t = 0; t < kNQ; ++t)
+        for (int hf = 0; hf < Lay::kHalves; ++hf)
+          tma_load_3d(smem + Lay::kQ0 + t * Lay::kTileBytes + hf * kHalfBytes, &tmap_q, hf * 64, g * G,
+                      i0 + t * tok_per_tile, &bars->q_full);
       const int64_t layer_rows = p.n_pool_pages * p.hkv * 2 * p.S;
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1;
-        if (j >= 2) mbar_wait(&bars->kv_empty[st], ((j >> 1) - 1) & 1);
+      for (int it = 0; it < n_iter; ++it) {
+        const int j = j_begin + it;
+        const int st = it & 1;
+        if (it >= 2) mbar_wait(&bars->kv_empty[st], ((it >> 1) - 1) & 1);
         uint8_t* ks = smem + Lay::kK0 + st * Lay::kTileBytes;
         uint8_t* vs = smem + Lay::kV0 + st * Lay::kTileBytes;
         mbar_arrive_expect_tx(&bars->k_full[st], Lay::kTileBytes);
@@ -109,166 +158,177 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int pidx = min(j * pages_per_tile + pp, p.n_req_pages - 1);  // clamp: finite, masked
           const int64_t page = p.pages[pidx];
           const int64_t row_k = int64_t(p.layer) * layer_rows + ((page * p.hkv + g) * 2 + 0) * p.S;
-          const int64_t row_v = row_k + p.S;
 #pragma unroll
-          for (int hf = 0; hf < Lay::kHalves; ++hf) {
-            tma_load_2d(ks + hf * kHalfBytes + pp * p.S * 128, &tmap, hf * 64, int32_t(row_k), &bars->k_full[st]);
-            tma_load_2d(vs + hf * kHalfBytes + pp * p.S * 128, &tmap, hf * 64, int32_t(row_v), &bars->v_full[st]);
-          }
+          for (int hf = 0; hf < Lay::kHalves; ++hf)
+            tma_load_2d(ks + hf * kHalfBytes + pp * p.S * 128, &tmap_pool, hf * 64, int32_t(row_k), &bars->k_full[st]);
+#pragma unroll
+          for (int hf = 0; hf < Lay::kHalves; ++hf)
+            tma_load_2d(vs + hf * kHalfBytes + pp * p.S * 128, &tmap_pool, hf * 64, int32_t(row_k + p.S),
+                        &bars->v_full[st]);
         }
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    if (lane == 0 && n_iter > 0) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(kBlockM, kBlockN, 0, 0);
       constexpr uint32_t idesc_o = idesc_bf16_f32(kBlockM, D, 0, 1);
-      const uint32_t q_addr = smem_u32(smem + Lay::kQ);
-      const uint32_t p_addr = smem_u32(smem + Lay::kP);
       mbar_wait(&bars->q_full, 0);
-      auto issue_s = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&bars->k_full[st], (j >> 1) & 1);
-        if (j >= 2) mbar_wait(&bars->s_empty[st], ((j >> 1) - 1) & 1);
-        tc_fence_after();
-        const uint32_t k_addr = smem_u32(smem + Lay::kK0 + st * Lay::kTileBytes);
+      auto issue_s = [&](int t, int it) {
+        const uint32_t q_addr = smem_u32(smem + Lay::kQ0 + t * Lay::kTileBytes);
+        const uint32_t k_addr = smem_u32(smem + Lay::kK0 + (it & 1) * Lay::kTileBytes);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-          mma_bf16_ss(tmem + st * kBlockN, smem_desc_sw128(q_addr + off, 16, 1024),
+          mma_bf16_ss(tmem + Lay::kColS + t * kBlockN, smem_desc_sw128(q_addr + off, 16, 1024),
                       smem_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0);
         }
-        mma_commit(&bars->s_full[st]);
+        mma_commit(&bars->s_full[t]);
       };
-      issue_s(0);
-      for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) issue_s(j + 1);
-        const int st = j & 1;
-        mbar_wait(&bars->p_full, j & 1);
-        mbar_wait(&bars->v_full[st], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t v_addr = smem_u32(smem + Lay::kV0 + st * Lay::kTileBytes);
+      auto issue_pv = [&](int t, int it) {
+        const uint32_t v_addr = smem_u32(smem + Lay::kV0 + (it & 1) * Lay::kTileBytes);
 #pragma unroll
-        for (int kk = 0; kk < kBlockN / 16; ++kk) {
-          const uint32_t poff = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-          mma_bf16_ss(tmem + 2 * kBlockN, smem_desc_sw128(p_addr + poff, 16, 1024),
-                      smem_desc_sw128(v_addr + kk * 2048, kHalfBytes, 1024), idesc_o, (j > 0 || kk > 0));
+        for (int kk = 0; kk < kBlockN / 16; ++kk)
+          mma_bf16_ts(tmem + Lay::kColO + t * D, tmem + Lay::kColS + t * kBlockN + kk * 8,
+                      smem_desc_sw128(v_addr + kk * 2048, kHalfBytes, 1024), idesc_o, (it > 0 || kk > 0));
+      };
+      mbar_wait(&bars->k_full[0], 0);
+      tc_fence_after();
+      for (int t = 0; t < kNQ; ++t) issue_s(t, 0);
+      for (int it = 0; it < n_iter; ++it) {
+        const int st = it & 1;
+        const bool more = it + 1 < n_iter;
+        mbar_wait(&bars->v_full[st], (it >> 1) & 1);
+        if (more) mbar_wait(&bars->k_full[st ^ 1], ((it + 1) >> 1) & 1);
+        for (int t = 0; t < kNQ; ++t) {
+          mbar_wait(&bars->p_full[t], it & 1);
+          tc_fence_after();
+          issue_pv(t, it);
+          if (t == kNQ - 1) mma_commit(&bars->kv_empty[st]);
+          if (more) issue_s(t, it + 1);
         }
-        mma_commit(&bars->o_done);
-        mma_commit(&bars->kv_empty[st]);
       }
+      mma_commit(&bars->o_full);
     }
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- softmax / epilogue
-    const int r = threadIdx.x - 128;             // M row == TMEM lane
-    const int i = i0 + r / G;                     // suffix token of this row
-    const int qh = g * G + (r % G);               // local query head
-    const uint32_t lane_addr = tmem + (uint32_t((warp & 3) * 32) << 16);
-    {
-      uint8_t* qs = smem + Lay::kQ;
-      const uint4* src = reinterpret_cast<const uint4*>(p.q + (int64_t(i) * p.hq + qh) * D);
-#pragma unroll
-      for (int c16 = 0; c16 < D / 8; ++c16) {
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (i < p.n2) v = src[c16];
-        const int hf = c16 >> 3, cc = c16 & 7;
-        *reinterpret_cast<uint4*>(qs + hf * kHalfBytes + r * 128 + ((cc ^ (r & 7)) << 4)) = v;
-      }
-      fence_proxy_async_smem();
-      mbar_arrive(&bars->q_full);
-    }
-    const int limit = p.n1 + i;                   // last visible key of this row
-    float m = -INFINITY, l = 0.f;
-    uint8_t* ps = smem + Lay::kP;
-    for (int j = 0; j < n_tiles; ++j) {
-      const int st = j & 1;
-      mbar_wait(&bars->s_full[st], (j >> 1) & 1);
+    const int t = (warp - 4) >> 2;              // Q tile of this warpgroup
+    const int r = threadIdx.x - 128 * (1 + t);   // row within the tile == TMEM lane
+    const int i = i0 + t * tok_per_tile + r / G; // suffix token of this row
+    const int qh = g * G + (r % G);              // local query head
+    const uint32_t lane_base = tmem + (uint32_t((warp & 3) * 32) << 16);
+    const uint32_t s_col = lane_base + Lay::kColS + t * kBlockN;
+    const uint32_t o_col = lane_base + Lay::kColO + t * D;
+    const int limit = p.n1 + i;  // last visible key of this row
+    const int tile_first_key_limit = p.n1 + i0 + t * tok_per_tile;
+    float m_raw = -INFINITY, l = 0.f;
+    for (int it = 0; it < n_iter; ++it) {
+      const int key0 = (j_begin + it) * kBlockN;
+      const bool diag = key0 + kBlockN - 1 > tile_first_key_limit;  // tile crosses this Q tile's diagonal
+      mbar_wait(&bars->s_full[t], it & 1);
       tc_fence_after();
-      float s[kBlockN];
-#pragma unroll
-      for (int c = 0; c < kBlockN / 32; ++c) tmem_ld32(lane_addr + st * kBlockN + c * 32, s + c * 32);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&bars->s_empty[st]);
-      const int key0 = j * kBlockN;
+      // pass 1: row max, streaming S from TMEM 32 columns at a time (TMEM reads are cheap; this
+      // keeps the softmax at ~90 registers so a gather CTA can co-reside on the SM)
       float rowmax = -INFINITY;
-      if (key0 + kBlockN - 1 > p.n1 + i0) {       // diagonal tile(s): causal mask
 #pragma unroll
-        for (int c = 0; c < kBlockN; ++c) {
-          s[c] = (key0 + c <= limit) ? s[c] * p.scale_log2 : -INFINITY;
-          rowmax = fmaxf(rowmax, s[c]);
-        }
-      } else {
+      for (int c = 0; c < kBlockN / 32; ++c) {
+        float v[32];
+        tmem_ld32(s_col + c * 32, v);
+        tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < kBlockN; ++c) {
-          s[c] *= p.scale_log2;
-          rowmax = fmaxf(rowmax, s[c]);
+        for (int e = 0; e < 32; ++e)
+          rowmax = fmaxf(rowmax, (!diag || key0 + c * 32 + e <= limit) ? v[e] : -INFINITY);
+      }
+      const float m_new = fmaxf(m_raw, rowmax);
+      const bool rescale = (m_new - m_raw) * p.scale_log2 > kRescaleThreshold;
+      const float m_use = rescale ? m_new : m_raw;
+      const float neg_m = -m_use * p.scale_log2;
+      const float alpha = ex2(fmaf(m_raw, p.scale_log2, neg_m));
+      // O_t(j-1) is complete here (in-order MMA completion, see header): rescale if needed.
+      if (it > 0 && __any_sync(0xffffffffu, rescale)) {
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          float o[32];
+          tmem_ld32(o_col + c * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] *= alpha;
+          tmem_st32(o_col + c * 32, o);
         }
       }
-      const float m_new = fmaxf(m, rowmax);
-      const float m_use = (m_new > m + kRescaleThreshold) ? m_new : m;
-      const float alpha = ex2(m - m_use);
+      // pass 2: P = bf16(2^(s*scale - m)) written over the S columns it was computed from
+      // (P chunk c -> columns [16c, 16c+16), all of which were already read).
       float rowsum = 0.f;
-      uint32_t pk[kBlockN / 2];
 #pragma unroll
-      for (int c = 0; c < kBlockN; c += 2) {
-        const float e0 = ex2(s[c] - m_use), e1 = ex2(s[c + 1] - m_use);
-        __nv_bfloat162 b = __floats2bfloat162_rn(e0, e1);
-        // l sums the SAME bf16-rounded weights the PV product uses, so out = sum(w v)/sum(w)
-        // is an exact convex combination of V rows (no numerator/denominator mismatch).
-        rowsum += __low2float(b) + __high2float(b);
-        pk[c / 2] = *reinterpret_cast<uint32_t*>(&b);
+      for (int c = 0; c < kBlockN / 32; ++c) {
+        float v[32];
+        tmem_ld32(s_col + c * 32, v);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float x0 = (!diag || key0 + c * 32 + e <= limit) ? fmaf(v[e], p.scale_log2, neg_m) : -INFINITY;
+          const float x1 = (!diag || key0 + c * 32 + e + 1 <= limit) ? fmaf(v[e + 1], p.scale_log2, neg_m) : -INFINITY;
+          pk[e / 2] = pack_bf16(ex2(x0), ex2(x1), rowsum);
+        }
+        tmem_st16(s_col + c * 16, pk);
       }
       l = l * alpha + rowsum;
-      if (j > 0) {
-        mbar_wait(&bars->o_done, (j - 1) & 1);   // PV(j-1) done: O stable, P buffer free
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, m_use != m)) {
-          float o[32];
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            tmem_ld32(lane_addr + 2 * kBlockN + c * 32, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] *= alpha;
-            tmem_st32(lane_addr + 2 * kBlockN + c * 32, o);
-          }
-          tmem_st_wait();
-        }
-      }
-#pragma unroll
-      for (int c16 = 0; c16 < kBlockN / 8; ++c16) {
-        const int hf = c16 >> 3, cc = c16 & 7;
-        *reinterpret_cast<uint4*>(ps + hf * kHalfBytes + r * 128 + ((cc ^ (r & 7)) << 4)) =
-            make_uint4(pk[c16 * 4 + 0], pk[c16 * 4 + 1], pk[c16 * 4 + 2], pk[c16 * 4 + 3]);
-      }
-      fence_proxy_async_smem();
+      tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&bars->p_full);
-      m = m_use;
+      mbar_arrive(&bars->p_full[t]);
+      m_raw = m_use;
     }
     // ---------------------------------------------------------------- epilogue
-    mbar_wait(&bars->o_done, (n_tiles - 1) & 1);
-    tc_fence_after();
-    const float inv_l = 1.f / l;
-    uint4* dst = reinterpret_cast<uint4*>(p.out + (int64_t(i) * p.hq + qh) * D);
+    const bool row_ok = i < p.n2;
+    const int64_t row_id = int64_t(i) * p.hq + qh;
+    if (n_iter > 0) {
+      mbar_wait(&bars->o_full, 0);
+      tc_fence_after();
+    }
+    const float inv_l = n_iter > 0 ? 1.f / l : 0.f;
+    if (p.n_splits == 1) {
+      uint4* dst = reinterpret_cast<uint4*>(p.out + row_id * D);
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      float o[32];
-      tmem_ld32(lane_addr + 2 * kBlockN + c * 32, o);
-      tmem_ld_wait();
-      if (i < p.n2) {
+      for (int c = 0; c < D / 32; ++c) {
+        float o[32];
+        tmem_ld32(o_col + c * 32, o);
+        tmem_ld_wait();
+        if (row_ok) {
 #pragma unroll
-        for (int q8 = 0; q8 < 4; ++q8) {
-          uint32_t w[4];
+          for (int q8 = 0; q8 < 4; ++q8) {
+            uint32_t w[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            __nv_bfloat162 b = __floats2bfloat162_rn(o[q8 * 8 + 2 * e] * inv_l, o[q8 * 8 + 2 * e + 1] * inv_l);
-            w[e] = *reinterpret_cast<uint32_t*>(&b);
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 b = __floats2bfloat162_rn(o[q8 * 8 + 2 * e] * inv_l, o[q8 * 8 + 2 * e + 1] * inv_l);
+              w[e] = *reinterpret_cast<uint32_t*>(&b);
+            }
+            dst[c * 4 + q8] = make_uint4(w[0], w[1], w[2], w[3]);
           }
-          dst[c * 4 + q8] = make_uint4(w[0], w[1], w[2], w[3]);
         }
       }
+    } else {
+      // split-KV partial: normalised O of this key range + its log2-domain LSE
+      const int64_t rows_total = int64_t(p.n2) * p.hq;
+      float4* dst = reinterpret_cast<float4*>(p.ws_o + (int64_t(blockIdx.z) * rows_total + row_id) * D);
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        float o[32];
+        if (n_iter > 0) {
+          tmem_ld32(o_col + c * 32, o);
+          tmem_ld_wait();
+        }
+        if (row_ok) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            dst[c * 8 + e] = n_iter > 0 ? make_float4(o[4 * e] * inv_l, o[4 * e + 1] * inv_l, o[4 * e + 2] * inv_l,
+                                                      o[4 * e + 3] * inv_l)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      if (row_ok)
+        p.ws_lse[int64_t(blockIdx.z) * rows_total + row_id] =
+            n_iter > 0 ? m_raw * p.scale_log2 + __log2f(l) : -INFINITY;
     }
     tc_fence_before();
   }
@@ -279,8 +339,55 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Merge split-KV partials: out = sum_s 2^(lse_s - M) O_s / sum_s 2^(lse_s - M), M = max_s lse_s.
 template <int D>
-cudaError_t launch_d(const CUtensorMap* tmap, const AttnParams& p, cudaStream_t stream) {
+__global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
+                                                      uint16_t* __restrict__ out, int64_t rows_total, int n_splits) {
+  constexpr int kVec = D / 8;  // 8 outputs (one 16-byte store) per thread
+  const int64_t n = rows_total * kVec;
+  for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < n; u += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = u / kVec;
+    const int c8 = int(u % kVec) * 8;
+    float mx = -INFINITY;
+    for (int s = 0; s < n_splits; ++s) mx = fmaxf(mx, ws_lse[s * rows_total + row]);
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, wsum = 0.f;
+    for (int s = 0; s < n_splits; ++s) {
+      const float w = ex2(ws_lse[s * rows_total + row] - mx);
+      wsum += w;
+      const float4* src = reinterpret_cast<const float4*>(ws_o + (s * rows_total + row) * D + c8);
+      const float4 a = src[0], b = src[1];
+      acc[0] += w * a.x; acc[1] += w * a.y; acc[2] += w * a.z; acc[3] += w * a.w;
+      acc[4] += w * b.x; acc[5] += w * b.y; acc[6] += w * b.z; acc[7] += w * b.w;
+    }
+    const float inv = 1.f / wsum;
+    uint32_t wv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      __nv_bfloat162 b = __floats2bfloat162_rn(acc[2 * e] * inv, acc[2 * e + 1] * inv);
+      wv[e] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    *reinterpret_cast<uint4*>(out + row * D + c8) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+  }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  }
+  return fn;
+}
+
+template <int D>
+cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStream_t stream, int* launches) {
   static bool configured = false;
   auto kern = suffix_attn_kernel<D>;
   if (!configured) {
@@ -288,19 +395,56 @@ cudaError_t launch_d(const CUtensorMap* tmap, const AttnParams& p, cudaStream_t 
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  AttnParams p = p0;
   const int G = p.hq / p.hkv;
-  const int tok_per_tile = kBlockM / G;
-  dim3 grid((p.n2 + tok_per_tile - 1) / tok_per_tile, p.hkv);
-  kern<<<grid, kThreads, Layout<D>::kAlloc, stream>>>(*tmap, p);
-  return cudaGetLastError();
+  // Q tensor map over q [N2][Hq][D]: box {64, G, 128/G} lands a Q tile as rows r = t*G + gg.
+  CUtensorMap tmap_q;
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  cuuint64_t dims[3] = {cuuint64_t(D), cuuint64_t(p.hq), cuuint64_t(p.n2)};
+  cuuint64_t strides[2] = {cuuint64_t(D) * 2, cuuint64_t(p.hq) * D * 2};
+  cuuint32_t box[3] = {64, cuuint32_t(G), cuuint32_t(kBlockM / G)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  if (enc(&tmap_q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(p.q), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  const int tok_per_cta = kNQ * kBlockM / G;
+  const int n_mblocks = (p.n2 + tok_per_cta - 1) / tok_per_cta;
+  // Split-KV when the (m-block x kv-head) grid leaves SMs idle; each split keeps >= 2 key tiles.
+  const int ctas = n_mblocks * p.hkv;
+  const int max_tiles = (p.n1 + p.n2 + kBlockN - 1) / kBlockN;
+  int splits = 1;
+  if (p.ws_o && ctas < 148) {
+    splits = (148 + ctas - 1) / ctas;
+    splits = std::min(splits, std::max(1, max_tiles / 2));
+    const int64_t per_split_bytes = int64_t(p.n2) * p.hq * (D + 1) * 4;
+    splits = int(std::min<int64_t>(splits, std::max<int64_t>(1, p.ws_bytes / per_split_bytes)));
+  }
+  p.n_splits = splits;
+  dim3 grid(n_mblocks, p.hkv, splits);
+  kern<<<grid, kThreads, Layout<D>::kAlloc, stream>>>(*tmap_pool, tmap_q, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  *launches += 1;
+  if (splits > 1) {
+    const int64_t rows_total = int64_t(p.n2) * p.hq;
+    int64_t blocks = (rows_total * (D / 8) + 255) / 256;
+    blocks = std::min<int64_t>(blocks, 148 * 8);
+    combine_kernel<D><<<int(blocks), 256, 0, stream>>>(p.ws_o, p.ws_lse, p.out, rows_total, splits);
+    e = cudaGetLastError();
+    *launches += 1;
+  }
+  return e;
 }
 
 }  // namespace
 
-cudaError_t launch_suffix_attn(const CUtensorMap* tmap, const AttnParams& p, int32_t d, cudaStream_t stream) {
+cudaError_t launch_suffix_attn(const CUtensorMap* tmap_pool, const AttnParams& p, int32_t d, cudaStream_t stream,
+                               int* launches) {
   if (p.n2 <= 0) return cudaSuccess;
-  if (d == 128) return launch_d<128>(tmap, p, stream);
-  if (d == 64) return launch_d<64>(tmap, p, stream);
+  if (d == 128) return launch_d<128>(tmap_pool, p, stream, launches);
+  if (d == 64) return launch_d<64>(tmap_pool, p, stream, launches);
   return cudaErrorInvalidValue;
 }
 

@@ -46,6 +46,9 @@ struct pcr_ctx {
   int64_t launches = 0;
   pcr::KvGeom geom{};
   int32_t gather_ctas = 16;
+  // split-KV workspace: ws_floats partial-O floats followed by ws_floats/d LSE floats
+  float* ws = nullptr;
+  int64_t ws_floats = 0;
 };
 
 namespace {
@@ -170,8 +173,13 @@ pcr_status enqueue_attn(pcr_ctx* c, Request* r, int32_t layer, const void* q, co
   p.n_req_pages = n_pages;
   p.n_pool_pages = c->n_pool_pages;
   p.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(c->cfg.head_dim));
-  CUDA_TRY(c, pcr::launch_suffix_attn(&c->tmap, p, c->cfg.head_dim, s));
-  c->launches += 2;
+  p.ws_o = c->ws;
+  p.ws_lse = c->ws ? c->ws + c->ws_floats : nullptr;
+  p.ws_bytes = c->ws_floats * 4;
+  int n = 0;
+  cudaError_t e = pcr::launch_suffix_attn(&c->tmap, p, c->cfg.head_dim, s, &n);
+  c->launches += 1 + n;
+  if (e != cudaSuccess) return cuda_fail(c, e, "launch_suffix_attn");
   return PCR_OK;
 }
 
@@ -254,6 +262,10 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
       if (e == cudaSuccess) cp->ev_load.push_back(ev);
     }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cp->ev_join, cudaEventDisableTiming);
+    if (e == cudaSuccess) {
+      cp->ws_floats = (int64_t(32) << 20) / 4;  // 32 MiB of partial O (+ LSE)
+      e = cudaMalloc(reinterpret_cast<void**>(&cp->ws), (cp->ws_floats + cp->ws_floats / 64 + 64) * 4);
+    }
     for (int l = 0; e == cudaSuccess && l < 4 * k.n_layers; ++l) {
       cudaEvent_t ev;
       e = cudaEventCreate(&ev);
@@ -287,6 +299,7 @@ void pcr_destroy(pcr_ctx* c) {
     for (auto e : c->ev_t) cudaEventDestroy(e);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->d_arena) cudaFree(c->d_arena);
+    if (c->ws) cudaFree(c->ws);
     if (c->h_arena) cudaFreeHost(c->h_arena);
     if (c->registered) cudaHostUnregister(c->store);
   } else {
