@@ -210,7 +210,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2603_23049_b200 import MODE_OVERLAP, MODE_SYNC, Context
+    from paper_2603_23049_b200 import MODE_OVERLAP, MODE_SYNC, Context, comm_unique_id
     from pcrgen import make_rng, randn_bf16
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -259,7 +259,15 @@ def run_ours(args):
     v_h = randn_bf16(rng, (L, N2, hkv, d))
     q_d, k_d, v_d = dev(q_h), dev(k_h), dev(v_h)
     out_d = torch.empty_like(q_d)
-    gathered = torch.empty((world,) + tuple(out_d.shape), dtype=out_d.dtype, device="cuda") if world > 1 else None
+    # N > 1: the library re-assembles each layer's head-sharded output with an NCCL all-gather on
+    # a comm stream, overlapped with the next layer (pcr_run_prefill_sharded)
+    gathered, xs = None, None
+    if world > 1:
+        uid = [comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.comm_init(uid[0])
+        gathered = torch.empty((L, world) + tuple(out_d.shape[1:]), dtype=out_d.dtype, device="cuda")
+        xs = torch.cuda.Stream()
     # the load stream gets the highest priority: its few gather CTAs are scheduled ahead of the
     # attention grid's CTAs whenever an SM slot frees up
     cs, ls = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
@@ -278,12 +286,12 @@ def run_ours(args):
         assert plan["n1"] == N1, plan["n1"]
         if load_events:
             load_events[0].record(ls)
-        t = ctx.run_prefill(rid, q, k, v, out, cs, ls, mode=mode, layer_times=times)
+        if world > 1:
+            t = ctx.run_prefill_sharded(rid, q, k, v, out, gathered, cs, ls, xs, mode=mode, layer_times=times)
+        else:
+            t = ctx.run_prefill(rid, q, k, v, out, cs, ls, mode=mode, layer_times=times)
         if load_events:
             load_events[1].record(ls)
-        if world > 1:
-            with torch.cuda.stream(cs):
-                dist.all_gather_into_tensor(gathered, out)
         cs.synchronize()
         # No offload stream yet: the request's newly reserved chunks have no KV
         # written, so they are dropped instead of committed; the cached prefix stays resident.
@@ -339,7 +347,8 @@ def run_ours(args):
         q_p = torch.from_numpy(q_h.view(np.int16)).pin_memory()
         k_p = torch.from_numpy(k_h.view(np.int16)).pin_memory()
         v_p = torch.from_numpy(v_h.view(np.int16)).pin_memory()
-        o_p = torch.empty(q_p.shape, dtype=torch.int16).pin_memory()
+        res = gathered if world > 1 else None   # the step's result: full (re-assembled) output
+        o_p = torch.empty(tuple(res.shape) if res is not None else q_p.shape, dtype=torch.int16).pin_memory()
         q2, k2, v2, o2 = (torch.empty_like(q_d), torch.empty_like(k_d), torch.empty_like(v_d),
                           torch.empty_like(out_d))
         if world > 1:
@@ -356,7 +365,7 @@ def run_ours(args):
             ls.wait_stream(cs)
             step(q2, k2, v2, o2)
             with torch.cuda.stream(cs):
-                o_p.copy_(o2, non_blocking=True)
+                o_p.copy_(res if res is not None else o2, non_blocking=True)
             cs.synchronize()
         b.record(cs)
         b.synchronize()

@@ -204,6 +204,28 @@ pcr_status pcr_run_prefill(pcr_ctx* ctx, int64_t req_id, const void* q_all, cons
                            const void* v_all, void* out_all, void* compute_stream,
                            void* load_stream, int32_t mode, float* layer_times_ms);
 
+/* ---------------------------------------------------------------- multi-GPU (§8(e)) - */
+
+/* KV-head sharding: every rank runs the same request on its head slice (pcr_config.rank /
+ * world) and the attention outputs are re-assembled with one NCCL all-gather per layer
+ * (north_star: "NCCL is used only where outputs must be re-assembled").  NCCL is loaded
+ * at run time (dlopen "libnccl.so.2"); nothing else in the library depends on it.
+ * pcr_comm_unique_id: ncclGetUniqueId into out[128] (call on one rank, broadcast the bytes).
+ * pcr_comm_init: ncclCommInitRank(world, id, rank) for this ctx (collective over ranks).
+ * PCR_E_UNSUPPORTED if NCCL cannot be loaded; PCR_E_CUDA on an NCCL error. */
+pcr_status pcr_comm_unique_id(uint8_t* out);
+pcr_status pcr_comm_init(pcr_ctx* ctx, const uint8_t* id);
+
+/* pcr_run_prefill plus, per layer, after attn(l): comm_stream waits for it and runs
+ * ncclAllGather(out_l -> gathered_l), so the gather of layer l overlaps the work of layer l+1.
+ * gathered_all = [L][world][N2][Hq_loc][d] (rank-major; rank r's block holds query heads
+ * [r*Hq/world, (r+1)*Hq/world)).  compute_stream is joined after the last all-gather.
+ * PCR_E_STATE if pcr_comm_init has not been called. */
+pcr_status pcr_run_prefill_sharded(pcr_ctx* ctx, int64_t req_id, const void* q_all, const void* k_all,
+                                   const void* v_all, void* out_all, void* gathered_all,
+                                   void* compute_stream, void* load_stream, void* comm_stream,
+                                   int32_t mode, float* layer_times_ms);
+
 /* Count of kernels launched by this ctx since creation (bench `gpu_launches`). */
 int64_t pcr_kernel_launches(const pcr_ctx* ctx);
 

@@ -26,9 +26,10 @@ SOURCES = [
     "host/planner.cpp",
     "kernels/kv_copy.cu",
     "kernels/suffix_attn.cu",
+    "runtime/nccl_dl.cpp",
     "runtime/capi.cu",
 ]
-HEADERS = ["host/blake2b.h", "host/planner.h", "kernels/kernels.h", "kernels/sm100_ptx.cuh"]
+HEADERS = ["host/blake2b.h", "host/planner.h", "kernels/kernels.h", "kernels/sm100_ptx.cuh", "runtime/nccl_dl.h"]
 
 
 def _mtime(p):
@@ -52,7 +53,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
     if force or _mtime(LIB) < max(_mtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lpthread"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lpthread", "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

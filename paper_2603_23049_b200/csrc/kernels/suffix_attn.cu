@@ -92,8 +92,10 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b, float& sum) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// 136 registers x 384 threads = 52K of the SM's 64K: a 256-thread gather CTA (10K) still fits
+// beside an attention CTA, so layer l+1's host->HBM load never waits for attention SMs.
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __maxnreg__(136)
     suffix_attn_kernel(const __grid_constant__ CUtensorMap tmap_pool, const __grid_constant__ CUtensorMap tmap_q,
                        const AttnParams p) {
   using Lay = Layout<D>;
@@ -221,28 +223,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t o_col = lane_base + Lay::kColO + t * D;
     const int limit = p.n1 + i;  // last visible key of this row
     const int tile_first_key_limit = p.n1 + i0 + t * tok_per_tile;
+    // Two passes over S in TMEM, 32 columns at a time (TMEM reads are cheap; this keeps the
+    // softmax at <= 136 registers so a gather CTA can co-reside): (1) row max with the 3-input
+    // FMNMX3; (2) P = bf16(2^(s*scale - m)) via FFMA2 + ex2, written over the S columns it came
+    // from (P chunk c -> columns [16c, 16c+16), all already read), row sum via FADD2.
     float m_raw = -INFINITY, l = 0.f;
+    const uint64_t scale2 = f2_pack(p.scale_log2, p.scale_log2);
     for (int it = 0; it < n_iter; ++it) {
       const int key0 = (j_begin + it) * kBlockN;
       const bool diag = key0 + kBlockN - 1 > tile_first_key_limit;  // tile crosses this Q tile's diagonal
       mbar_wait(&bars->s_full[t], it & 1);
       tc_fence_after();
-      // pass 1: row max, streaming S from TMEM 32 columns at a time (TMEM reads are cheap; this
-      // keeps the softmax at ~90 registers so a gather CTA can co-reside on the SM)
       float rowmax = -INFINITY;
 #pragma unroll
       for (int c = 0; c < kBlockN / 32; ++c) {
         float v[32];
         tmem_ld32(s_col + c * 32, v);
         tmem_ld_wait();
+        if (diag) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
-          rowmax = fmaxf(rowmax, (!diag || key0 + c * 32 + e <= limit) ? v[e] : -INFINITY);
+          for (int e = 0; e < 32; ++e) v[e] = (key0 + c * 32 + e <= limit) ? v[e] : -INFINITY;
+        }
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) rowmax = fmax3(rowmax, v[e], v[e + 1]);
       }
       const float m_new = fmaxf(m_raw, rowmax);
       const bool rescale = (m_new - m_raw) * p.scale_log2 > kRescaleThreshold;
       const float m_use = rescale ? m_new : m_raw;
       const float neg_m = -m_use * p.scale_log2;
+      const uint64_t negm2 = f2_pack(neg_m, neg_m);
       const float alpha = ex2(fmaf(m_raw, p.scale_log2, neg_m));
       // O_t(j-1) is complete here (in-order MMA completion, see header): rescale if needed.
       if (it > 0 && __any_sync(0xffffffffu, rescale)) {
@@ -256,24 +265,32 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st32(o_col + c * 32, o);
         }
       }
-      // pass 2: P = bf16(2^(s*scale - m)) written over the S columns it was computed from
-      // (P chunk c -> columns [16c, 16c+16), all of which were already read).
-      float rowsum = 0.f;
+      uint64_t sum2 = 0;
 #pragma unroll
       for (int c = 0; c < kBlockN / 32; ++c) {
         float v[32];
         tmem_ld32(s_col + c * 32, v);
         tmem_ld_wait();
+        if (diag) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = (key0 + c * 32 + e <= limit) ? v[e] : -INFINITY;
+        }
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          const float x0 = (!diag || key0 + c * 32 + e <= limit) ? fmaf(v[e], p.scale_log2, neg_m) : -INFINITY;
-          const float x1 = (!diag || key0 + c * 32 + e + 1 <= limit) ? fmaf(v[e + 1], p.scale_log2, neg_m) : -INFINITY;
-          pk[e / 2] = pack_bf16(ex2(x0), ex2(x1), rowsum);
+          float x0, x1;
+          f2_unpack(ffma2(f2_pack(v[e], v[e + 1]), scale2, negm2), x0, x1);
+          __nv_bfloat162 b = __floats2bfloat162_rn(ex2(x0), ex2(x1));
+          const uint32_t w = *reinterpret_cast<uint32_t*>(&b);
+          pk[e / 2] = w;
+          // row sum of the same bf16-rounded weights (R18), two lanes per FADD2
+          sum2 = fadd2(sum2, f2_pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u)));
         }
         tmem_st16(s_col + c * 16, pk);
       }
-      l = l * alpha + rowsum;
+      float s0, s1;
+      f2_unpack(sum2, s0, s1);
+      l = l * alpha + (s0 + s1);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars->p_full[t]);

@@ -17,6 +17,7 @@
 #include "../host/blake2b.h"
 #include "../host/planner.h"
 #include "../kernels/kernels.h"
+#include "nccl_dl.h"
 
 using pcr::Planner;
 using pcr::Request;
@@ -49,6 +50,10 @@ struct pcr_ctx {
   // split-KV workspace: ws_floats partial-O floats followed by ws_floats/d LSE floats
   float* ws = nullptr;
   int64_t ws_floats = 0;
+  // multi-GPU output re-assembly (§8(e))
+  void* nccl_comm = nullptr;
+  std::vector<cudaEvent_t> ev_attn;
+  cudaEvent_t ev_comm = nullptr;
 };
 
 namespace {
@@ -183,6 +188,72 @@ pcr_status enqueue_attn(pcr_ctx* c, Request* r, int32_t layer, const void* q, co
   return PCR_OK;
 }
 
+
+pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const void* k_all, const void* v_all,
+                            void* out_all, void* gathered_all, void* compute_stream, void* load_stream,
+                            void* comm_stream, int32_t mode, float* layer_times_ms) {
+  if (!c) return PCR_E_INVAL;
+  pcr_status st = device_ready(c);
+  if (st != PCR_OK) return st;
+  Request* r = planned_request(c, req_id, &st);
+  if (!r) return st;
+  if (!q_all || !k_all || !v_all || !out_all) return fail(c, PCR_E_INVAL, "null q/k/v/out");
+  if (mode != 0 && mode != 1) return fail(c, PCR_E_INVAL, "mode must be 0 (OVERLAP) or 1 (SYNC)");
+  cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
+  cudaStream_t ls = mode == 0 ? static_cast<cudaStream_t>(load_stream) : cs;
+  cudaStream_t xs = static_cast<cudaStream_t>(comm_stream);
+  if (mode == 0 && load_stream == compute_stream)
+    return fail(c, PCR_E_INVAL, "OVERLAP mode needs two distinct streams");
+  const int64_t n2 = r->plan.n2;
+  const int64_t q_layer = n2 * c->hq * c->cfg.head_dim, kv_layer = n2 * c->hkv * c->cfg.head_dim;
+  const bool timed = layer_times_ms != nullptr;
+  const pcr::NcclApi* api = gathered_all ? pcr::nccl_api() : nullptr;
+  if (gathered_all && !api) return fail(c, PCR_E_UNSUPPORTED, "libnccl.so.2 not loadable");
+  if ((st = ensure_tables(c, r, ls)) != PCR_OK) return st;
+  if (mode == 0) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->region_ev[r->plan.region], 0));
+  for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
+    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 0], ls));
+    if ((st = enqueue_gather(c, r, l, ls)) != PCR_OK) return st;
+    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 1], ls));
+    if (mode == 0) {
+      CUDA_TRY(c, cudaEventRecord(c->ev_load[l], ls));
+      CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_load[l], 0));
+    }
+    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 2], cs));
+    uint16_t* out_l = static_cast<uint16_t*>(out_all) + l * q_layer;
+    st = enqueue_attn(c, r, l, static_cast<const uint16_t*>(q_all) + l * q_layer,
+                      static_cast<const uint16_t*>(k_all) + l * kv_layer,
+                      static_cast<const uint16_t*>(v_all) + l * kv_layer, out_l, cs);
+    if (st != PCR_OK) return st;
+    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 3], cs));
+    if (gathered_all) {
+      // re-assemble this layer's head-sharded output on the comm stream while layer l+1 runs
+      CUDA_TRY(c, cudaEventRecord(c->ev_attn[l], cs));
+      CUDA_TRY(c, cudaStreamWaitEvent(xs, c->ev_attn[l], 0));
+      const size_t bytes = static_cast<size_t>(q_layer) * 2;
+      int rr = api->all_gather(out_l, static_cast<uint8_t*>(gathered_all) + bytes * c->cfg.world * l, bytes,
+                               /*ncclInt8*/ 0, c->nccl_comm, xs);
+      if (rr != 0) return fail(c, PCR_E_CUDA, "ncclAllGather failed");
+    }
+  }
+  if (mode == 0) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_join, ls));
+    CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_join, 0));
+  }
+  if (gathered_all) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_comm, xs));
+    CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_comm, 0));
+  }
+  if (timed) {
+    CUDA_TRY(c, cudaStreamSynchronize(cs));
+    for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
+      CUDA_TRY(c, cudaEventElapsedTime(&layer_times_ms[2 * l], c->ev_t[4 * l + 0], c->ev_t[4 * l + 1]));
+      CUDA_TRY(c, cudaEventElapsedTime(&layer_times_ms[2 * l + 1], c->ev_t[4 * l + 2], c->ev_t[4 * l + 3]));
+    }
+  }
+  return PCR_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -262,6 +333,12 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
       if (e == cudaSuccess) cp->ev_load.push_back(ev);
     }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cp->ev_join, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cp->ev_comm, cudaEventDisableTiming);
+    for (int l = 0; e == cudaSuccess && l < k.n_layers; ++l) {
+      cudaEvent_t ev;
+      e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e == cudaSuccess) cp->ev_attn.push_back(ev);
+    }
     if (e == cudaSuccess) {
       cp->ws_floats = (int64_t(32) << 20) / 4;  // 32 MiB of partial O (+ LSE)
       e = cudaMalloc(reinterpret_cast<void**>(&cp->ws), (cp->ws_floats + cp->ws_floats / 64 + 64) * 4);
@@ -298,6 +375,11 @@ void pcr_destroy(pcr_ctx* c) {
     for (auto e : c->ev_load) cudaEventDestroy(e);
     for (auto e : c->ev_t) cudaEventDestroy(e);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+    for (auto e : c->ev_attn) cudaEventDestroy(e);
+    if (c->nccl_comm) {
+      if (const pcr::NcclApi* api = pcr::nccl_api()) api->comm_destroy(c->nccl_comm);
+    }
     if (c->d_arena) cudaFree(c->d_arena);
     if (c->ws) cudaFree(c->ws);
     if (c->h_arena) cudaFreeHost(c->h_arena);
@@ -421,49 +503,44 @@ pcr_status pcr_prefill_attn_layer(pcr_ctx* c, int64_t req_id, int32_t layer, con
 pcr_status pcr_run_prefill(pcr_ctx* c, int64_t req_id, const void* q_all, const void* k_all, const void* v_all,
                            void* out_all, void* compute_stream, void* load_stream, int32_t mode,
                            float* layer_times_ms) {
+  return run_prefill_impl(c, req_id, q_all, k_all, v_all, out_all, nullptr, compute_stream, load_stream, nullptr,
+                          mode, layer_times_ms);
+}
+
+pcr_status pcr_run_prefill_sharded(pcr_ctx* c, int64_t req_id, const void* q_all, const void* k_all,
+                                   const void* v_all, void* out_all, void* gathered_all, void* compute_stream,
+                                   void* load_stream, void* comm_stream, int32_t mode, float* layer_times_ms) {
   if (!c) return PCR_E_INVAL;
+  if (!c->nccl_comm) return fail(c, PCR_E_STATE, "pcr_run_prefill_sharded: call pcr_comm_init first");
+  if (!gathered_all || !comm_stream) return fail(c, PCR_E_INVAL, "null gathered_all or comm_stream");
+  return run_prefill_impl(c, req_id, q_all, k_all, v_all, out_all, gathered_all, compute_stream, load_stream,
+                          comm_stream, mode, layer_times_ms);
+}
+
+pcr_status pcr_comm_unique_id(uint8_t* out) {
+  if (!out) return PCR_E_INVAL;
+  const pcr::NcclApi* api = pcr::nccl_api();
+  if (!api) return PCR_E_UNSUPPORTED;
+  pcr::NcclApi::UniqueId id;
+  if (api->get_unique_id(&id) != 0) return PCR_E_CUDA;
+  std::memcpy(out, id.internal, 128);
+  return PCR_OK;
+}
+
+pcr_status pcr_comm_init(pcr_ctx* c, const uint8_t* id) {
+  if (!c || !id) return c ? fail(c, PCR_E_INVAL, "pcr_comm_init: null id") : PCR_E_INVAL;
   pcr_status st = device_ready(c);
   if (st != PCR_OK) return st;
-  Request* r = planned_request(c, req_id, &st);
-  if (!r) return st;
-  if (!q_all || !k_all || !v_all || !out_all) return fail(c, PCR_E_INVAL, "null q/k/v/out");
-  if (mode != 0 && mode != 1) return fail(c, PCR_E_INVAL, "mode must be 0 (OVERLAP) or 1 (SYNC)");
-  cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
-  cudaStream_t ls = mode == 0 ? static_cast<cudaStream_t>(load_stream) : cs;
-  if (mode == 0 && load_stream == compute_stream)
-    return fail(c, PCR_E_INVAL, "OVERLAP mode needs two distinct streams");
-  const int64_t n2 = r->plan.n2;
-  const int64_t q_layer = n2 * c->hq * c->cfg.head_dim, kv_layer = n2 * c->hkv * c->cfg.head_dim;
-  const bool timed = layer_times_ms != nullptr;
-  if ((st = ensure_tables(c, r, ls)) != PCR_OK) return st;
-  if (mode == 0) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->region_ev[r->plan.region], 0));
-  for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
-    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 0], ls));
-    if ((st = enqueue_gather(c, r, l, ls)) != PCR_OK) return st;
-    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 1], ls));
-    if (mode == 0) {
-      CUDA_TRY(c, cudaEventRecord(c->ev_load[l], ls));
-      CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_load[l], 0));
-    }
-    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 2], cs));
-    st = enqueue_attn(c, r, l, static_cast<const uint16_t*>(q_all) + l * q_layer,
-                      static_cast<const uint16_t*>(k_all) + l * kv_layer,
-                      static_cast<const uint16_t*>(v_all) + l * kv_layer, static_cast<uint16_t*>(out_all) + l * q_layer,
-                      cs);
-    if (st != PCR_OK) return st;
-    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 3], cs));
-  }
-  if (mode == 0) {
-    CUDA_TRY(c, cudaEventRecord(c->ev_join, ls));
-    CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_join, 0));
-  }
-  if (timed) {
-    CUDA_TRY(c, cudaStreamSynchronize(cs));
-    for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
-      CUDA_TRY(c, cudaEventElapsedTime(&layer_times_ms[2 * l], c->ev_t[4 * l + 0], c->ev_t[4 * l + 1]));
-      CUDA_TRY(c, cudaEventElapsedTime(&layer_times_ms[2 * l + 1], c->ev_t[4 * l + 2], c->ev_t[4 * l + 3]));
-    }
-  }
+  if (c->nccl_comm) return fail(c, PCR_E_STATE, "pcr_comm_init: communicator already attached");
+  const pcr::NcclApi* api = pcr::nccl_api();
+  if (!api) return fail(c, PCR_E_UNSUPPORTED, "pcr_comm_init: libnccl.so.2 not loadable");
+  pcr::NcclApi::UniqueId uid;
+  std::memcpy(uid.internal, id, 128);
+  void* comm = nullptr;
+  int r = api->comm_init_rank(&comm, c->cfg.world, uid, c->cfg.rank);
+  if (r != 0)
+    return fail(c, PCR_E_CUDA, std::string("ncclCommInitRank: ") + (api->get_error_string ? api->get_error_string(r) : "error"));
+  c->nccl_comm = comm;
   return PCR_OK;
 }
 

@@ -66,6 +66,10 @@ PROTOTYPES = {
     "pcr_prefill_attn_layer": (_I32, [_VP, _I64, _I32, _VP, _VP, _VP, _VP, _VP]),
     "pcr_run_prefill": (_I32, [_VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _I32, _P(ctypes.c_float)]),
     "pcr_kernel_launches": (_I64, [_VP]),
+    "pcr_comm_unique_id": (_I32, [_P(ctypes.c_uint8)]),
+    "pcr_comm_init": (_I32, [_VP, _P(ctypes.c_uint8)]),
+    "pcr_run_prefill_sharded": (_I32, [_VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32,
+                                       _P(ctypes.c_float)]),
 }
 
 _lib = None
@@ -107,6 +111,16 @@ def blake2b(data: bytes, digest_len: int = 64, key: bytes = b"") -> bytes:
     st = lib.pcr_blake2b(data, len(data), key if key else None, len(key), digest_len, out)
     if st != 0:
         raise PcrError(st, "pcr_blake2b")
+    return bytes(out)
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId through libpcr (create on one rank, broadcast the 128 bytes)."""
+    lib = load_library()
+    out = (ctypes.c_uint8 * 128)()
+    st = lib.pcr_comm_unique_id(out)
+    if st != 0:
+        raise PcrError(st, "pcr_comm_unique_id")
     return bytes(out)
 
 
@@ -225,4 +239,19 @@ class Context:
         if layer_times:
             t = np.array(times[:], dtype=np.float64).reshape(self.n_layers, 2)
             return t
+        return None
+
+    def comm_init(self, uid: bytes):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        self._check(self.lib.pcr_comm_init(self.h, buf), "pcr_comm_init")
+
+    def run_prefill_sharded(self, req_id, q_all, k_all, v_all, out_all, gathered_all, compute_stream,
+                            load_stream, comm_stream, mode=MODE_OVERLAP, layer_times=False):
+        times = (ctypes.c_float * (2 * self.n_layers))() if layer_times else None
+        self._check(self.lib.pcr_run_prefill_sharded(self.h, req_id, _ptr(q_all), _ptr(k_all), _ptr(v_all),
+                                                     _ptr(out_all), _ptr(gathered_all), _stream(compute_stream),
+                                                     _stream(load_stream), _stream(comm_stream), mode, times),
+                    "pcr_run_prefill_sharded")
+        if layer_times:
+            return np.array(times[:], dtype=np.float64).reshape(self.n_layers, 2)
         return None

@@ -218,3 +218,26 @@ def test_l8_full_size_sampled():
         kc, vc = rig.expected_context(plan, k[:, N1:], v[:, N1:], l)
         r, m = check_attention(out[l], q[l], kc, vc, N1, rows=rows)
         assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (l, r, m)
+
+
+def test_sharded_run_with_nccl_allgather_world1():
+    """The in-library per-layer NCCL all-gather path (pcr_run_prefill_sharded) on a world-1
+    communicator: the gathered tensor equals the local output bit for bit, and the output
+    equals pcr_run_prefill's."""
+    from paper_2603_23049_b200 import comm_unique_id
+    rig, plan, q, k, v, out = _single_request("iid", 2, 32, 8, 128, 256, 64, 512, 100, seed=33)
+    rig.ctx.release(1, True)
+    rng = make_rng(33)
+    doc = rng.integers(0, 1000, 512, dtype=np.uint32)
+    toks = np.concatenate([doc, rng.integers(0, 1000, 100, dtype=np.uint32)])
+    rig.ctx.submit(2, toks, n_cacheable=512)
+    rig.ctx.match_prefix(2, [])
+    rig.ctx.comm_init(comm_unique_id())
+    qd, kd, vd = to_dev(q), to_dev(k[:, 512:]), to_dev(v[:, 512:])
+    o = torch.empty_like(qd)
+    gathered = torch.empty((2, 1) + tuple(qd.shape[1:]), dtype=qd.dtype, device="cuda")
+    xs = torch.cuda.Stream()
+    rig.ctx.run_prefill_sharded(2, qd, kd, vd, o, gathered, rig.cs, rig.ls, xs)
+    rig.cs.synchronize()
+    assert np.array_equal(to_host(o), out)
+    assert np.array_equal(to_host(gathered)[:, 0], out)
