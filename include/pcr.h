@@ -86,7 +86,11 @@ typedef struct pcr_config {
   int32_t max_inflight;  /* requests planned but not yet released; 0 -> 4 */
   int32_t max_tokens;    /* max tokens of one request; 0 -> pool capacity in tokens */
   int32_t gather_ctas;   /* CTAs of the host->HBM gather kernel; 0 -> library default */
-  int32_t reserved0;
+  int32_t load_mode;     /* a2 implementation: 0 = sm_100a 16-byte gather kernel (default);
+                            baselines of the paper's copy path (fig:api), no SMs used:
+                            1 = copy engine, one cudaMemcpyBatchAsync per layer over all page
+                            segments; 2 = copy engine, one cudaMemcpyAsync per page segment;
+                            3 = experiment: TMA bulk copies host -> smem -> pool page */
 } pcr_config;
 
 /* Create a context.  Allocates the pinned store (mmap + NUMA-local mbind to the GPU's
@@ -225,6 +229,33 @@ pcr_status pcr_run_prefill_sharded(pcr_ctx* ctx, int64_t req_id, const void* q_a
                                    const void* v_all, void* out_all, void* gathered_all,
                                    void* compute_stream, void* load_stream, void* comm_stream,
                                    int32_t mode, float* layer_times_ms);
+
+/* ---------------------------------------------------------------- offload (§8 f1) --- */
+
+/* f1 — layer-wise offload of the request's new chunks (gpu_to_cpu, Alg.1; P:166,
+ * P:400 "offloading can commence immediately after each layer's computation"): enqueue on
+ * offload_stream the copy of layer `layer` of every reserved chunk from its pool pages into its
+ * store slot (16-byte SM loads from HBM, 16-byte stores over PCIe into the mapped store).  The
+ * caller orders it after pcr_prefill_attn_layer(layer) (which appended the suffix K/V).  Once
+ * all layers' copies have completed, pcr_release(commit=1) makes the chunks RESIDENT. */
+pcr_status pcr_offload_layer_kv(pcr_ctx* ctx, int64_t req_id, int32_t layer, void* offload_stream);
+
+/* Options of pcr_run_prefill_ex: the paper's three streams + the optional all-gather. */
+typedef struct pcr_run_opts {
+  void* compute_stream;    /* required; joined with every other stream at the end */
+  void* load_stream;       /* required in OVERLAP mode (distinct from compute_stream) */
+  void* offload_stream;    /* nullable: offload reserved chunks layer by layer on this stream */
+  void* comm_stream;       /* required iff gathered_all != NULL */
+  void* gathered_all;      /* nullable: per-layer NCCL all-gather target (pcr_run_prefill_sharded) */
+  float* layer_times_ms;   /* nullable: [3L] per-layer gather, append+attention, offload (ms); blocks */
+  int32_t mode;            /* 0 OVERLAP, 1 SYNC (everything in order on compute_stream) */
+  int32_t reserved0;
+} pcr_run_opts;
+
+/* The full per-request pipeline: pcr_run_prefill + (optional) offload on a third stream, the
+ * per-layer event chain being load(l) -> append+attn(l) -> offload(l) (and -> all-gather(l)). */
+pcr_status pcr_run_prefill_ex(pcr_ctx* ctx, int64_t req_id, const void* q_all, const void* k_all,
+                              const void* v_all, void* out_all, const pcr_run_opts* opts);
 
 /* Count of kernels launched by this ctx since creation (bench `gpu_launches`). */
 int64_t pcr_kernel_launches(const pcr_ctx* ctx);

@@ -20,6 +20,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall", "-I" + os.path.join(ROOT, "include")]
+# experiment knobs only (e.g. PCR_NVCC_EXTRA="-DPCR_POLY_PAIRS=2"); the default build uses none
+COMMON += os.environ.get("PCR_NVCC_EXTRA", "").split()
 
 SOURCES = [
     "host/blake2b.cpp",

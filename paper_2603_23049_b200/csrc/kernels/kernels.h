@@ -19,6 +19,16 @@ cudaError_t launch_kv_gather(const void* store, void* pool, const int32_t* d_slo
                              int32_t n_matched, int32_t layer, const KvGeom& g, int32_t target_ctas,
                              cudaStream_t stream);
 
+// a2 variant (load_mode 3, experiment): same copy with TMA bulk copies (host -> smem -> pool).
+cudaError_t launch_kv_gather_tma(const void* store, void* pool, const int32_t* d_slots, const int32_t* d_pages,
+                                 int32_t n_matched, int32_t layer, const KvGeom& g, int32_t ctas, cudaStream_t stream);
+
+// f1: store[slots[c]][layer][h][kv][t%C] = pool[layer][pages[t/S]][h][kv][t%S] for the chain
+// chunks c in [chunk0, chunk0+n_chunks) (the request's reserved chunks), into the mapped store.
+cudaError_t launch_kv_scatter(const void* pool, void* store, const int32_t* d_slots, const int32_t* d_pages,
+                              int32_t chunk0, int32_t n_chunks, int32_t layer, const KvGeom& g, int32_t target_ctas,
+                              cudaStream_t stream);
+
 // a3: suffix token i -> pool token n1+i for K and V; zero-fills rows [n1+n2, n_pages*S) of the
 // request's last page so the attention never reads uninitialised (possibly NaN) bits.
 cudaError_t launch_kv_append(const void* k_new, const void* v_new, void* pool, const int32_t* d_pages,

@@ -97,6 +97,95 @@ __global__ void kv_append_kernel(const uint4* __restrict__ k_new, const uint4* _
   }
 }
 
+// f1 offload (the inverse of the gather): layer `layer` of every reserved chunk, pool pages ->
+// pinned host store slot, 16-byte loads from HBM and 16-byte stores over PCIe into the mapped
+// store.  grid = (ctas_per_chunk, n_chunks); chunk c is chain index chunk0 + c.
+__global__ void __launch_bounds__(kThreads, 6) kv_scatter_kernel(const uint4* __restrict__ pool,
+                                                              uint4* __restrict__ store,
+                                                              const int32_t* __restrict__ slots,
+                                                              const int32_t* __restrict__ pages, int32_t chunk0,
+                                                              int32_t layer, KvGeom g, int32_t row16_log2,
+                                                              int32_t C_log2, int32_t S_log2) {
+  const int32_t c = chunk0 + blockIdx.y;
+  const int64_t row16 = int64_t(1) << row16_log2;
+  const int64_t block16 = int64_t(g.Hkv) * 2 * g.C * row16;
+  uint4* dst = store + (int64_t(slots[c]) * g.slot_elems + int64_t(layer) * g.Hkv * 2 * g.C * g.d) / 8;
+  const int64_t page16 = int64_t(g.Hkv) * 2 * g.S * row16;
+  const uint4* src_layer = pool + int64_t(layer) * g.n_pool_pages * page16;
+  const int64_t stride = int64_t(gridDim.x) * kThreads;
+  for (int64_t base = int64_t(blockIdx.x) * kThreads + threadIdx.x; base < block16; base += stride * kUnroll) {
+    uint4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t o = base + u * stride;
+      if (o < block16) {
+        const int64_t row = o >> row16_log2;
+        const int64_t col = o & (row16 - 1);
+        const int64_t hk = row >> C_log2;
+        const int64_t tt = (int64_t(c) << C_log2) + (row & (g.C - 1));
+        const int64_t page = pages[tt >> S_log2];
+        v[u] = src_layer[page * page16 + ((hk << S_log2) + (tt & (g.S - 1))) * row16 + col];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t o = base + u * stride;
+      if (o < block16) dst[o] = v[u];
+    }
+  }
+}
+
+// load_mode 3 experiment: the same page segments moved with the Tensor Memory Accelerator's
+// bulk copies instead of 16-byte thread loads: host store --cp.async.bulk--> smem --cp.async.bulk-->
+// pool page.  One elected thread per CTA keeps kStages segments in flight.
+constexpr int kTmaStages = 2;
+constexpr int kTmaSegMax = 16384;  // bytes per segment buffer (S_pg * d * 2 <= 16 KB)
+
+__global__ void __launch_bounds__(32) kv_gather_tma_kernel(const uint8_t* __restrict__ store, uint8_t* __restrict__ pool,
+                                                          const int32_t* __restrict__ slots,
+                                                          const int32_t* __restrict__ pages, int32_t n_matched,
+                                                          int32_t layer, KvGeom g) {
+  __shared__ __align__(128) uint8_t buf[kTmaStages][kTmaSegMax];
+  __shared__ __align__(8) uint64_t full[kTmaStages];
+  if (threadIdx.x != 0) return;
+  const int64_t seg = int64_t(g.S) * g.d * 2;
+  const int32_t ppc = g.C / g.S;
+  const int64_t n_seg = int64_t(n_matched) * g.Hkv * 2 * ppc;
+  for (int s = 0; s < kTmaStages; ++s)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&full[s]))));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  uint32_t phase[kTmaStages] = {0};
+  int it = 0;
+  for (int64_t i = blockIdx.x; i < n_seg; i += gridDim.x, ++it) {
+    const int st = it % kTmaStages;
+    const uint32_t sbuf = static_cast<uint32_t>(__cvta_generic_to_shared(buf[st]));
+    const uint32_t sbar = static_cast<uint32_t>(__cvta_generic_to_shared(&full[st]));
+    if (it >= kTmaStages)  // the store that last read this buffer must have finished reading it
+      asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTmaStages - 1) : "memory");
+    // segment i -> (chunk, h, kv, page-in-chunk)
+    const int32_t pp = int32_t(i % ppc);
+    const int64_t hk = (i / ppc) % (g.Hkv * 2);
+    const int32_t c = int32_t(i / (ppc * g.Hkv * 2));
+    const uint8_t* src = store + (int64_t(slots[c]) * g.slot_elems + int64_t(layer) * g.Hkv * 2 * g.C * g.d) * 2 +
+                         hk * int64_t(g.C) * g.d * 2 + pp * seg;
+    const int64_t page = pages[c * ppc + pp];
+    uint8_t* dst = pool + ((int64_t(layer) * g.n_pool_pages + page) * g.Hkv * 2 + hk) * seg;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(uint32_t(seg)) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sbuf),
+                 "l"(src), "r"(uint32_t(seg)), "r"(sbar)
+                 : "memory");
+    asm volatile(
+        "{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(sbar),
+        "r"(phase[st])
+        : "memory");
+    phase[st] ^= 1;
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sbuf), "r"(uint32_t(seg))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int ilog2(int64_t x) {
   int r = 0;
   while ((int64_t(1) << r) < x) ++r;
@@ -114,6 +203,27 @@ cudaError_t launch_kv_gather(const void* store, void* pool, const int32_t* d_slo
   kv_gather_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint4*>(store), static_cast<uint4*>(pool),
                                                   d_slots, d_pages, layer, g, ilog2(g.d / 8), ilog2(g.C),
                                                   ilog2(g.S));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kv_gather_tma(const void* store, void* pool, const int32_t* d_slots, const int32_t* d_pages,
+                                 int32_t n_matched, int32_t layer, const KvGeom& g, int32_t ctas, cudaStream_t stream) {
+  if (n_matched <= 0) return cudaSuccess;
+  if (int64_t(g.S) * g.d * 2 > kTmaSegMax) return cudaErrorInvalidValue;
+  kv_gather_tma_kernel<<<ctas, 32, 0, stream>>>(static_cast<const uint8_t*>(store), static_cast<uint8_t*>(pool),
+                                                d_slots, d_pages, n_matched, layer, g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kv_scatter(const void* pool, void* store, const int32_t* d_slots, const int32_t* d_pages,
+                              int32_t chunk0, int32_t n_chunks, int32_t layer, const KvGeom& g, int32_t target_ctas,
+                              cudaStream_t stream) {
+  if (n_chunks <= 0) return cudaSuccess;
+  const int per_chunk = (target_ctas + n_chunks - 1) / n_chunks;
+  dim3 grid(per_chunk, n_chunks);
+  kv_scatter_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint4*>(pool), static_cast<uint4*>(store),
+                                                   d_slots, d_pages, chunk0, layer, g, ilog2(g.d / 8), ilog2(g.C),
+                                                   ilog2(g.S));
   return cudaGetLastError();
 }
 

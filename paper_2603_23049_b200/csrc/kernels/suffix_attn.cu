@@ -46,6 +46,13 @@ constexpr int kThreads = 128 + kNQ * 128;
 constexpr int kHalfBytes = 128 * 128;  // 128 rows x 128 bytes (64 bf16) per swizzle column block
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+// Pairs (of 16 per 32-column chunk) whose exp2 runs as a polynomial on the FMA pipe instead of
+// MUFU.EX2: at d = 128 the MUFU rate (16/clk/SM) equals the tensor rate per score, so moving
+// a quarter of the exponentials to the FMA pipe lets the softmax keep up with the MMAs.
+#ifndef PCR_POLY_PAIRS
+#define PCR_POLY_PAIRS 4
+#endif
+constexpr int kPolyPairs = PCR_POLY_PAIRS;
 
 template <int D>
 struct Layout {
@@ -86,14 +93,31 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       : "memory");
 }
 
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b, float& sum) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-  sum += __low2float(v) + __high2float(v);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
 
 // 136 registers x 384 threads = 52K of the SM's 64K: a 256-thread gather CTA (10K) still fits
 // beside an attention CTA, so layer l+1's host->HBM load never waits for attention SMs.
+// 2^x for a pair of x <= 0 on the FMA pipe (FA4-style MUFU offload): x = n + f with
+// n = round(x), f in [-1/2, 1/2]; 2^f by a degree-3 minimax polynomial (max relative error
+// 7.5e-5, far below the 2^-9 bf16 rounding P gets next); 2^n added to the exponent bits.
+// x is clamped at -126 (result >= 2^-126 instead of 0 for masked keys: < 1e-37 relative).
+__device__ __forceinline__ void exp2_poly2(uint64_t x2, float& y0, float& y1) {
+  float x0, x1;
+  f2_unpack(x2, x0, x1);
+  const uint64_t xc = f2_pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  const uint64_t t = fadd2(xc, f2_pack(12582912.f, 12582912.f));      // 1.5 * 2^23: round to int
+  const uint64_t r = fadd2(t, f2_pack(-12582912.f, -12582912.f));     // round(x)
+  const uint64_t f = ffma2(r, f2_pack(-1.f, -1.f), xc);               // x - round(x)
+  uint64_t q = ffma2(f, f2_pack(0.055171095f, 0.055171095f), f2_pack(0.24260999f, 0.24260999f));
+  q = ffma2(q, f, f2_pack(0.69326097f, 0.69326097f));
+  q = ffma2(q, f, f2_pack(0.99992812f, 0.99992812f));
+  float q0, q1, t0, t1;
+  f2_unpack(q, q0, q1);
+  f2_unpack(t, t0, t1);
+  // bits(t) = bits(1.5*2^23) + n and (bits(1.5*2^23) << 23) == 0 mod 2^32, so n << 23 == bits(t) << 23
+  y0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23));
+  y1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
+}
+
 template <int D>
 __global__ void __maxnreg__(136)
     suffix_attn_kernel(const __grid_constant__ CUtensorMap tmap_pool, const __grid_constant__ CUtensorMap tmap_q,
@@ -278,9 +302,17 @@ __global__ void __maxnreg__(136)
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          float x0, x1;
-          f2_unpack(ffma2(f2_pack(v[e], v[e + 1]), scale2, negm2), x0, x1);
-          __nv_bfloat162 b = __floats2bfloat162_rn(ex2(x0), ex2(x1));
+          const uint64_t x2 = ffma2(f2_pack(v[e], v[e + 1]), scale2, negm2);
+          float y0, y1;
+          if (e >= 32 - 2 * kPolyPairs) {
+            exp2_poly2(x2, y0, y1);       // FMA pipe
+          } else {
+            float x0, x1;
+            f2_unpack(x2, x0, x1);
+            y0 = ex2(x0);                 // MUFU
+            y1 = ex2(x1);
+          }
+          __nv_bfloat162 b = __floats2bfloat162_rn(y0, y1);
           const uint32_t w = *reinterpret_cast<uint32_t*>(&b);
           pk[e / 2] = w;
           // row sum of the same bf16-rounded weights (R18), two lanes per FADD2

@@ -52,8 +52,11 @@ struct pcr_ctx {
   int64_t ws_floats = 0;
   // multi-GPU output re-assembly (§8(e))
   void* nccl_comm = nullptr;
+  std::vector<void*> ce_dst, ce_src;  // copy-engine baseline batch (load_mode 1/2)
+  std::vector<size_t> ce_size;
   std::vector<cudaEvent_t> ev_attn;
   cudaEvent_t ev_comm = nullptr;
+  cudaEvent_t ev_off = nullptr;
 };
 
 namespace {
@@ -152,8 +155,51 @@ pcr_status device_ready(pcr_ctx* c) {
   return PCR_OK;
 }
 
+// Copy-engine baselines of a2 (the paper's path): the same page segments as the gather
+// kernel — for each matched chunk, kv head, K/V and page of the chunk, S_pg*d*2 contiguous bytes.
+pcr_status enqueue_ce_copy(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s) {
+  const pcr_config& k = c->cfg;
+  const int64_t seg = int64_t(k.page_tokens) * k.head_dim * 2;
+  const int32_t pages_per_chunk = k.chunk_tokens / k.page_tokens;
+  const int64_t n = int64_t(r->plan.n_matched) * c->hkv * 2 * pages_per_chunk;
+  c->ce_dst.resize(n);
+  c->ce_src.resize(n);
+  c->ce_size.assign(n, static_cast<size_t>(seg));
+  int64_t i = 0;
+  uint8_t* pool = static_cast<uint8_t*>(k.pool);
+  uint8_t* store = static_cast<uint8_t*>(c->store);
+  for (int32_t ch = 0; ch < r->plan.n_matched; ++ch)
+    for (int32_t h = 0; h < c->hkv; ++h)
+      for (int32_t kv = 0; kv < 2; ++kv)
+        for (int32_t pp = 0; pp < pages_per_chunk; ++pp, ++i) {
+          const int64_t page = r->plan.pages[ch * pages_per_chunk + pp];
+          c->ce_src[i] = store + r->plan.slots[ch] * c->slot_bytes +
+                         ((int64_t(layer) * c->hkv + h) * 2 + kv) * int64_t(k.chunk_tokens) * k.head_dim * 2 + pp * seg;
+          c->ce_dst[i] = pool + (((int64_t(layer) * c->n_pool_pages + page) * c->hkv + h) * 2 + kv) * seg;
+        }
+  if (k.load_mode == 1) {
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    size_t idx = 0, fail_idx = 0;
+    CUDA_TRY(c, cudaMemcpyBatchAsync(c->ce_dst.data(), c->ce_src.data(), c->ce_size.data(), n, &attr, &idx, 1,
+                                     &fail_idx, s));
+  } else {
+    for (int64_t j = 0; j < n; ++j)
+      CUDA_TRY(c, cudaMemcpyAsync(c->ce_dst[j], c->ce_src[j], seg, cudaMemcpyHostToDevice, s));
+  }
+  return PCR_OK;
+}
+
 pcr_status enqueue_gather(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s) {
   if (r->plan.n_matched == 0) return PCR_OK;
+  if (c->cfg.load_mode == 3) {
+    CUDA_TRY(c, pcr::launch_kv_gather_tma(c->store_dev, c->cfg.pool, d_slots_of(c, r), d_pages_of(c, r),
+                                          r->plan.n_matched, layer, c->geom, 4 * c->gather_ctas, s));
+    c->launches += 1;
+    return PCR_OK;
+  }
+  if (c->cfg.load_mode != 0) return enqueue_ce_copy(c, r, layer, s);
   CUDA_TRY(c, pcr::launch_kv_gather(c->store_dev, c->cfg.pool, d_slots_of(c, r), d_pages_of(c, r),
                                     r->plan.n_matched, layer, c->geom, c->gather_ctas, s));
   c->launches += 1;
@@ -189,66 +235,94 @@ pcr_status enqueue_attn(pcr_ctx* c, Request* r, int32_t layer, const void* q, co
 }
 
 
+pcr_status enqueue_offload(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s) {
+  if (r->plan.n_reserved == 0) return PCR_OK;
+  CUDA_TRY(c, pcr::launch_kv_scatter(c->cfg.pool, c->store_dev, d_slots_of(c, r), d_pages_of(c, r),
+                                     r->plan.n_matched, r->plan.n_reserved, layer, c->geom, c->gather_ctas, s));
+  c->launches += 1;
+  return PCR_OK;
+}
+
 pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const void* k_all, const void* v_all,
-                            void* out_all, void* gathered_all, void* compute_stream, void* load_stream,
-                            void* comm_stream, int32_t mode, float* layer_times_ms) {
+                            void* out_all, const pcr_run_opts& o, int times_stride) {
   if (!c) return PCR_E_INVAL;
   pcr_status st = device_ready(c);
   if (st != PCR_OK) return st;
   Request* r = planned_request(c, req_id, &st);
   if (!r) return st;
   if (!q_all || !k_all || !v_all || !out_all) return fail(c, PCR_E_INVAL, "null q/k/v/out");
-  if (mode != 0 && mode != 1) return fail(c, PCR_E_INVAL, "mode must be 0 (OVERLAP) or 1 (SYNC)");
-  cudaStream_t cs = static_cast<cudaStream_t>(compute_stream);
-  cudaStream_t ls = mode == 0 ? static_cast<cudaStream_t>(load_stream) : cs;
-  cudaStream_t xs = static_cast<cudaStream_t>(comm_stream);
-  if (mode == 0 && load_stream == compute_stream)
-    return fail(c, PCR_E_INVAL, "OVERLAP mode needs two distinct streams");
+  if (o.mode != 0 && o.mode != 1) return fail(c, PCR_E_INVAL, "mode must be 0 (OVERLAP) or 1 (SYNC)");
+  if (!o.compute_stream) return fail(c, PCR_E_INVAL, "null compute stream");
+  if (o.mode == 0 && (!o.load_stream || o.load_stream == o.compute_stream))
+    return fail(c, PCR_E_INVAL, "OVERLAP mode needs a load stream distinct from the compute stream");
+  if (o.gathered_all && (!o.comm_stream || !c->nccl_comm))
+    return fail(c, o.comm_stream ? PCR_E_STATE : PCR_E_INVAL, "all-gather needs pcr_comm_init and a comm stream");
+  cudaStream_t cs = static_cast<cudaStream_t>(o.compute_stream);
+  cudaStream_t ls = o.mode == 0 ? static_cast<cudaStream_t>(o.load_stream) : cs;
+  cudaStream_t os = o.offload_stream ? (o.mode == 0 ? static_cast<cudaStream_t>(o.offload_stream) : cs) : nullptr;
+  cudaStream_t xs = static_cast<cudaStream_t>(o.comm_stream);
   const int64_t n2 = r->plan.n2;
   const int64_t q_layer = n2 * c->hq * c->cfg.head_dim, kv_layer = n2 * c->hkv * c->cfg.head_dim;
-  const bool timed = layer_times_ms != nullptr;
-  const pcr::NcclApi* api = gathered_all ? pcr::nccl_api() : nullptr;
-  if (gathered_all && !api) return fail(c, PCR_E_UNSUPPORTED, "libnccl.so.2 not loadable");
+  float* times = o.layer_times_ms;
+  const pcr::NcclApi* api = o.gathered_all ? pcr::nccl_api() : nullptr;
+  if (o.gathered_all && !api) return fail(c, PCR_E_UNSUPPORTED, "libnccl.so.2 not loadable");
   if ((st = ensure_tables(c, r, ls)) != PCR_OK) return st;
-  if (mode == 0) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->region_ev[r->plan.region], 0));
+  if (o.mode == 0) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->region_ev[r->plan.region], 0));
   for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
-    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 0], ls));
+    cudaEvent_t* et = &c->ev_t[6 * l];
+    if (times) CUDA_TRY(c, cudaEventRecord(et[0], ls));
     if ((st = enqueue_gather(c, r, l, ls)) != PCR_OK) return st;
-    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 1], ls));
-    if (mode == 0) {
+    if (times) CUDA_TRY(c, cudaEventRecord(et[1], ls));
+    if (o.mode == 0) {
       CUDA_TRY(c, cudaEventRecord(c->ev_load[l], ls));
       CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_load[l], 0));
     }
-    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 2], cs));
+    if (times) CUDA_TRY(c, cudaEventRecord(et[2], cs));
     uint16_t* out_l = static_cast<uint16_t*>(out_all) + l * q_layer;
     st = enqueue_attn(c, r, l, static_cast<const uint16_t*>(q_all) + l * q_layer,
                       static_cast<const uint16_t*>(k_all) + l * kv_layer,
                       static_cast<const uint16_t*>(v_all) + l * kv_layer, out_l, cs);
     if (st != PCR_OK) return st;
-    if (timed) CUDA_TRY(c, cudaEventRecord(c->ev_t[4 * l + 3], cs));
-    if (gathered_all) {
+    if (times) CUDA_TRY(c, cudaEventRecord(et[3], cs));
+    if (os || o.gathered_all) CUDA_TRY(c, cudaEventRecord(c->ev_attn[l], cs));
+    if (os) {
+      // layer-wise offload of the new chunks right after this layer's KV exists
+      if (os != cs) CUDA_TRY(c, cudaStreamWaitEvent(os, c->ev_attn[l], 0));
+      if (times) CUDA_TRY(c, cudaEventRecord(et[4], os));
+      if ((st = enqueue_offload(c, r, l, os)) != PCR_OK) return st;
+      if (times) CUDA_TRY(c, cudaEventRecord(et[5], os));
+    }
+    if (o.gathered_all) {
       // re-assemble this layer's head-sharded output on the comm stream while layer l+1 runs
-      CUDA_TRY(c, cudaEventRecord(c->ev_attn[l], cs));
       CUDA_TRY(c, cudaStreamWaitEvent(xs, c->ev_attn[l], 0));
       const size_t bytes = static_cast<size_t>(q_layer) * 2;
-      int rr = api->all_gather(out_l, static_cast<uint8_t*>(gathered_all) + bytes * c->cfg.world * l, bytes,
+      int rr = api->all_gather(out_l, static_cast<uint8_t*>(o.gathered_all) + bytes * c->cfg.world * l, bytes,
                                /*ncclInt8*/ 0, c->nccl_comm, xs);
       if (rr != 0) return fail(c, PCR_E_CUDA, "ncclAllGather failed");
     }
   }
-  if (mode == 0) {
+  if (o.mode == 0) {
     CUDA_TRY(c, cudaEventRecord(c->ev_join, ls));
     CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_join, 0));
   }
-  if (gathered_all) {
+  if (os && os != cs) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_off, os));
+    CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_off, 0));
+  }
+  if (o.gathered_all) {
     CUDA_TRY(c, cudaEventRecord(c->ev_comm, xs));
     CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_comm, 0));
   }
-  if (timed) {
+  if (times) {
     CUDA_TRY(c, cudaStreamSynchronize(cs));
     for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
-      CUDA_TRY(c, cudaEventElapsedTime(&layer_times_ms[2 * l], c->ev_t[4 * l + 0], c->ev_t[4 * l + 1]));
-      CUDA_TRY(c, cudaEventElapsedTime(&layer_times_ms[2 * l + 1], c->ev_t[4 * l + 2], c->ev_t[4 * l + 3]));
+      cudaEvent_t* et = &c->ev_t[6 * l];
+      CUDA_TRY(c, cudaEventElapsedTime(&times[times_stride * l], et[0], et[1]));
+      CUDA_TRY(c, cudaEventElapsedTime(&times[times_stride * l + 1], et[2], et[3]));
+      if (times_stride > 2) {
+        times[times_stride * l + 2] = 0.f;
+        if (os) CUDA_TRY(c, cudaEventElapsedTime(&times[times_stride * l + 2], et[4], et[5]));
+      }
     }
   }
   return PCR_OK;
@@ -274,7 +348,7 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
       k.head_dim < 8 || k.head_dim % 8 || k.world < 1 || k.rank < 0 || k.rank >= k.world ||
       k.n_kv_heads % k.world || k.chunk_tokens < 1 || k.page_tokens < 1 || k.chunk_tokens % k.page_tokens ||
       k.store_chunks < 1 || k.window < 0 || k.pool_bytes < 0 || k.max_inflight < 0 || k.max_tokens < 0 ||
-      k.gather_ctas < 0)
+      k.gather_ctas < 0 || k.load_mode < 0 || k.load_mode > 3)
     return PCR_E_INVAL;
   auto c = std::make_unique<pcr_ctx>();
   c->cfg = k;
@@ -334,6 +408,7 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
     }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cp->ev_join, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cp->ev_comm, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cp->ev_off, cudaEventDisableTiming);
     for (int l = 0; e == cudaSuccess && l < k.n_layers; ++l) {
       cudaEvent_t ev;
       e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
@@ -343,7 +418,7 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
       cp->ws_floats = (int64_t(32) << 20) / 4;  // 32 MiB of partial O (+ LSE)
       e = cudaMalloc(reinterpret_cast<void**>(&cp->ws), (cp->ws_floats + cp->ws_floats / 64 + 64) * 4);
     }
-    for (int l = 0; e == cudaSuccess && l < 4 * k.n_layers; ++l) {
+    for (int l = 0; e == cudaSuccess && l < 6 * k.n_layers; ++l) {
       cudaEvent_t ev;
       e = cudaEventCreate(&ev);
       if (e == cudaSuccess) cp->ev_t.push_back(ev);
@@ -376,6 +451,7 @@ void pcr_destroy(pcr_ctx* c) {
     for (auto e : c->ev_t) cudaEventDestroy(e);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+    if (c->ev_off) cudaEventDestroy(c->ev_off);
     for (auto e : c->ev_attn) cudaEventDestroy(e);
     if (c->nccl_comm) {
       if (const pcr::NcclApi* api = pcr::nccl_api()) api->comm_destroy(c->nccl_comm);
@@ -430,7 +506,7 @@ pcr_status pcr_match_prefix(pcr_ctx* c, int64_t req_id, const int64_t* pending, 
   // Stage the device tables (host memory only; uploaded by the first device call).
   int32_t* h = c->h_arena + pl.region * c->region_words;
   std::copy(pl.pages.begin(), pl.pages.end(), h);
-  std::copy(pl.slots.begin(), pl.slots.begin() + pl.n_matched, h + c->region_page_cap);
+  std::copy(pl.slots.begin(), pl.slots.end(), h + c->region_page_cap);
   return PCR_OK;
 }
 
@@ -503,8 +579,12 @@ pcr_status pcr_prefill_attn_layer(pcr_ctx* c, int64_t req_id, int32_t layer, con
 pcr_status pcr_run_prefill(pcr_ctx* c, int64_t req_id, const void* q_all, const void* k_all, const void* v_all,
                            void* out_all, void* compute_stream, void* load_stream, int32_t mode,
                            float* layer_times_ms) {
-  return run_prefill_impl(c, req_id, q_all, k_all, v_all, out_all, nullptr, compute_stream, load_stream, nullptr,
-                          mode, layer_times_ms);
+  pcr_run_opts o{};
+  o.compute_stream = compute_stream;
+  o.load_stream = load_stream;
+  o.mode = mode;
+  o.layer_times_ms = layer_times_ms;
+  return run_prefill_impl(c, req_id, q_all, k_all, v_all, out_all, o, 2);
 }
 
 pcr_status pcr_run_prefill_sharded(pcr_ctx* c, int64_t req_id, const void* q_all, const void* k_all,
@@ -513,8 +593,32 @@ pcr_status pcr_run_prefill_sharded(pcr_ctx* c, int64_t req_id, const void* q_all
   if (!c) return PCR_E_INVAL;
   if (!c->nccl_comm) return fail(c, PCR_E_STATE, "pcr_run_prefill_sharded: call pcr_comm_init first");
   if (!gathered_all || !comm_stream) return fail(c, PCR_E_INVAL, "null gathered_all or comm_stream");
-  return run_prefill_impl(c, req_id, q_all, k_all, v_all, out_all, gathered_all, compute_stream, load_stream,
-                          comm_stream, mode, layer_times_ms);
+  pcr_run_opts o{};
+  o.compute_stream = compute_stream;
+  o.load_stream = load_stream;
+  o.comm_stream = comm_stream;
+  o.gathered_all = gathered_all;
+  o.mode = mode;
+  o.layer_times_ms = layer_times_ms;
+  return run_prefill_impl(c, req_id, q_all, k_all, v_all, out_all, o, 2);
+}
+
+pcr_status pcr_run_prefill_ex(pcr_ctx* c, int64_t req_id, const void* q_all, const void* k_all, const void* v_all,
+                              void* out_all, const pcr_run_opts* opts) {
+  if (!c || !opts) return c ? fail(c, PCR_E_INVAL, "null options") : PCR_E_INVAL;
+  return run_prefill_impl(c, req_id, q_all, k_all, v_all, out_all, *opts, 3);
+}
+
+pcr_status pcr_offload_layer_kv(pcr_ctx* c, int64_t req_id, int32_t layer, void* offload_stream) {
+  if (!c) return PCR_E_INVAL;
+  pcr_status st = device_ready(c);
+  if (st != PCR_OK) return st;
+  Request* r = planned_request(c, req_id, &st);
+  if (!r) return st;
+  if (layer < 0 || layer >= c->cfg.n_layers) return fail(c, PCR_E_INVAL, "layer out of range");
+  cudaStream_t s = static_cast<cudaStream_t>(offload_stream);
+  if ((st = ensure_tables(c, r, s)) != PCR_OK) return st;
+  return enqueue_offload(c, r, layer, s);
 }
 
 pcr_status pcr_comm_unique_id(uint8_t* out) {

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libpcr.so")
 STATUS = {0: "OK", -1: "INVAL", -2: "NOMEM", -3: "CUDA", -4: "STATE", -5: "NOREQ", -6: "INTERNAL",
           -7: "UNSUPPORTED"}
 MODE_OVERLAP, MODE_SYNC = 0, 1
+LOAD_SM_GATHER, LOAD_CE_BATCH, LOAD_CE_BLOCKS = 0, 1, 2
 
 
 class PcrError(RuntimeError):
@@ -34,7 +35,7 @@ class PcrConfig(ctypes.Structure):
                 ("chunk_tokens", ctypes.c_int32), ("page_tokens", ctypes.c_int32),
                 ("store_chunks", ctypes.c_int64), ("window", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("pool", ctypes.c_void_p), ("pool_bytes", ctypes.c_int64), ("max_inflight", ctypes.c_int32),
-                ("max_tokens", ctypes.c_int32), ("gather_ctas", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
+                ("max_tokens", ctypes.c_int32), ("gather_ctas", ctypes.c_int32), ("load_mode", ctypes.c_int32)]
 
 
 class PcrPlan(ctypes.Structure):
@@ -44,6 +45,13 @@ class PcrPlan(ctypes.Structure):
                 ("cap_pages", ctypes.c_int32), ("n_pages", ctypes.c_int32), ("n_evicted", ctypes.c_int32),
                 ("evicted_keys", ctypes.POINTER(ctypes.c_uint8)), ("evicted_slots", ctypes.POINTER(ctypes.c_int32)),
                 ("cap_evicted", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
+
+
+class PcrRunOpts(ctypes.Structure):
+    _fields_ = [("compute_stream", ctypes.c_void_p), ("load_stream", ctypes.c_void_p),
+                ("offload_stream", ctypes.c_void_p), ("comm_stream", ctypes.c_void_p),
+                ("gathered_all", ctypes.c_void_p), ("layer_times_ms", ctypes.POINTER(ctypes.c_float)),
+                ("mode", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
 
 
 # Every exported symbol of include/pcr.h with its prototype (restype, argtypes).
@@ -70,6 +78,8 @@ PROTOTYPES = {
     "pcr_comm_init": (_I32, [_VP, _P(ctypes.c_uint8)]),
     "pcr_run_prefill_sharded": (_I32, [_VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32,
                                        _P(ctypes.c_float)]),
+    "pcr_offload_layer_kv": (_I32, [_VP, _I64, _I32, _VP]),
+    "pcr_run_prefill_ex": (_I32, [_VP, _I64, _VP, _VP, _VP, _VP, _P(PcrRunOpts)]),
 }
 
 _lib = None
@@ -129,14 +139,14 @@ class Context:
 
     def __init__(self, n_layers, n_q_heads, n_kv_heads, head_dim, chunk_tokens, page_tokens, store_chunks,
                  window, device=-1, pool=None, pool_bytes=None, rank=0, world=1, max_inflight=0, max_tokens=0,
-                 gather_ctas=0):
+                 gather_ctas=0, load_mode=LOAD_SM_GATHER):
         self.lib = load_library()
         if pool_bytes is None:
             pool_bytes = pool.numel() * pool.element_size() if hasattr(pool, "numel") else 0
         self._pool = pool
         cfg = PcrConfig(n_layers, n_q_heads, n_kv_heads, head_dim, rank, world, chunk_tokens, page_tokens,
                         store_chunks, window, device, _ptr(pool), int(pool_bytes), max_inflight, max_tokens,
-                        gather_ctas, 0)
+                        gather_ctas, load_mode)
         h = ctypes.c_void_p()
         st = self.lib.pcr_create(ctypes.byref(cfg), ctypes.byref(h))
         if st != 0:
@@ -239,6 +249,25 @@ class Context:
         if layer_times:
             t = np.array(times[:], dtype=np.float64).reshape(self.n_layers, 2)
             return t
+        return None
+
+    def offload_layer_kv(self, req_id, layer, offload_stream):
+        self._check(self.lib.pcr_offload_layer_kv(self.h, req_id, layer, _stream(offload_stream)),
+                    "pcr_offload_layer_kv")
+
+    def run_prefill_ex(self, req_id, q_all, k_all, v_all, out_all, compute_stream, load_stream=None,
+                       offload_stream=None, comm_stream=None, gathered_all=None, mode=MODE_OVERLAP,
+                       layer_times=False):
+        """Full pipeline (P:480 three streams): returns [L][3] ms (gather, append+attn, offload) if
+        layer_times, else None."""
+        times = (ctypes.c_float * (3 * self.n_layers))() if layer_times else None
+        o = PcrRunOpts(_stream(compute_stream), _stream(load_stream), _stream(offload_stream),
+                       _stream(comm_stream), _ptr(gathered_all),
+                       ctypes.cast(times, _P(ctypes.c_float)) if times is not None else None, mode, 0)
+        self._check(self.lib.pcr_run_prefill_ex(self.h, req_id, _ptr(q_all), _ptr(k_all), _ptr(v_all),
+                                                _ptr(out_all), ctypes.byref(o)), "pcr_run_prefill_ex")
+        if layer_times:
+            return np.array(times[:], dtype=np.float64).reshape(self.n_layers, 3)
         return None
 
     def comm_init(self, uid: bytes):

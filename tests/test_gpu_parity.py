@@ -35,7 +35,7 @@ def _warm_prefix(rig, req_id, doc_tokens, k_ctx, v_ctx, n_chunks):
     rig.ctx.release(req_id, True)
 
 
-def _single_request(kind, L, Hq, Hkv, d, C, S, N1, N2, seed, mode=0, world=1, rank=0):
+def _single_request(kind, L, Hq, Hkv, d, C, S, N1, N2, seed, mode=0, world=1, rank=0, **ctx_kw):
     """Warm N1 tokens, then run one request [doc | query] and return everything to compare."""
     rng = make_rng(seed)
     Hkv_l, Hq_l = Hkv // world, Hq // world
@@ -51,7 +51,7 @@ def _single_request(kind, L, Hq, Hkv, d, C, S, N1, N2, seed, mode=0, world=1, ra
     q, k, v = q[:, :, qs], k[:, :, hs], v[:, :, hs]
     n_pages = (N1 + N2) // S + 8
     rig = Rig(L, Hq, Hkv, d, C, S, store_chunks=max(1, N1 // C) + 2, n_pool_pages=n_pages + N1 // S + 2,
-              rank=rank, world=world)
+              rank=rank, world=world, **ctx_kw)
     doc = rng.integers(0, 1000, N1, dtype=np.uint32)
     if N1:
         _warm_prefix(rig, 1000, doc, k[:, :N1], v[:, :N1], N1 // C)
@@ -241,3 +241,53 @@ def test_sharded_run_with_nccl_allgather_world1():
     rig.cs.synchronize()
     assert np.array_equal(to_host(o), out)
     assert np.array_equal(to_host(gathered)[:, 0], out)
+
+
+@pytest.mark.parametrize("load_mode", [1, 2, 3])
+def test_copy_engine_baselines_match_gather(load_mode):
+    """f4 baselines (the paper's cudaMemcpyBatchAsync / block-by-block path) produce the
+    same pool bits and outputs as the SM gather kernel."""
+    args = ("kout", 2, 32, 8, 128, 256, 16, 768, 90)
+    rig0, plan0, q, k, v, out0 = _single_request(*args, seed=44)
+    rig1, plan1, _, _, _, out1 = _single_request(*args, seed=44, load_mode=load_mode)
+    assert plan0["pages"] == plan1["pages"] and plan0["slots"] == plan1["slots"]
+    assert np.array_equal(out0, out1)
+    p0, p1 = rig0.pool_np(), rig1.pool_np()
+    assert np.array_equal(p0[:, plan0["pages"]], p1[:, plan1["pages"]])
+
+
+def test_offload_third_stream_commits_real_kv():
+    """f1: the Appendix C trace where new chunks reach the store ONLY through the library's
+    layer-wise offload on a third stream (pcr_run_prefill_ex); every committed slot must hold
+    exactly the K/V the request computed (bitwise), and later hits must attend correctly."""
+    docs, order, reqs = appendix_c_trace(0)
+    model = TinyModel(L=2, Hq=4, Hkv=2, d=64, d_model=96, d_ff=128, vocab=1 << 17, seed=0)
+    W = 2
+    rig = Rig(2, 4, 2, 64, 64, 16, store_chunks=10, n_pool_pages=64, window=W)
+    os_ = torch.cuda.Stream()
+    for i, t in enumerate(reqs):
+        rig.ctx.submit(i, t)
+    for i, toks in enumerate(reqs):
+        pend = list(range(i + 1, min(len(reqs), i + 1 + W)))
+        plan = rig.ctx.match_prefix(i, pend)
+        _, kv, qs = model.forward(toks)
+        N1 = plan["n1"]
+        q = np.stack([f32_to_bf16_bits(qs[l][N1:].astype(np.float32)) for l in range(2)])
+        k = np.stack([f32_to_bf16_bits(kv[l][0].astype(np.float32)) for l in range(2)])
+        v = np.stack([f32_to_bf16_bits(kv[l][1].astype(np.float32)) for l in range(2)])
+        qd, kd, vd = to_dev(q), to_dev(k[:, N1:]), to_dev(v[:, N1:])
+        od = torch.empty_like(qd)
+        t3 = rig.ctx.run_prefill_ex(i, qd, kd, vd, od, rig.cs, rig.ls, offload_stream=os_, layer_times=True)
+        rig.cs.synchronize()
+        assert t3.shape == (2, 3)
+        out = to_host(od)
+        for l in range(2):
+            kc, vc = rig.expected_context(plan, k[:, N1:], v[:, N1:], l)
+            r, m = check_attention(out[l], q[l], kc, vc, N1)
+            assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (i, l, r, m)
+        recs = pack_store_slots(k, v, plan["n_matched"] + plan["n_reserved"], 64)
+        for c in range(plan["n_matched"], plan["n_matched"] + plan["n_reserved"]):
+            got = rig.ctx.store_read(plan["slots"][c]).reshape(recs[c].shape)
+            assert np.array_equal(got, recs[c]), (i, c)
+            rig.store[plan["slots"][c]] = got          # mirror for expected_context of later hits
+        rig.ctx.release(i, True)
