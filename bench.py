@@ -38,6 +38,7 @@ WORKLOADS = {
     "M7": ("M7", 8192, 128),
     "L70": ("L70", 16384, 128),
     "T": ("T", 256, 64),
+    "Z": ("L8", 0, 0),   # configs[4]: 1000-request Zipf trace (run_trace_z)
 }
 
 
@@ -54,6 +55,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gather-ctas", type=int, default=0, help="CTAs of the host->HBM gather (0 = library default)")
     ap.add_argument("--profile-steps", type=int, default=5, help="extra steps with per-layer events (after timing)")
+    ap.add_argument("--window", type=int, default=4, help="look-ahead window W (Z trace)")
+    ap.add_argument("--store-frac", type=float, default=0.10, help="Z: DRAM store size / distinct chunks")
+    ap.add_argument("--requests", type=int, default=1000, help="Z: requests in the trace")
     ap.add_argument("--load-mode", default="sm", choices=["sm", "ce_batch", "ce_blocks", "tma"],
                     help="a2 implementation: sm_100a gather kernel, or the paper's copy-engine paths")
     return ap.parse_args()
@@ -441,10 +445,100 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_trace_z(args):
+    """configs[4]: the Zipf RAG trace end to end on one GPU (look-ahead LRU + layer overlap +
+    layer-wise offload of new chunks on a third stream, committed at release).  One step = one
+    request; value = trace context tokens / device time; TTFT per request from CUDA events."""
+    import torch
+
+    from paper_2603_23049_b200 import MODE_OVERLAP, Context
+    from pcrgen import make_rng, randn_bf16, zipf_trace
+    torch.cuda.set_device(0)
+    geo = geometry("L8")
+    L, Hq, Hkv, d, C, S = geo["L"], geo["Hq"], geo["Hkv"], geo["d"], geo["C"], geo["S_pg"]
+    reqs, _, ndoc = zipf_trace(seed=4, n_requests=args.requests, C=C)
+    distinct = set()
+    for r, n in zip(reqs, ndoc):
+        for c in range(n // C):
+            distinct.add(r[: (c + 1) * C].tobytes())
+    cap = max(8, int(args.store_frac * len(distinct)))
+    max_n = max(len(r) for r in reqs)
+    pages_req = -(-max_n // S)
+    page_elems = L * Hkv * 2 * S * d
+    pool = torch.empty(2 * pages_req * page_elems + page_elems, dtype=torch.int16, device="cuda")
+    t0 = time.perf_counter()
+    ctx = Context(L, Hq, Hkv, d, C, S, cap, args.window, device=0, pool=pool, max_tokens=max_n,
+                  gather_ctas=args.gather_ctas)
+    t_pin = time.perf_counter() - t0
+    rng = make_rng(11)
+    max_n2 = max_n
+    q_d = torch.from_numpy(randn_bf16(rng, (L, max_n2, Hq, d)).view(np.int16)).cuda()
+    k_d = torch.from_numpy(randn_bf16(rng, (L, max_n2, Hkv, d)).view(np.int16)).cuda()
+    v_d = torch.from_numpy(randn_bf16(rng, (L, max_n2, Hkv, d)).view(np.int16)).cuda()
+    o_d = torch.empty_like(q_d)
+    cs, ls, os_ = torch.cuda.Stream(), torch.cuda.Stream(priority=-1), torch.cuda.Stream()
+    for i, (t, n) in enumerate(zip(reqs, ndoc)):
+        ctx.submit(i, t, n)
+    ttft, hits, chunks, toks, n1s, plan_us = [], 0, 0, 0, [], []
+    launches0 = ctx.kernel_launches
+    clocks = ClockSampler(0)
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(cs)
+    for i in range(len(reqs)):
+        pend = list(range(i + 1, min(len(reqs), i + 1 + args.window)))
+        tp = time.perf_counter()
+        plan = ctx.match_prefix(i, pend)
+        plan_us.append((time.perf_counter() - tp) * 1e6)
+        n2 = plan["n2"]
+        # contiguous [L][N2][H][d] views over the front of the max-size buffers
+        q = q_d.view(-1)[: L * n2 * Hq * d].view(L, n2, Hq, d)
+        k = k_d.view(-1)[: L * n2 * Hkv * d].view(L, n2, Hkv, d)
+        v = v_d.view(-1)[: L * n2 * Hkv * d].view(L, n2, Hkv, d)
+        o = o_d.view(-1)[: L * n2 * Hq * d].view(L, n2, Hq, d)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cs)
+        ls.wait_event(a)
+        os_.wait_event(a)
+        ctx.run_prefill_ex(i, q, k, v, o, cs, ls, offload_stream=os_, mode=MODE_OVERLAP)
+        b.record(cs)
+        b.synchronize()
+        ttft.append(a.elapsed_time(b))
+        ctx.release(i, True)
+        hits += plan["n_matched"]
+        chunks += ndoc[i] // C
+        toks += len(reqs[i])
+        n1s.append(plan["n1"])
+    ev1.record(cs)
+    torch.cuda.synchronize()
+    total_ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    tt = np.array(ttft)
+    line = {
+        "metric": "Z trace: context tokens/s over 1000 Zipf RAG requests (TTFT per request in ttft_ms_*)",
+        "value": toks / (total_ms * 1e-3), "unit": "tokens/s", "n_gpus": 1, "steps": len(reqs), "warmup": 0,
+        "ms_per_step": total_ms / len(reqs), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (seeded Zipf(1.0) corpus of 1000 docs x 4-16 chunks, 2 docs + "
+                                   "128-256 query tokens per request; random bf16 KV)",
+        "config": {"workload": f"Z: L8 shape, W={args.window}, store={cap} chunks "
+                               f"({args.store_frac:.0%} of {len(distinct)} distinct), offload on",
+                   "requests": len(reqs), "window": args.window, "store_chunks": cap},
+        "ttft_ms_mean": float(tt.mean()), "ttft_ms_p50": float(np.percentile(tt, 50)),
+        "ttft_ms_p95": float(np.percentile(tt, 95)), "ttft_ms_p99": float(np.percentile(tt, 99)),
+        "chunk_hit_ratio": hits / max(1, chunks), "mean_n1_tokens": float(np.mean(n1s)),
+        "match_prefix_us_p50": float(np.percentile(plan_us, 50)), "store_pin_s": t_pin,
+        "gpu_launches": ctx.kernel_launches - launches0, "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "Z":
+        run_trace_z(args)
     else:
         run_ours(args)
 

@@ -225,13 +225,18 @@ __global__ void __maxnreg__(136)
         const int st = it & 1;
         const bool more = it + 1 < n_iter;
         mbar_wait(&bars->v_full[st], (it >> 1) & 1);
-        if (more) mbar_wait(&bars->k_full[st ^ 1], ((it + 1) >> 1) & 1);
         for (int t = 0; t < kNQ; ++t) {
           mbar_wait(&bars->p_full[t], it & 1);
           tc_fence_after();
           issue_pv(t, it);
           if (t == kNQ - 1) mma_commit(&bars->kv_empty[st]);
-          if (more) issue_s(t, it + 1);
+          if (more) {
+            if (t == 0) {  // K(j+1) is only needed here, after PV_0(j) has been queued
+              mbar_wait(&bars->k_full[st ^ 1], ((it + 1) >> 1) & 1);
+              tc_fence_after();
+            }
+            issue_s(t, it + 1);
+          }
         }
       }
       mma_commit(&bars->o_full);
@@ -258,19 +263,29 @@ __global__ void __maxnreg__(136)
       const bool diag = key0 + kBlockN - 1 > tile_first_key_limit;  // tile crosses this Q tile's diagonal
       mbar_wait(&bars->s_full[t], it & 1);
       tc_fence_after();
+      // TMEM loads are software-pipelined: chunk c+1 is in flight while chunk c is processed.
+      float va[32], vb[32];
       float rowmax = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < kBlockN / 32; ++c) {
-        float v[32];
-        tmem_ld32(s_col + c * 32, v);
-        tmem_ld_wait();
+      auto max_chunk = [&](float* v, int c) {
         if (diag) {
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = (key0 + c * 32 + e <= limit) ? v[e] : -INFINITY;
         }
 #pragma unroll
         for (int e = 0; e < 32; e += 2) rowmax = fmax3(rowmax, v[e], v[e + 1]);
-      }
+      };
+      tmem_ld32(s_col, va);
+      tmem_ld_wait();
+      tmem_ld32(s_col + 32, vb);
+      max_chunk(va, 0);
+      tmem_ld_wait();
+      tmem_ld32(s_col + 64, va);
+      max_chunk(vb, 1);
+      tmem_ld_wait();
+      tmem_ld32(s_col + 96, vb);
+      max_chunk(va, 2);
+      tmem_ld_wait();
+      max_chunk(vb, 3);
       const float m_new = fmaxf(m_raw, rowmax);
       const bool rescale = (m_new - m_raw) * p.scale_log2 > kRescaleThreshold;
       const float m_use = rescale ? m_new : m_raw;
@@ -290,11 +305,7 @@ __global__ void __maxnreg__(136)
         }
       }
       uint64_t sum2 = 0;
-#pragma unroll
-      for (int c = 0; c < kBlockN / 32; ++c) {
-        float v[32];
-        tmem_ld32(s_col + c * 32, v);
-        tmem_ld_wait();
+      auto exp_chunk = [&](float* v, int c) {
         if (diag) {
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = (key0 + c * 32 + e <= limit) ? v[e] : -INFINITY;
@@ -318,8 +329,20 @@ __global__ void __maxnreg__(136)
           // row sum of the same bf16-rounded weights (R18), two lanes per FADD2
           sum2 = fadd2(sum2, f2_pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u)));
         }
-        tmem_st16(s_col + c * 16, pk);
-      }
+        tmem_st16(s_col + c * 16, pk);   // P chunk c -> columns [16c, 16c+16): already read
+      };
+      tmem_ld32(s_col, va);
+      tmem_ld_wait();
+      tmem_ld32(s_col + 32, vb);
+      exp_chunk(va, 0);
+      tmem_ld_wait();
+      tmem_ld32(s_col + 64, va);
+      exp_chunk(vb, 1);
+      tmem_ld_wait();
+      tmem_ld32(s_col + 96, vb);
+      exp_chunk(va, 2);
+      tmem_ld_wait();
+      exp_chunk(vb, 3);
       float s0, s1;
       f2_unpack(sum2, s0, s1);
       l = l * alpha + (s0 + s1);

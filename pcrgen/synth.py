@@ -11,7 +11,7 @@ import numpy as np
 __all__ = [
     "PRESETS", "make_rng", "f32_to_bf16_bits", "randn_bf16", "doc_tokens",
     "appendix_c_trace", "rag_request_tokens", "stress_values", "pack_store_slots",
-    "random_tiny_trace", "l8_request", "hit_ratio_request",
+    "random_tiny_trace", "l8_request", "hit_ratio_request", "zipf_trace",
 ]
 
 # Model geometry per preset (BASELINE.json configs[0..3]).
@@ -142,3 +142,27 @@ def random_tiny_trace(rng: np.random.Generator, C: int = 4, n_docs: int = 5,
         ql = int(rng.integers(query_len[0], query_len[1] + 1))
         reqs.append(np.concatenate(pick + [rng.integers(0, 50, size=ql, dtype=np.uint32)]))
     return reqs
+
+
+def zipf_trace(seed: int = 4, n_docs: int = 1000, n_requests: int = 1000, C: int = 256,
+               doc_chunks=(4, 16), zipf_s: float = 1.0, query_len=(128, 256)):
+    """configs[4] / SURVEY §8(d) preset Z: a corpus of n_docs documents of 4-16 chunks, doc
+    popularity Zipf(s) over a seeded random ranking; each request = 2 distinct docs (ordered,
+    drawn by popularity) + a 128-256-token query (2 docs per query).  Returns
+    (requests: list of uint32 token arrays, doc_ids: list of (a, b), n_doc_tokens: list)."""
+    rng = make_rng(seed)
+    docs = [rng.integers(0, VOCAB, size=C * int(rng.integers(doc_chunks[0], doc_chunks[1] + 1)),
+                         dtype=np.uint32) for _ in range(n_docs)]
+    ranks = rng.permutation(n_docs)
+    w = 1.0 / np.arange(1, n_docs + 1, dtype=np.float64) ** zipf_s
+    prob = np.empty(n_docs)
+    prob[ranks] = w / w.sum()
+    reqs, ids, ndoc = [], [], []
+    for _ in range(n_requests):
+        a, b = rng.choice(n_docs, size=2, replace=False, p=prob)
+        ql = int(rng.integers(query_len[0], query_len[1] + 1))
+        q = rng.integers(0, VOCAB, size=ql, dtype=np.uint32)
+        reqs.append(np.concatenate([docs[a], docs[b], q]))
+        ids.append((int(a), int(b)))
+        ndoc.append(len(docs[a]) + len(docs[b]))
+    return reqs, ids, ndoc
