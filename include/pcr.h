@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define PCR_ABI_VERSION 1
+#define PCR_ABI_VERSION 2
 
 typedef struct pcr_ctx pcr_ctx;
 
@@ -91,6 +91,12 @@ typedef struct pcr_config {
                             1 = copy engine, one cudaMemcpyBatchAsync per layer over all page
                             segments; 2 = copy engine, one cudaMemcpyAsync per page segment;
                             3 = experiment: TMA bulk copies host -> smem -> pool page */
+  /* SSD tier (§8 f2): a file of ssd_chunks chunk records behind the DRAM store.
+   * Committed chunks are written back asynchronously; chunks of requests in the
+   * look-ahead window that are only on the SSD are prefetched into DRAM by an I/O thread
+   * (P:456); a scheduled request's SSD-only chunks are loaded on demand.  NULL / 0 = no SSD. */
+  const char* ssd_path;
+  int64_t ssd_chunks;
 } pcr_config;
 
 /* Create a context.  Allocates the pinned store (mmap + NUMA-local mbind to the GPU's
@@ -135,7 +141,7 @@ typedef struct pcr_plan {
   uint8_t* evicted_keys; /* [n_evicted][16] keys evicted to make room, in eviction order */
   int32_t* evicted_slots;/* [n_evicted] their freed slots */
   int32_t cap_evicted;
-  int32_t reserved0;
+  int32_t n_from_ssd;    /* chunks of this chain loaded from the SSD on demand (ssd_to_gpu) */
 } pcr_plan;
 
 /* Plan one request (§4.2; Alg.1), in this order:
@@ -159,15 +165,28 @@ pcr_status pcr_match_prefix(pcr_ctx* ctx, int64_t req_id, const int64_t* pending
                             int32_t n_pending, pcr_plan* out);
 
 /* End of the step (Alg.1).  commit != 0: reserved chunks become RESIDENT
- * (their slot data must have been written: by offload, or by pcr_store_write);
+ * (their slot data must have been written: by offload, or by pcr_store_write) and, with an
+ * SSD tier, are queued for asynchronous write-back to the SSD;
  * commit == 0: reserved chunks are dropped deepest-first.  All pins are released and the
- * pool pages returned.  The request id is then forgotten. */
+ * pool pages returned.  SSD loads started by this request's match are drained first
+ * (DrainCompletedSSDLoads, Alg.1).  The request id is then forgotten. */
 pcr_status pcr_release(pcr_ctx* ctx, int64_t req_id, int32_t commit);
 
 /* Copy one chunk record ([L][Hkv_loc][2][C][d] bf16, pcr_slot_bytes bytes) into / out of
  * the pinned DRAM store.  Host memcpy; PCR_E_INVAL on a bad slot or null pointer. */
 pcr_status pcr_store_write(pcr_ctx* ctx, int32_t slot, const void* src);
 pcr_status pcr_store_read(const pcr_ctx* ctx, int32_t slot, void* dst);
+
+/* Cache-engine counters since creation (SSD tier and evictions). */
+typedef struct pcr_stats {
+  int64_t prefetch_loads;   /* SSD->DRAM loads submitted by the look-ahead prefetch phase */
+  int64_t ondemand_loads;   /* SSD->DRAM loads of a scheduled request's own chain */
+  int64_t writebacks;       /* DRAM->SSD write-backs of committed chunks */
+  int64_t ssd_evictions;    /* SSD records overwritten (LRU) */
+  int64_t dram_evictions;   /* DRAM leaves evicted */
+  int64_t ssd_bytes_read, ssd_bytes_written;
+} pcr_stats;
+pcr_status pcr_get_stats(const pcr_ctx* ctx, pcr_stats* out);
 
 /* Inspection for tests: the leaf list in LRU->MRU order as 16-byte keys. */
 pcr_status pcr_leaf_list(const pcr_ctx* ctx, uint8_t* keys, int32_t cap, int32_t* n_out);

@@ -29,9 +29,10 @@ SOURCES = [
     "kernels/kv_copy.cu",
     "kernels/suffix_attn.cu",
     "runtime/nccl_dl.cpp",
+    "runtime/ssd_io.cpp",
     "runtime/capi.cu",
 ]
-HEADERS = ["host/blake2b.h", "host/planner.h", "kernels/kernels.h", "kernels/sm100_ptx.cuh", "runtime/nccl_dl.h"]
+HEADERS = ["host/blake2b.h", "host/planner.h", "kernels/kernels.h", "kernels/sm100_ptx.cuh", "runtime/nccl_dl.h", "runtime/ssd_io.h"]
 
 
 def _mtime(p):

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../../include/pcr.h"
@@ -18,6 +19,7 @@
 #include "../host/planner.h"
 #include "../kernels/kernels.h"
 #include "nccl_dl.h"
+#include "ssd_io.h"
 
 using pcr::Planner;
 using pcr::Request;
@@ -52,6 +54,9 @@ struct pcr_ctx {
   int64_t ws_floats = 0;
   // multi-GPU output re-assembly (§8(e))
   void* nccl_comm = nullptr;
+  std::unique_ptr<pcr::SsdIo> ssd;    // SSD tier I/O thread (f2)
+  std::vector<int64_t> slot_write_seq; // per DRAM slot: last write-back task reading it
+  std::unordered_map<int64_t, int64_t> req_load_seq;  // request -> last SSD load it started
   std::vector<void*> ce_dst, ce_src;  // copy-engine baseline batch (load_mode 1/2)
   std::vector<size_t> ce_size;
   std::vector<cudaEvent_t> ev_attn;
@@ -348,7 +353,8 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
       k.head_dim < 8 || k.head_dim % 8 || k.world < 1 || k.rank < 0 || k.rank >= k.world ||
       k.n_kv_heads % k.world || k.chunk_tokens < 1 || k.page_tokens < 1 || k.chunk_tokens % k.page_tokens ||
       k.store_chunks < 1 || k.window < 0 || k.pool_bytes < 0 || k.max_inflight < 0 || k.max_tokens < 0 ||
-      k.gather_ctas < 0 || k.load_mode < 0 || k.load_mode > 3)
+      k.gather_ctas < 0 || k.load_mode < 0 || k.load_mode > 3 || k.ssd_chunks < 0 ||
+      (k.ssd_chunks > 0 && !k.ssd_path))
     return PCR_E_INVAL;
   auto c = std::make_unique<pcr_ctx>();
   c->cfg = k;
@@ -373,7 +379,7 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
   c->region_words = c->region_page_cap + (max_tokens + k.chunk_tokens - 1) / k.chunk_tokens;
   c->region_words = (c->region_words + 63) / 64 * 64;
   c->planner = std::make_unique<Planner>(k.chunk_tokens, k.page_tokens, k.store_chunks, c->n_pool_pages, k.window,
-                                         c->max_regions);
+                                         c->max_regions, k.ssd_chunks);
   c->geom = pcr::KvGeom{k.n_layers, c->hkv, k.head_dim, k.chunk_tokens, k.page_tokens, c->n_pool_pages,
                         c->slot_elems};
   if (k.gather_ctas > 0) c->gather_ctas = k.gather_ctas;
@@ -385,6 +391,15 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
   c->store = p;
   madvise(p, c->store_bytes, MADV_HUGEPAGE);
   c->h_arena = nullptr;
+  if (k.ssd_chunks > 0) {
+    c->ssd = std::make_unique<pcr::SsdIo>(k.ssd_path, k.ssd_chunks, c->slot_bytes);
+    if (!c->ssd->ok()) {
+      std::fprintf(stderr, "pcr_create: SSD tier: %s\n", c->ssd->error().c_str());
+      pcr_destroy(c.release());
+      return PCR_E_NOMEM;
+    }
+    c->slot_write_seq.assign(k.store_chunks, 0);
+  }
   if (c->device) {
     pcr_ctx* cp = c.get();
     cudaError_t e = cudaSetDevice(k.device);
@@ -463,6 +478,7 @@ void pcr_destroy(pcr_ctx* c) {
   } else {
     std::free(c->h_arena);
   }
+  c->ssd.reset();  // drains queued I/O before the store goes away
   if (c->store) munmap(c->store, c->store_bytes);
   delete c;
 }
@@ -491,12 +507,26 @@ pcr_status pcr_match_prefix(pcr_ctx* c, int64_t req_id, const int64_t* pending, 
                                        out->cap_evicted, &err);
   if (s != 0) return fail(c, static_cast<pcr_status>(s), err);
   const pcr::Plan& pl = r->plan;
+  if (c->ssd) {
+    // SSD -> DRAM loads (prefetch + on demand); reserved slots must not be overwritten while an
+    // earlier write-back still reads them; the chain's own loads complete before returning.
+    int64_t wait_seq = 0, last = 0;
+    uint8_t* store = static_cast<uint8_t*>(c->store);
+    for (const pcr::IoOp& op : pl.loads) {
+      last = c->ssd->read(op.ssd_slot, store + static_cast<size_t>(op.dram_slot) * c->slot_bytes);
+      if (op.wait_now) wait_seq = last;
+    }
+    for (int32_t slot : pl.new_slots) wait_seq = std::max(wait_seq, c->slot_write_seq[slot]);
+    if (last) c->req_load_seq[req_id] = last;
+    if (wait_seq && !c->ssd->wait(wait_seq)) return fail(c, PCR_E_INTERNAL, "SSD I/O failed");
+  }
   out->n_matched = pl.n_matched;
   out->n_reserved = pl.n_reserved;
   out->n1_tokens = pl.n1;
   out->n2_tokens = pl.n2;
   out->n_pages = static_cast<int32_t>(pl.pages.size());
   out->n_evicted = static_cast<int32_t>(pl.evicted.size());
+  out->n_from_ssd = pl.n_from_ssd;
   std::copy(pl.slots.begin(), pl.slots.end(), out->slots);
   std::copy(pl.pages.begin(), pl.pages.end(), out->pages);
   for (size_t i = 0; i < pl.evicted.size(); ++i) {
@@ -512,9 +542,33 @@ pcr_status pcr_match_prefix(pcr_ctx* c, int64_t req_id, const int64_t* pending, 
 
 pcr_status pcr_release(pcr_ctx* c, int64_t req_id, int32_t commit) {
   if (!c) return PCR_E_INVAL;
+  if (c->ssd) {  // DrainCompletedSSDLoads (Alg.1): loads this request's match started
+    auto it = c->req_load_seq.find(req_id);
+    if (it != c->req_load_seq.end()) {
+      if (c->planner->find(req_id) && !c->ssd->wait(it->second)) return fail(c, PCR_E_INTERNAL, "SSD I/O failed");
+    }
+  }
   std::string err;
-  int32_t s = c->planner->release(req_id, commit != 0, &err);
+  std::vector<pcr::IoOp> writes;
+  int32_t s = c->planner->release(req_id, commit != 0, &err, &writes);
   if (s != 0) return fail(c, static_cast<pcr_status>(s), err);
+  c->req_load_seq.erase(req_id);
+  uint8_t* store = static_cast<uint8_t*>(c->store);
+  for (const pcr::IoOp& op : writes)  // asynchronous write-back
+    c->slot_write_seq[op.dram_slot] = c->ssd->write(op.ssd_slot, store + static_cast<size_t>(op.dram_slot) * c->slot_bytes);
+  return PCR_OK;
+}
+
+pcr_status pcr_get_stats(const pcr_ctx* c, pcr_stats* out) {
+  if (!c || !out) return PCR_E_INVAL;
+  const pcr::TierStats& t = c->planner->stats();
+  out->prefetch_loads = t.prefetch;
+  out->ondemand_loads = t.ondemand;
+  out->writebacks = t.writeback;
+  out->ssd_evictions = t.ssd_evict;
+  out->dram_evictions = t.dram_evict;
+  out->ssd_bytes_read = c->ssd ? c->ssd->bytes_read() : 0;
+  out->ssd_bytes_written = c->ssd ? c->ssd->bytes_written() : 0;
   return PCR_OK;
 }
 

@@ -35,7 +35,8 @@ class PcrConfig(ctypes.Structure):
                 ("chunk_tokens", ctypes.c_int32), ("page_tokens", ctypes.c_int32),
                 ("store_chunks", ctypes.c_int64), ("window", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("pool", ctypes.c_void_p), ("pool_bytes", ctypes.c_int64), ("max_inflight", ctypes.c_int32),
-                ("max_tokens", ctypes.c_int32), ("gather_ctas", ctypes.c_int32), ("load_mode", ctypes.c_int32)]
+                ("max_tokens", ctypes.c_int32), ("gather_ctas", ctypes.c_int32), ("load_mode", ctypes.c_int32),
+                ("ssd_path", ctypes.c_char_p), ("ssd_chunks", ctypes.c_int64)]
 
 
 class PcrPlan(ctypes.Structure):
@@ -44,7 +45,14 @@ class PcrPlan(ctypes.Structure):
                 ("cap_slots", ctypes.c_int32), ("pages", ctypes.POINTER(ctypes.c_int32)),
                 ("cap_pages", ctypes.c_int32), ("n_pages", ctypes.c_int32), ("n_evicted", ctypes.c_int32),
                 ("evicted_keys", ctypes.POINTER(ctypes.c_uint8)), ("evicted_slots", ctypes.POINTER(ctypes.c_int32)),
-                ("cap_evicted", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
+                ("cap_evicted", ctypes.c_int32), ("n_from_ssd", ctypes.c_int32)]
+
+
+class PcrStats(ctypes.Structure):
+    _fields_ = [("prefetch_loads", ctypes.c_int64), ("ondemand_loads", ctypes.c_int64),
+                ("writebacks", ctypes.c_int64), ("ssd_evictions", ctypes.c_int64),
+                ("dram_evictions", ctypes.c_int64), ("ssd_bytes_read", ctypes.c_int64),
+                ("ssd_bytes_written", ctypes.c_int64)]
 
 
 class PcrRunOpts(ctypes.Structure):
@@ -80,6 +88,7 @@ PROTOTYPES = {
                                        _P(ctypes.c_float)]),
     "pcr_offload_layer_kv": (_I32, [_VP, _I64, _I32, _VP]),
     "pcr_run_prefill_ex": (_I32, [_VP, _I64, _VP, _VP, _VP, _VP, _P(PcrRunOpts)]),
+    "pcr_get_stats": (_I32, [_VP, _P(PcrStats)]),
 }
 
 _lib = None
@@ -139,14 +148,15 @@ class Context:
 
     def __init__(self, n_layers, n_q_heads, n_kv_heads, head_dim, chunk_tokens, page_tokens, store_chunks,
                  window, device=-1, pool=None, pool_bytes=None, rank=0, world=1, max_inflight=0, max_tokens=0,
-                 gather_ctas=0, load_mode=LOAD_SM_GATHER):
+                 gather_ctas=0, load_mode=LOAD_SM_GATHER, ssd_path=None, ssd_chunks=0):
         self.lib = load_library()
         if pool_bytes is None:
             pool_bytes = pool.numel() * pool.element_size() if hasattr(pool, "numel") else 0
         self._pool = pool
+        self._ssd_path = ssd_path.encode() if isinstance(ssd_path, str) else ssd_path
         cfg = PcrConfig(n_layers, n_q_heads, n_kv_heads, head_dim, rank, world, chunk_tokens, page_tokens,
                         store_chunks, window, device, _ptr(pool), int(pool_bytes), max_inflight, max_tokens,
-                        gather_ctas, load_mode)
+                        gather_ctas, load_mode, self._ssd_path, ssd_chunks)
         h = ctypes.c_void_p()
         st = self.lib.pcr_create(ctypes.byref(cfg), ctypes.byref(h))
         if st != 0:
@@ -180,6 +190,12 @@ class Context:
         return int(self.lib.pcr_slot_bytes(self.h))
 
     @property
+    def stats(self):
+        st = PcrStats()
+        self._check(self.lib.pcr_get_stats(self.h, ctypes.byref(st)), "pcr_get_stats")
+        return {f: getattr(st, f) for f, _ in PcrStats._fields_}
+
+    @property
     def kernel_launches(self):
         return int(self.lib.pcr_kernel_launches(self.h))
 
@@ -206,7 +222,7 @@ class Context:
         self._check(self.lib.pcr_match_prefix(self.h, req_id, pend.ctypes.data_as(_P(_I64)) if len(pend) else None,
                                               len(pend), ctypes.byref(plan)), "pcr_match_prefix")
         nm, nr, ne = plan.n_matched, plan.n_reserved, plan.n_evicted
-        return dict(n_matched=nm, n_reserved=nr, n1=plan.n1_tokens, n2=plan.n2_tokens,
+        return dict(n_matched=nm, n_reserved=nr, n1=plan.n1_tokens, n2=plan.n2_tokens, n_from_ssd=plan.n_from_ssd,
                     slots=slots[:nm + nr].tolist(), pages=pages[:plan.n_pages].tolist(),
                     evicted=[(bytes(ev_keys[i]), int(ev_slots[i])) for i in range(ne)])
 
