@@ -56,8 +56,13 @@ def parse():
     ap.add_argument("--gather-ctas", type=int, default=0, help="CTAs of the host->HBM gather (0 = library default)")
     ap.add_argument("--profile-steps", type=int, default=5, help="extra steps with per-layer events (after timing)")
     ap.add_argument("--window", type=int, default=4, help="look-ahead window W (Z trace)")
+    ap.add_argument("--layer-body", action="store_true",
+                    help="f3: stand-in layer body per layer (QKV / O projections + SwiGLU MLP GEMMs via "
+                         "cuBLAS) around the attention, driven through the per-layer C-ABI calls")
     ap.add_argument("--store-frac", type=float, default=0.10, help="Z: DRAM store size / distinct chunks")
     ap.add_argument("--requests", type=int, default=1000, help="Z: requests in the trace")
+    ap.add_argument("--ssd-frac", type=float, default=0.0, help="Z: SSD tier size / distinct chunks (0 = none)")
+    ap.add_argument("--ssd-path", default="/tmp/pcr_ssd_tier.bin", help="Z: SSD tier file")
     ap.add_argument("--load-mode", default="sm", choices=["sm", "ce_batch", "ce_blocks", "tma"],
                     help="a2 implementation: sm_100a gather kernel, or the paper's copy-engine paths")
     return ap.parse_args()
@@ -252,8 +257,12 @@ def run_ours(args):
         ctx.submit(-1, np.concatenate([doc[:N1], [1]]).astype(np.uint32))
         warm = ctx.match_prefix(-1, [])
         assert warm["n_reserved"] == n_chunks
-        for s in warm["slots"]:
-            ctx.store_write(s, randn_bf16(rng, (ctx.slot_bytes // 2,)))
+        # one N(0,1) record per 8 slots (rolled per slot): cheap to generate, finite bf16 values
+        base = None
+        for j, s in enumerate(warm["slots"]):
+            if j % 8 == 0:
+                base = randn_bf16(rng, (ctx.slot_bytes // 2,))
+            ctx.store_write(s, np.roll(base, j))
         ctx.release(-1, True)
     query = make_rng(8).integers(0, 128256, n_query, dtype=np.uint32)
     toks = np.concatenate([doc, query])
@@ -282,6 +291,40 @@ def run_ours(args):
     req_counter = [0]
     match_us = []
 
+    # f3 stand-in layer body: per layer, the suffix hidden state goes
+    # through Wq/Wk/Wv projections (producing this layer's q, k_new, v_new), the PCR attention,
+    # Wo and a SwiGLU MLP (Llama-3-8B widths, one random bf16 weight set shared by all layers).
+    # The host->HBM load of layer l+1 runs on the load stream meanwhile.
+    body = None
+    if args.layer_body:
+        assert world == 1, "--layer-body is single-GPU"
+        dm, dff = 4096, 14336
+        g = torch.Generator(device="cuda").manual_seed(5)
+        wgt = lambda i, o: (torch.randn(i, o, device="cuda", generator=g, dtype=torch.bfloat16) / i ** 0.5)  # noqa: E731
+        body = dict(wq=wgt(dm, hq * d), wk=wgt(dm, hkv * d), wv=wgt(dm, hkv * d), wo=wgt(hq * d, dm),
+                    wg=wgt(dm, dff), wu=wgt(dm, dff), wd=wgt(dff, dm),
+                    x=torch.randn(N2, dm, device="cuda", generator=g, dtype=torch.bfloat16))
+        ev_ld = [torch.cuda.Event() for _ in range(L)]
+
+    def run_with_layer_body(rid, out):
+        b = body
+        x = b["x"]
+        ls.wait_stream(cs)
+        for l in range(L):
+            ctx.load_layer_kv(rid, l, ls)
+            ev_ld[l].record(ls)
+            with torch.cuda.stream(cs):
+                qd = (x @ b["wq"]).view(N2, hq, d)
+                kd = (x @ b["wk"]).view(N2, hkv, d)
+                vd = (x @ b["wv"]).view(N2, hkv, d)
+                cs.wait_event(ev_ld[l])
+                ctx.prefill_attn_layer(rid, l, qd.view(torch.int16), kd.view(torch.int16), vd.view(torch.int16),
+                                       out[l], cs)
+                x = x + out[l].view(torch.bfloat16).view(N2, hq * d) @ b["wo"]
+                x = x + (torch.nn.functional.silu(x @ b["wg"]) * (x @ b["wu"])) @ b["wd"]
+        cs.wait_stream(ls)
+        return None
+
     def step(q, k, v, out, times=False, load_events=None):
         """One request.  The caller's stream sync precedes pcr_release (pages are reused)."""
         rid = req_counter[0]
@@ -293,7 +336,9 @@ def run_ours(args):
         assert plan["n1"] == N1, plan["n1"]
         if load_events:
             load_events[0].record(ls)
-        if world > 1:
+        if body is not None:
+            t = run_with_layer_body(rid, out)
+        elif world > 1:
             t = ctx.run_prefill_sharded(rid, q, k, v, out, gathered, cs, ls, xs, mode=mode, layer_times=times)
         else:
             t = ctx.run_prefill(rid, q, k, v, out, cs, ls, mode=mode, layer_times=times)
@@ -344,9 +389,12 @@ def run_ours(args):
     # duration, measured over the timed steps with two events per step on that stream.
     # append+attention: per-layer events on the compute stream, in extra profiling steps.
     gather_ms = float(np.mean(load_ms)) / L
-    lt = np.array([step(q_d, k_d, v_d, out_d, times=True) for _ in range(max(1, args.profile_steps))])
-    attn_ms = float(lt[:, :, 1].mean())
-    gather_ms_evented = float(lt[:, :, 0].mean())
+    if body is None:
+        lt = np.array([step(q_d, k_d, v_d, out_d, times=True) for _ in range(max(1, args.profile_steps))])
+        attn_ms = float(lt[:, :, 1].mean())
+        gather_ms_evented = float(lt[:, :, 0].mean())
+    else:   # per-layer events are not recorded on the layer-body path
+        attn_ms = gather_ms_evented = float("nan")
 
     # e2e: the same step through the C-ABI with HOST buffers (H2D of q/k/v, D2H of out, per step)
     e2e = None
@@ -396,9 +444,9 @@ def run_ours(args):
     bf16_peak = peaks.get("bf16_tflops", 1590.0)
     bf16_src = "MEASURED_PEAKS.json bf16_tflops (burst)" if "bf16_tflops" in peaks else "fallback 1590 (B200_PROFILING.md)"
     gather_gbs = load_bytes / (gather_ms * 1e-3) / 1e9 if N1 else 0.0
-    attn_tflops = attn_flops / (attn_ms * 1e-3) / 1e12
+    attn_tflops = attn_flops / (attn_ms * 1e-3) / 1e12 if attn_ms == attn_ms else None
     # two in-order streams, identical layers: T* = t_ld + (L-1) max(t_ld, t_at) + t_at
-    ttft_pred = gather_ms + (L - 1) * max(gather_ms, attn_ms) + attn_ms
+    ttft_pred = gather_ms + (L - 1) * max(gather_ms, attn_ms) + attn_ms if attn_tflops else None
     value = args.steps * N / (total_ms * 1e-3)
 
     cpu = None
@@ -411,27 +459,30 @@ def run_ours(args):
         if world > 1:
             dist.destroy_process_group()
         return
-    dominant = "kv_gather" if N1 and gather_ms >= attn_ms else "suffix_attn"
+    dominant = "kv_gather" if N1 and (attn_ms != attn_ms or gather_ms >= attn_ms) else "suffix_attn"
     rl_gather = {"bound": "host-link", "kernel": "kv_gather" if load_mode == 0 else f"copy engine ({args.load_mode})", "achieved": gather_gbs, "peak": peak_h2d,
                  "unit": "GB/s", "frac": gather_gbs / peak_h2d, "traffic": None,
                  "peak_source": "live: cudaMemcpyAsync H2D from pinned host, 256 MiB, best of 5",
                  "algorithmic_bytes_per_launch": load_bytes, "avg_launch_ms": gather_ms}
-    rl_attn = {"bound": "tensor", "kernel": "kv_append+suffix_attn", "achieved": attn_tflops, "peak": bf16_peak,
-               "unit": "TFLOP/s", "frac": attn_tflops / bf16_peak, "traffic": None, "peak_source": bf16_src,
-               "algorithmic_flops_per_launch": attn_flops, "avg_launch_ms": attn_ms}
+    rl_attn = None if attn_tflops is None else {
+        "bound": "tensor", "kernel": "kv_append+suffix_attn", "achieved": attn_tflops, "peak": bf16_peak,
+        "unit": "TFLOP/s", "frac": attn_tflops / bf16_peak, "traffic": None, "peak_source": bf16_src,
+        "algorithmic_flops_per_launch": attn_flops, "avg_launch_ms": attn_ms}
     line = {
         "metric": f"reuse-prefill tokens/s ({args.workload}: context tokens N1+N2 per second; TTFT in ttft_ms)",
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) bf16 KV/Q, random token ids)",
         "config": {"workload": f"{args.workload}: {L}L {Hq}/{Hkv} heads d={d}, N1={N1} cached (host DRAM) + "
-                               f"N2={N2} computed, B=1, C={C}, S_pg={S}, mode={args.mode}, load={args.load_mode}",
+                               f"N2={N2} computed, B=1, C={C}, S_pg={S}, mode={args.mode}, load={args.load_mode}"
+                               + (", +layer body (f3)" if body is not None else ""),
                    "N1": N1, "N2": N2, "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
                    "l2": f"inputs > L2: {L * load_bytes / 2**20:.0f} MiB of prefix KV streamed from host per step"},
         "ttft_ms": statistics.median(step_ms), "ttft_ms_p90": float(np.percentile(step_ms, 90)),
-        "ttft_pred_ms": ttft_pred, "sync_bound_ms": L * (gather_ms + attn_ms),
-        "gather_ms_per_layer": gather_ms, "gather_ms_per_layer_evented": gather_ms_evented,
-        "attn_ms_per_layer": attn_ms, "gather_ctas": args.gather_ctas or 16,
+        "ttft_pred_ms": ttft_pred, "sync_bound_ms": L * (gather_ms + attn_ms) if attn_tflops else None,
+        "gather_ms_per_layer": gather_ms,
+        "gather_ms_per_layer_evented": gather_ms_evented if attn_tflops else None,
+        "attn_ms_per_layer": attn_ms if attn_tflops else None, "gather_ctas": args.gather_ctas or 16,
         "match_prefix_us": statistics.median(match_us),
         "gpu_launches": launches,
         "roofline": rl_gather if dominant == "kv_gather" else rl_attn,
@@ -467,8 +518,10 @@ def run_trace_z(args):
     page_elems = L * Hkv * 2 * S * d
     pool = torch.empty(2 * pages_req * page_elems + page_elems, dtype=torch.int16, device="cuda")
     t0 = time.perf_counter()
+    ssd_chunks = int(args.ssd_frac * len(distinct))
     ctx = Context(L, Hq, Hkv, d, C, S, cap, args.window, device=0, pool=pool, max_tokens=max_n,
-                  gather_ctas=args.gather_ctas)
+                  gather_ctas=args.gather_ctas, ssd_path=args.ssd_path if ssd_chunks else None,
+                  ssd_chunks=ssd_chunks)
     t_pin = time.perf_counter() - t0
     rng = make_rng(11)
     max_n2 = max_n
@@ -479,7 +532,7 @@ def run_trace_z(args):
     cs, ls, os_ = torch.cuda.Stream(), torch.cuda.Stream(priority=-1), torch.cuda.Stream()
     for i, (t, n) in enumerate(zip(reqs, ndoc)):
         ctx.submit(i, t, n)
-    ttft, hits, chunks, toks, n1s, plan_us = [], 0, 0, 0, [], []
+    ttft, wall, hits, chunks, toks, n1s, plan_us = [], [], 0, 0, 0, [], []
     launches0 = ctx.kernel_launches
     clocks = ClockSampler(0)
     clocks.start()
@@ -505,6 +558,7 @@ def run_trace_z(args):
         b.record(cs)
         b.synchronize()
         ttft.append(a.elapsed_time(b))
+        wall.append((time.perf_counter() - tp) * 1e3)   # host plan (+ on-demand SSD loads) + GPU
         ctx.release(i, True)
         hits += plan["n_matched"]
         chunks += ndoc[i] // C
@@ -522,8 +576,11 @@ def run_trace_z(args):
         "dtype": "bf16", "data": "synthetic (seeded Zipf(1.0) corpus of 1000 docs x 4-16 chunks, 2 docs + "
                                    "128-256 query tokens per request; random bf16 KV)",
         "config": {"workload": f"Z: L8 shape, W={args.window}, store={cap} chunks "
-                               f"({args.store_frac:.0%} of {len(distinct)} distinct), offload on",
-                   "requests": len(reqs), "window": args.window, "store_chunks": cap},
+                               f"({args.store_frac:.0%} of {len(distinct)} distinct), ssd={ssd_chunks} chunks, "
+                               f"offload on",
+                   "requests": len(reqs), "window": args.window, "store_chunks": cap, "ssd_chunks": ssd_chunks},
+        "ttft_wall_ms_mean": float(np.mean(wall)), "ttft_wall_ms_p95": float(np.percentile(wall, 95)),
+        "tier_stats": ctx.stats,
         "ttft_ms_mean": float(tt.mean()), "ttft_ms_p50": float(np.percentile(tt, 50)),
         "ttft_ms_p95": float(np.percentile(tt, 95)), "ttft_ms_p99": float(np.percentile(tt, 99)),
         "chunk_hit_ratio": hits / max(1, chunks), "mean_n1_tokens": float(np.mean(n1s)),

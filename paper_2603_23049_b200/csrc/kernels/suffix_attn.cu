@@ -165,58 +165,88 @@ __global__ void __maxnreg__(136)
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
-    if (lane == 0 && n_iter > 0) {
-      mbar_arrive_expect_tx(&bars->q_full, kNQ * Lay::kTileBytes);
-      for (int t = 0; t < kNQ; ++t)
-        for (int hf = 0; hf < Lay::kHalves; ++hf)
-          tma_load_3d(smem + Lay::kQ0 + t * Lay::kTileBytes + hf * kHalfBytes, &tmap_q, hf * 64, g * G,
-                      i0 + t * tok_per_tile, &bars->q_full);
+    // Converged warp; one elected lane issues the copies of each stage.
+    if (n_iter > 0) {
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&bars->q_full, kNQ * Lay::kTileBytes);
+        for (int t = 0; t < kNQ; ++t)
+          for (int hf = 0; hf < Lay::kHalves; ++hf)
+            tma_load_3d(smem + Lay::kQ0 + t * Lay::kTileBytes + hf * kHalfBytes, &tmap_q, hf * 64, g * G,
+                        i0 + t * tok_per_tile, &bars->q_full);
+      }
+      __syncwarp();
       const int64_t layer_rows = p.n_pool_pages * p.hkv * 2 * p.S;
       for (int it = 0; it < n_iter; ++it) {
         const int j = j_begin + it;
         const int st = it & 1;
         if (it >= 2) mbar_wait(&bars->kv_empty[st], ((it >> 1) - 1) & 1);
-        uint8_t* ks = smem + Lay::kK0 + st * Lay::kTileBytes;
-        uint8_t* vs = smem + Lay::kV0 + st * Lay::kTileBytes;
-        mbar_arrive_expect_tx(&bars->k_full[st], Lay::kTileBytes);
-        mbar_arrive_expect_tx(&bars->v_full[st], Lay::kTileBytes);
-        for (int pp = 0; pp < pages_per_tile; ++pp) {
-          const int pidx = min(j * pages_per_tile + pp, p.n_req_pages - 1);  // clamp: finite, masked
-          const int64_t page = p.pages[pidx];
-          const int64_t row_k = int64_t(p.layer) * layer_rows + ((page * p.hkv + g) * 2 + 0) * p.S;
+        // page rows of this tile, one per lane (pages_per_tile <= 8)
+        const int pidx = min(j * pages_per_tile + lane, p.n_req_pages - 1);  // clamp: finite, masked
+        const int64_t my_row = int64_t(p.layer) * layer_rows + ((int64_t(p.pages[pidx]) * p.hkv + g) * 2) * p.S;
+        int32_t rows[8];
 #pragma unroll
-          for (int hf = 0; hf < Lay::kHalves; ++hf)
-            tma_load_2d(ks + hf * kHalfBytes + pp * p.S * 128, &tmap_pool, hf * 64, int32_t(row_k), &bars->k_full[st]);
+        for (int pp = 0; pp < 8; ++pp) rows[pp] = int32_t(__shfl_sync(0xffffffffu, my_row, pp));
+        if (elect_one()) {
+          uint8_t* ks = smem + Lay::kK0 + st * Lay::kTileBytes;
+          uint8_t* vs = smem + Lay::kV0 + st * Lay::kTileBytes;
+          mbar_arrive_expect_tx(&bars->k_full[st], Lay::kTileBytes);
+          mbar_arrive_expect_tx(&bars->v_full[st], Lay::kTileBytes);
 #pragma unroll
-          for (int hf = 0; hf < Lay::kHalves; ++hf)
-            tma_load_2d(vs + hf * kHalfBytes + pp * p.S * 128, &tmap_pool, hf * 64, int32_t(row_k + p.S),
-                        &bars->v_full[st]);
+          for (int pp = 0; pp < 8; ++pp) {
+            if (pp < pages_per_tile) {
+              const int32_t row_k = rows[pp];
+#pragma unroll
+              for (int hf = 0; hf < Lay::kHalves; ++hf)
+                tma_load_2d(ks + hf * kHalfBytes + pp * p.S * 128, &tmap_pool, hf * 64, row_k, &bars->k_full[st]);
+#pragma unroll
+              for (int hf = 0; hf < Lay::kHalves; ++hf)
+                tma_load_2d(vs + hf * kHalfBytes + pp * p.S * 128, &tmap_pool, hf * 64, row_k + p.S,
+                            &bars->v_full[st]);
+            }
+          }
         }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0 && n_iter > 0) {
+    // The whole warp runs the loop (converged); one elected lane issues each MMA group.
+    if (n_iter > 0) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(kBlockM, kBlockN, 0, 0);
       constexpr uint32_t idesc_o = idesc_bf16_f32(kBlockM, D, 0, 1);
       mbar_wait(&bars->q_full, 0);
+      // Descriptor bases computed once; a K step only adds (byte offset >> 4) to the start
+      // address field (addresses < 256 KB, so the 14-bit field never carries).
+      // (selected with ternaries, not indexed arrays, so they stay in registers)
+      const uint64_t q_desc0 = smem_desc_sw128(smem_u32(smem + Lay::kQ0), 16, 1024);
+      const uint64_t q_desc1 = q_desc0 + (Lay::kTileBytes >> 4);
+      const uint64_t k_desc0 = smem_desc_sw128(smem_u32(smem + Lay::kK0), 16, 1024);
+      const uint64_t k_desc1 = k_desc0 + (Lay::kTileBytes >> 4);
+      const uint64_t v_desc0 = smem_desc_sw128(smem_u32(smem + Lay::kV0), kHalfBytes, 1024);
+      const uint64_t v_desc1 = v_desc0 + (Lay::kTileBytes >> 4);
+      static_assert(kNQ == 2, "descriptor selection assumes two Q tiles");
       auto issue_s = [&](int t, int it) {
-        const uint32_t q_addr = smem_u32(smem + Lay::kQ0 + t * Lay::kTileBytes);
-        const uint32_t k_addr = smem_u32(smem + Lay::kK0 + (it & 1) * Lay::kTileBytes);
+        const uint64_t qd = t ? q_desc1 : q_desc0, kd = (it & 1) ? k_desc1 : k_desc0;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-          mma_bf16_ss(tmem + Lay::kColS + t * kBlockN, smem_desc_sw128(q_addr + off, 16, 1024),
-                      smem_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t off = ((kk >> 2) * kHalfBytes + (kk & 3) * 32) >> 4;
+            mma_bf16_ss(tmem + Lay::kColS + t * kBlockN, qd + off, kd + off, idesc_s, kk > 0);
+          }
+          mma_commit(&bars->s_full[t]);
         }
-        mma_commit(&bars->s_full[t]);
+        __syncwarp();
       };
       auto issue_pv = [&](int t, int it) {
-        const uint32_t v_addr = smem_u32(smem + Lay::kV0 + (it & 1) * Lay::kTileBytes);
+        const uint64_t vd = (it & 1) ? v_desc1 : v_desc0;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < kBlockN / 16; ++kk)
-          mma_bf16_ts(tmem + Lay::kColO + t * D, tmem + Lay::kColS + t * kBlockN + kk * 8,
-                      smem_desc_sw128(v_addr + kk * 2048, kHalfBytes, 1024), idesc_o, (it > 0 || kk > 0));
+          for (int kk = 0; kk < kBlockN / 16; ++kk)
+            mma_bf16_ts(tmem + Lay::kColO + t * D, tmem + Lay::kColS + t * kBlockN + kk * 8, vd + (kk * 2048 >> 4),
+                        idesc_o, (it > 0 || kk > 0));
+          if (t == kNQ - 1) mma_commit(&bars->kv_empty[it & 1]);
+        }
+        __syncwarp();
       };
       mbar_wait(&bars->k_full[0], 0);
       tc_fence_after();
@@ -229,7 +259,6 @@ __global__ void __maxnreg__(136)
           mbar_wait(&bars->p_full[t], it & 1);
           tc_fence_after();
           issue_pv(t, it);
-          if (t == kNQ - 1) mma_commit(&bars->kv_empty[st]);
           if (more) {
             if (t == 0) {  // K(j+1) is only needed here, after PV_0(j) has been queued
               mbar_wait(&bars->k_full[st ^ 1], ((it + 1) >> 1) & 1);
@@ -239,7 +268,8 @@ __global__ void __maxnreg__(136)
           }
         }
       }
-      mma_commit(&bars->o_full);
+      if (elect_one()) mma_commit(&bars->o_full);
+      __syncwarp();
     }
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- softmax / epilogue
@@ -265,14 +295,15 @@ __global__ void __maxnreg__(136)
       tc_fence_after();
       // TMEM loads are software-pipelined: chunk c+1 is in flight while chunk c is processed.
       float va[32], vb[32];
-      float rowmax = -INFINITY;
+      // four independent max chains (a single FMNMX3 chain would be 64 dependent ops per tile)
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
       auto max_chunk = [&](float* v, int c) {
         if (diag) {
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = (key0 + c * 32 + e <= limit) ? v[e] : -INFINITY;
         }
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) rowmax = fmax3(rowmax, v[e], v[e + 1]);
+        for (int e = 0; e < 32; e += 2) mx4[(e >> 1) & 3] = fmax3(mx4[(e >> 1) & 3], v[e], v[e + 1]);
       };
       tmem_ld32(s_col, va);
       tmem_ld_wait();
@@ -286,6 +317,7 @@ __global__ void __maxnreg__(136)
       max_chunk(va, 2);
       tmem_ld_wait();
       max_chunk(vb, 3);
+      const float rowmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
       const float m_new = fmaxf(m_raw, rowmax);
       const bool rescale = (m_new - m_raw) * p.scale_log2 > kRescaleThreshold;
       const float m_use = rescale ? m_new : m_raw;
@@ -304,7 +336,7 @@ __global__ void __maxnreg__(136)
           tmem_st32(o_col + c * 32, o);
         }
       }
-      uint64_t sum2 = 0;
+      uint64_t sum4[4] = {0, 0, 0, 0};  // four independent FADD2 chains
       auto exp_chunk = [&](float* v, int c) {
         if (diag) {
 #pragma unroll
@@ -327,7 +359,7 @@ __global__ void __maxnreg__(136)
           const uint32_t w = *reinterpret_cast<uint32_t*>(&b);
           pk[e / 2] = w;
           // row sum of the same bf16-rounded weights (R18), two lanes per FADD2
-          sum2 = fadd2(sum2, f2_pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u)));
+          sum4[(e >> 1) & 3] = fadd2(sum4[(e >> 1) & 3], f2_pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u)));
         }
         tmem_st16(s_col + c * 16, pk);   // P chunk c -> columns [16c, 16c+16): already read
       };
@@ -344,7 +376,7 @@ __global__ void __maxnreg__(136)
       tmem_ld_wait();
       exp_chunk(vb, 3);
       float s0, s1;
-      f2_unpack(sum2, s0, s1);
+      f2_unpack(fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3])), s0, s1);
       l = l * alpha + (s0 + s1);
       tmem_st_wait();
       tc_fence_before();

@@ -1,0 +1,64 @@
+"""Attention-only microbenchmark through the C-ABI (pcr_prefill_attn_layer, append + attention),
+for comparing suffix_attn variants quickly.  Prints one JSON line per shape.
+
+    python tools/attn_bench.py [--iters 20]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2603_23049_b200 import Context  # noqa: E402
+from pcrgen import make_rng, randn_bf16  # noqa: E402
+
+
+def run(n1, n2, hq, hkv, d=128, L=4, iters=20, C=256, S=64):
+    rng = make_rng(3)
+    N = n1 + n2
+    n_pages = 2 * (-(-N // S)) + 4
+    pool = torch.empty(n_pages * L * hkv * 2 * S * d, dtype=torch.int16, device="cuda")
+    ctx = Context(L, hq, hkv, d, C, S, n1 // C + 2, 0, device=0, pool=pool)
+    doc = rng.integers(0, 1000, n1, dtype=np.uint32)
+    if n1:
+        ctx.submit(0, np.concatenate([doc, [1]]).astype(np.uint32))
+        w = ctx.match_prefix(0, [])
+        rec = randn_bf16(rng, (ctx.slot_bytes // 2,))
+        for s in w["slots"]:
+            ctx.store_write(s, rec)
+        ctx.release(0, True)
+    ctx.submit(1, np.concatenate([doc, rng.integers(0, 1000, n2, dtype=np.uint32)]), n_cacheable=n1)
+    plan = ctx.match_prefix(1, [])
+    assert plan["n1"] == n1
+    dev = lambda a: torch.from_numpy(a.view(np.int16)).cuda()  # noqa: E731
+    q = dev(randn_bf16(rng, (L, n2, hq, d)))
+    k = dev(randn_bf16(rng, (L, n2, hkv, d)))
+    v = dev(randn_bf16(rng, (L, n2, hkv, d)))
+    o = torch.empty_like(q)
+    cs, ls = torch.cuda.Stream(), torch.cuda.Stream()
+    ctx.run_prefill(1, q, k, v, o, cs, ls)   # loads the pool, warms up
+    cs.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(cs)
+    for _ in range(iters):
+        for l in range(L):
+            ctx.prefill_attn_layer(1, l, q[l], k[l], v[l], o[l], cs)
+    b.record(cs)
+    b.synchronize()
+    ms = a.elapsed_time(b) / (iters * L)
+    flops = 4 * hq * d * (n2 * n1 + n2 * (n2 + 1) // 2)
+    ctx.release(1, False)
+    ctx.close()
+    return dict(n1=n1, n2=n2, hq=hq, hkv=hkv, ms_per_layer=ms, tflops=flops / ms / 1e9)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=20)
+    args = ap.parse_args()
+    for n1, n2, hq, hkv in [(0, 8320, 32, 8), (4096, 4224, 32, 8), (6144, 2176, 32, 8), (4096, 128, 32, 8),
+                            (8192, 8320, 64, 8)]:
+        print(json.dumps(run(n1, n2, hq, hkv, iters=args.iters)), flush=True)

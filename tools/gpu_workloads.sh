@@ -1,0 +1,26 @@
+#!/bin/bash
+# Workload coverage: Z trace (W sweep, DRAM only / + SSD tier), f3 layer body, L70, T.
+mkdir -p gpurun_out
+export PYTHONUNBUFFERED=1
+OUT=gpurun_out/workloads.jsonl; : > $OUT
+df -h /tmp | tail -1 > gpurun_out/disk.txt
+for W in 0 4; do
+  timeout 900 python bench.py --workload Z --window $W >> $OUT 2>> gpurun_out/workloads.err; echo "Z W=$W rc=$?"
+done
+timeout 900 python bench.py --workload Z --window 4 --store-frac 0.03 --ssd-frac 0.25 >> $OUT 2>> gpurun_out/workloads.err; echo "Z ssd rc=$?"
+timeout 900 python bench.py --workload Z --window 0 --store-frac 0.03 --ssd-frac 0.25 >> $OUT 2>> gpurun_out/workloads.err; echo "Z ssd W0 rc=$?"
+timeout 300 python bench.py --steps 10 --warmup 2 --no-e2e --no-cpu-baseline --layer-body >> $OUT 2>> gpurun_out/workloads.err; echo "f3 L8 rc=$?"
+timeout 300 python bench.py --workload M7 --ratio 0.5 --steps 10 --warmup 2 --no-e2e --no-cpu-baseline --layer-body >> $OUT 2>> gpurun_out/workloads.err; echo "f3 M7 rc=$?"
+timeout 300 python bench.py --workload M7 --ratio 1.0 --steps 10 --warmup 2 --no-e2e --no-cpu-baseline --layer-body >> $OUT 2>> gpurun_out/workloads.err; echo "f3 M7 r1 rc=$?"
+for r in 0.5 1.0; do
+  timeout 600 python bench.py --workload L70 --ratio $r --steps 5 --warmup 2 --no-e2e --no-cpu-baseline >> $OUT 2>> gpurun_out/workloads.err; echo "L70 $r rc=$?"
+done
+timeout 300 python bench.py --workload T --steps 20 --warmup 3 --no-e2e --no-cpu-baseline >> $OUT 2>> gpurun_out/workloads.err; echo "T rc=$?"
+python - <<'PY'
+import json
+for l in open("gpurun_out/workloads.jsonl"):
+    j=json.loads(l)
+    keep={k:j.get(k) for k in ("value","ttft_ms","ttft_ms_mean","ttft_ms_p95","ttft_wall_ms_mean","chunk_hit_ratio","gather_ms_per_layer","attn_ms_per_layer","tier_stats")}
+    print(j["config"]["workload"][:110], json.dumps(keep))
+PY
+tail -5 gpurun_out/workloads.err
