@@ -129,10 +129,14 @@ __global__ void __maxnreg__(136)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int g = blockIdx.y;  // local kv head
+  // Longest-processing-time-first order: with causal masking the last M-blocks see the most
+  // keys, so CTA c runs M-block (n_mblocks - 1 - c / hkv) of kv head c % hkv (heads interleaved).
   const int G = p.hq / p.hkv;
   const int tok_per_tile = kBlockM / G;
-  const int i0 = blockIdx.x * kNQ * tok_per_tile;
+  const int n_mblocks = (p.n2 + kNQ * tok_per_tile - 1) / (kNQ * tok_per_tile);
+  const int g = blockIdx.x % p.hkv;  // local kv head
+  const int mblock = n_mblocks - 1 - blockIdx.x / p.hkv;
+  const int i0 = mblock * kNQ * tok_per_tile;
   const int i_end = min(i0 + kNQ * tok_per_tile, p.n2);
   const int n_tiles_all = (p.n1 + i_end + kBlockN - 1) / kBlockN;
   const int per_split = (n_tiles_all + p.n_splits - 1) / p.n_splits;
@@ -526,7 +530,7 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
     splits = int(std::min<int64_t>(splits, std::max<int64_t>(1, p.ws_bytes / per_split_bytes)));
   }
   p.n_splits = splits;
-  dim3 grid(n_mblocks, p.hkv, splits);
+  dim3 grid(n_mblocks * p.hkv, 1, splits);
   kern<<<grid, kThreads, Layout<D>::kAlloc, stream>>>(*tmap_pool, tmap_q, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
