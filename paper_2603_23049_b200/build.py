@@ -27,7 +27,7 @@ SOURCES = [
     "host/blake2b.cpp",
     "host/planner.cpp",
     "kernels/kv_copy.cu",
-    "kernels/suffix_attn.cu",
+    os.environ.get("PCR_ATTN_SRC", "kernels/suffix_attn.cu"),   # experiment knob
     "runtime/nccl_dl.cpp",
     "runtime/ssd_io.cpp",
     "runtime/capi.cu",

@@ -55,6 +55,8 @@ struct AttnParams {
 // a4: suffix-query causal attention over the request's pool pages (tcgen05 + TMEM + TMA).
 // `tmap_pool` is a 2D tensor map over the pool viewed as [rows][d] (rows = L*pages*Hkv*2*S),
 // box {64, S}, SWIZZLE_128B.
+// Rows of the pool tensor map's TMA box the attention kernel expects (S_pg, or a 64-row part).
+int32_t attn_pool_box_rows(int32_t S);
 // `launches` is incremented by the number of kernels enqueued (attention [+ split-KV combine]).
 cudaError_t launch_suffix_attn(const CUtensorMap* tmap_pool, const AttnParams& p, int32_t d,
                                cudaStream_t stream, int* launches);

@@ -7,6 +7,8 @@
 // the request.  Measured on this pool's B200 (tools/h2d_probe.cu): 8+ CTAs x 256 threads with
 // 4 loads in flight per thread reach 51.2 GB/s = 92% of the copy engine's 55.6 GB/s, so the
 // gather needs only a handful of SMs and leaves the rest to the concurrent attention.
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace pcr {
@@ -26,39 +28,46 @@ __device__ __forceinline__ uint4 ld_host_stream(const uint4* p) {
   return v;
 }
 
-// grid = (ctas_per_chunk, n_matched).  Chunk c's layer block in the store is contiguous:
-// [Hkv][2][C][d] starting at store + slot*slot_elems + layer*Hkv*2*C*d.
+// The copy is a list of page segments: for chunk c (chain index), kv head h, K/V and page pp of
+// the chunk, S*d*2 contiguous bytes in the store slot map to S*d*2 contiguous bytes of one pool
+// page.  Each warp copies whole segments (address math once per segment, not per 16 bytes), every
+// lane keeping kUnroll independent 16-byte loads in flight.  grid-stride over segments.
+__device__ __forceinline__ void segment_addrs(int64_t seg, int32_t chunk0, int32_t layer, const KvGeom& g,
+                                              int32_t ppc_log2, int32_t row16_log2, const int32_t* slots,
+                                              const int32_t* pages, int64_t& store16, int64_t& pool16) {
+  const int32_t pp = int32_t(seg & ((1 << ppc_log2) - 1));
+  const int64_t hk = (seg >> ppc_log2) % (int64_t(g.Hkv) * 2);           // h*2 + kv
+  const int32_t c = chunk0 + int32_t((seg >> ppc_log2) / (int64_t(g.Hkv) * 2));
+  const int64_t seg16 = int64_t(g.S) << row16_log2;                       // 16-byte units per segment
+  store16 = (int64_t(slots[c]) * g.slot_elems + int64_t(layer) * g.Hkv * 2 * g.C * g.d) / 8 +
+            (hk * g.C << row16_log2) + pp * seg16;
+  const int64_t page = pages[(int64_t(c) << ppc_log2) + pp];
+  pool16 = ((int64_t(layer) * g.n_pool_pages + page) * g.Hkv * 2 + hk) * seg16;
+}
+
 __global__ void __launch_bounds__(kThreads, 6) kv_gather_kernel(const uint4* __restrict__ store,
                                                              uint4* __restrict__ pool,
                                                              const int32_t* __restrict__ slots,
-                                                             const int32_t* __restrict__ pages, int32_t layer,
-                                                             KvGeom g, int32_t row16_log2, int32_t C_log2,
-                                                             int32_t S_log2) {
-  const int32_t c = blockIdx.y;
-  const int64_t row16 = int64_t(1) << row16_log2;            // 16-byte units per d-row
-  const int64_t block16 = int64_t(g.Hkv) * 2 * g.C * row16;   // units of one chunk-layer
-  const uint4* src = store + (int64_t(slots[c]) * g.slot_elems + int64_t(layer) * g.Hkv * 2 * g.C * g.d) / 8;
-  const int64_t page16 = int64_t(g.Hkv) * 2 * g.S * row16;
-  uint4* dst_layer = pool + int64_t(layer) * g.n_pool_pages * page16;
-  const int64_t stride = int64_t(gridDim.x) * kThreads;
-  for (int64_t base = int64_t(blockIdx.x) * kThreads + threadIdx.x; base < block16; base += stride * kUnroll) {
-    uint4 v[kUnroll];
+                                                             const int32_t* __restrict__ pages, int32_t n_chunks,
+                                                             int32_t layer, KvGeom g, int32_t row16_log2,
+                                                             int32_t ppc_log2) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_seg = (int64_t(n_chunks) * g.Hkv * 2) << ppc_log2;
+  const int32_t seg16 = g.S << row16_log2;
+  const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
+  for (int64_t seg = int64_t(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5); seg < n_seg; seg += warps) {
+    int64_t s16, p16;
+    segment_addrs(seg, 0, layer, g, ppc_log2, row16_log2, slots, pages, s16, p16);
+    const uint4* src = store + s16;
+    uint4* dst = pool + p16;
+    for (int32_t base = lane; base < seg16; base += 32 * kUnroll) {
+      uint4 v[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t o = base + u * stride;
-      if (o < block16) v[u] = ld_host_stream(src + o);
-    }
+      for (int u = 0; u < kUnroll; ++u)
+        if (base + 32 * u < seg16) v[u] = ld_host_stream(src + base + 32 * u);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t o = base + u * stride;
-      if (o < block16) {
-        const int64_t row = o >> row16_log2;
-        const int64_t col = o & (row16 - 1);
-        const int64_t hk = row >> C_log2;               // h*2 + kv
-        const int64_t tt = (int64_t(c) << C_log2) + (row & (g.C - 1));
-        const int64_t page = pages[tt >> S_log2];
-        dst_layer[page * page16 + ((hk << S_log2) + (tt & (g.S - 1))) * row16 + col] = v[u];
-      }
+      for (int u = 0; u < kUnroll; ++u)
+        if (base + 32 * u < seg16) dst[base + 32 * u] = v[u];
     }
   }
 }
@@ -99,38 +108,30 @@ __global__ void kv_append_kernel(const uint4* __restrict__ k_new, const uint4* _
 
 // f1 offload (the inverse of the gather): layer `layer` of every reserved chunk, pool pages ->
 // pinned host store slot, 16-byte loads from HBM and 16-byte stores over PCIe into the mapped
-// store.  grid = (ctas_per_chunk, n_chunks); chunk c is chain index chunk0 + c.
+// store, page segment by page segment (see kv_gather_kernel).
 __global__ void __launch_bounds__(kThreads, 6) kv_scatter_kernel(const uint4* __restrict__ pool,
                                                               uint4* __restrict__ store,
                                                               const int32_t* __restrict__ slots,
                                                               const int32_t* __restrict__ pages, int32_t chunk0,
-                                                              int32_t layer, KvGeom g, int32_t row16_log2,
-                                                              int32_t C_log2, int32_t S_log2) {
-  const int32_t c = chunk0 + blockIdx.y;
-  const int64_t row16 = int64_t(1) << row16_log2;
-  const int64_t block16 = int64_t(g.Hkv) * 2 * g.C * row16;
-  uint4* dst = store + (int64_t(slots[c]) * g.slot_elems + int64_t(layer) * g.Hkv * 2 * g.C * g.d) / 8;
-  const int64_t page16 = int64_t(g.Hkv) * 2 * g.S * row16;
-  const uint4* src_layer = pool + int64_t(layer) * g.n_pool_pages * page16;
-  const int64_t stride = int64_t(gridDim.x) * kThreads;
-  for (int64_t base = int64_t(blockIdx.x) * kThreads + threadIdx.x; base < block16; base += stride * kUnroll) {
-    uint4 v[kUnroll];
+                                                              int32_t n_chunks, int32_t layer, KvGeom g,
+                                                              int32_t row16_log2, int32_t ppc_log2) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_seg = (int64_t(n_chunks) * g.Hkv * 2) << ppc_log2;
+  const int32_t seg16 = g.S << row16_log2;
+  const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
+  for (int64_t seg = int64_t(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5); seg < n_seg; seg += warps) {
+    int64_t s16, p16;
+    segment_addrs(seg, chunk0, layer, g, ppc_log2, row16_log2, slots, pages, s16, p16);
+    const uint4* src = pool + p16;
+    uint4* dst = store + s16;
+    for (int32_t base = lane; base < seg16; base += 32 * kUnroll) {
+      uint4 v[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t o = base + u * stride;
-      if (o < block16) {
-        const int64_t row = o >> row16_log2;
-        const int64_t col = o & (row16 - 1);
-        const int64_t hk = row >> C_log2;
-        const int64_t tt = (int64_t(c) << C_log2) + (row & (g.C - 1));
-        const int64_t page = pages[tt >> S_log2];
-        v[u] = src_layer[page * page16 + ((hk << S_log2) + (tt & (g.S - 1))) * row16 + col];
-      }
-    }
+      for (int u = 0; u < kUnroll; ++u)
+        if (base + 32 * u < seg16) v[u] = src[base + 32 * u];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t o = base + u * stride;
-      if (o < block16) dst[o] = v[u];
+      for (int u = 0; u < kUnroll; ++u)
+        if (base + 32 * u < seg16) dst[base + 32 * u] = v[u];
     }
   }
 }
@@ -198,11 +199,11 @@ cudaError_t launch_kv_gather(const void* store, void* pool, const int32_t* d_slo
                              int32_t n_matched, int32_t layer, const KvGeom& g, int32_t target_ctas,
                              cudaStream_t stream) {
   if (n_matched <= 0) return cudaSuccess;
-  const int per_chunk = (target_ctas + n_matched - 1) / n_matched;
-  dim3 grid(per_chunk, n_matched);
-  kv_gather_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint4*>(store), static_cast<uint4*>(pool),
-                                                  d_slots, d_pages, layer, g, ilog2(g.d / 8), ilog2(g.C),
-                                                  ilog2(g.S));
+  const int64_t n_seg = int64_t(n_matched) * g.Hkv * 2 * (g.C / g.S);
+  const int64_t ctas = std::min<int64_t>(target_ctas, (n_seg + kThreads / 32 - 1) / (kThreads / 32));
+  kv_gather_kernel<<<int(ctas), kThreads, 0, stream>>>(static_cast<const uint4*>(store), static_cast<uint4*>(pool),
+                                                       d_slots, d_pages, n_matched, layer, g, ilog2(g.d / 8),
+                                                       ilog2(g.C / g.S));
   return cudaGetLastError();
 }
 
@@ -219,11 +220,11 @@ cudaError_t launch_kv_scatter(const void* pool, void* store, const int32_t* d_sl
                               int32_t chunk0, int32_t n_chunks, int32_t layer, const KvGeom& g, int32_t target_ctas,
                               cudaStream_t stream) {
   if (n_chunks <= 0) return cudaSuccess;
-  const int per_chunk = (target_ctas + n_chunks - 1) / n_chunks;
-  dim3 grid(per_chunk, n_chunks);
-  kv_scatter_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint4*>(pool), static_cast<uint4*>(store),
-                                                   d_slots, d_pages, chunk0, layer, g, ilog2(g.d / 8), ilog2(g.C),
-                                                   ilog2(g.S));
+  const int64_t n_seg = int64_t(n_chunks) * g.Hkv * 2 * (g.C / g.S);
+  const int64_t ctas = std::min<int64_t>(target_ctas, (n_seg + kThreads / 32 - 1) / (kThreads / 32));
+  kv_scatter_kernel<<<int(ctas), kThreads, 0, stream>>>(static_cast<const uint4*>(pool), static_cast<uint4*>(store),
+                                                        d_slots, d_pages, chunk0, n_chunks, layer, g, ilog2(g.d / 8),
+                                                        ilog2(g.C / g.S));
   return cudaGetLastError();
 }
 

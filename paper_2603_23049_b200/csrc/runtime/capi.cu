@@ -117,7 +117,7 @@ pcr_status make_pool_tmap(pcr_ctx* c) {
   if (rows >= (int64_t(1) << 31)) return fail(c, PCR_E_INVAL, "pool too large for 32-bit TMA row coordinates");
   cuuint64_t dims[2] = {cuuint64_t(c->cfg.head_dim), cuuint64_t(rows)};
   cuuint64_t strides[1] = {cuuint64_t(c->cfg.head_dim) * 2};
-  cuuint32_t box[2] = {64, cuuint32_t(c->cfg.page_tokens)};
+  cuuint32_t box[2] = {64, cuuint32_t(pcr::attn_pool_box_rows(c->cfg.page_tokens))};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = reinterpret_cast<EncodeTiledFn>(fn)(
       &c->tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, c->cfg.pool, dims, strides, box, estr,

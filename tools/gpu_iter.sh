@@ -8,7 +8,7 @@ if [ $rc -ne 0 ]; then grep -E "Error|assert|FAILED" gpurun_out/gpu_tests.log | 
 OUT=gpurun_out/sweep.jsonl; : > $OUT
 timeout 200 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline >> $OUT 2>> gpurun_out/sweep.err
 timeout 200 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --mode sync >> $OUT 2>> gpurun_out/sweep.err
-for r in 0.0 0.5 1.0; do
+for r in 0.0 0.5 0.75 1.0; do
   timeout 300 python bench.py --workload M7 --ratio $r --steps 10 --warmup 2 --no-e2e --no-cpu-baseline >> $OUT 2>> gpurun_out/sweep.err
 done
 python - <<'PY'

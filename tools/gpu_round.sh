@@ -25,8 +25,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:kv_g
     python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --profile-steps 1 > /dev/null 2> gpurun_out/ncu_gather.err; echo "ncu gather rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:suffix_attn -s 40 -c 1 -o gpurun_out/prof_attn_M7 -f \
     python bench.py --workload M7 --ratio 0.5 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --profile-steps 1 > /dev/null 2> gpurun_out/ncu_attn.err; echo "ncu attn rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:suffix_attn -s 40 -c 1 -o gpurun_out/prof_attn_L8 -f \
-    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --profile-steps 1 > /dev/null 2> gpurun_out/ncu_attn_l8.err; echo "ncu attn L8 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:suffix_attn -s 6 -c 1 -o gpurun_out/prof_attn_micro -f \
+    python tools/attn_bench.py --iters 1 > /dev/null 2> gpurun_out/ncu_attn_micro.err; echo "ncu attn micro rc=$?"
 python - <<'PY'
 import json
 for l in open("gpurun_out/modes.jsonl"):
@@ -34,3 +34,4 @@ for l in open("gpurun_out/modes.jsonl"):
     print(j["config"]["workload"][:40], j["config"]["workload"][-30:], "ttft %.2f"%j["ttft_ms"], "load/layer %.1fus"%(j["gather_ms_per_layer"]*1e3), "attn/layer %.1fus %.0f TF/s (%.1f%%)"%(j["attn_ms_per_layer"]*1e3, j["roofline_attn"]["achieved"], 100*j["roofline_attn"]["frac"]))
 PY
 cat gpurun_out/bench_default.json
+timeout 300 python tools/attn_bench.py > gpurun_out/attn_micro.jsonl 2> gpurun_out/attn_micro.err; cat gpurun_out/attn_micro.jsonl
