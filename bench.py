@@ -472,13 +472,23 @@ def run_ours(args):
             dist.destroy_process_group()
         return
     dominant = "kv_gather" if N1 and (attn_ms != attn_ms or gather_ms >= attn_ms) else "suffix_attn"
+    # per-launch traffic of the dominant kernels from the committed ncu capture (profiles/)
+    try:
+        ncu_t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    except Exception:
+        ncu_t = {}
     rl_gather = {"bound": "host-link", "kernel": "kv_gather" if load_mode == 0 else f"copy engine ({args.load_mode})", "achieved": gather_gbs, "peak": peak_h2d,
-                 "unit": "GB/s", "frac": gather_gbs / peak_h2d, "traffic": None,
+                 "unit": "GB/s", "frac": gather_gbs / peak_h2d,
+                 "traffic": ncu_t.get("gather", {}).get("pcie_read_bytes") if args.workload == "L8" else None,
+                 "traffic_note": "PCIe read bytes per launch (ncu pcie__read_bytes x duration, L8 capture in "
+                                 "profiles/ncu_traffic.json); DRAM bytes per launch ~7.7 KB: pool writes stay in L2",
                  "peak_source": "live: cudaMemcpyAsync H2D from pinned host, 256 MiB, best of 5",
                  "algorithmic_bytes_per_launch": load_bytes, "avg_launch_ms": gather_ms}
     rl_attn = None if attn_tflops is None else {
         "bound": "tensor", "kernel": "kv_append+suffix_attn", "achieved": attn_tflops, "peak": bf16_peak,
-        "unit": "TFLOP/s", "frac": attn_tflops / bf16_peak, "traffic": None, "peak_source": bf16_src,
+        "unit": "TFLOP/s", "frac": attn_tflops / bf16_peak,
+        "traffic": ncu_t.get("attn_M7_r05", {}).get("dram_bytes") if (args.workload, args.ratio) == ("M7", 0.5) else None,
+        "peak_source": bf16_src,
         "algorithmic_flops_per_launch": attn_flops, "avg_launch_ms": attn_ms}
     line = {
         "metric": f"reuse-prefill tokens/s ({args.workload}: context tokens N1+N2 per second; TTFT in ttft_ms)",

@@ -9,23 +9,25 @@
 // B200 design (DESIGN.md §6 "suffix_attn"):
 //  * GQA packing: M rows are (token, head-in-group) pairs, r = t*G + gg, so one K/V tile read
 //    serves all G query heads of the group.  A CTA owns NQ = 2 Q tiles of 128 rows (256 rows)
-//    of one kv head and one range of 128-key tiles (split-KV when the grid is small).
-//  * warp 0: TMA producer — Q tiles once (3D tensor map over q [N2][Hq][d], box {64, G, 128/G},
-//    rows past N2 zero-filled), then K and V pages of every key tile (2D tensor map over the
-//    pool, one box {64 dims, S_pg rows} per page and 64-column half, SWIZZLE_128B), 2 stages.
-//  * warp 1: one thread issues tcgen05.mma (kind::f16, fp32 accumulate):
-//        S_t = Q_t K^T      (A, B from smem, K-major; D -> TMEM S_t, 128 columns)
-//        O_t += P_t V       (A = P_t from TMEM, B = V from smem MN-major; D -> TMEM O_t)
-//    ping-ponging the two Q tiles so the tensor pipe works on one tile while the other tile's
-//    softmax runs.  tcgen05 MMAs of one thread complete in issue order, so the commit that
-//    signals "S_t(j+1) ready" also certifies that O_t(j) += P_t(j) V(j) finished.
-//  * warp 2: tcgen05.alloc of all 512 TMEM columns: S_0, S_1 (128 each, P_t aliases S_t as
-//    packed bf16x2), O_0, O_1 (d each).
-//  * warps 4-7 / 8-11: softmax of Q tile 0 / 1, one thread per M row (= TMEM lane): tcgen05.ld
-//    of its S row, causal mask only on tiles crossing the diagonal, online softmax in the log2
-//    domain (one FFMA + ex2.approx per score) with lazy rescaling of O in TMEM (only when the
-//    running max grows by > 8, so P <= 256 in bf16), P -> TMEM with tcgen05.st, row sum of the
-//    same bf16-rounded weights (R18).  Epilogue: O / l -> bf16 (or fp32 partial + LSE per split).
+//    of one kv head and a range of 64-key tiles (split-KV when the grid is small); CTAs run
+//    heaviest causal M-blocks first.
+//  * warp 0 (converged, one elected lane issues): TMA producer — Q tiles once (3D tensor map
+//    over q [N2][Hq][d], box {64, G, 128/G}, rows past N2 zero-filled), then K and V of every
+//    key tile (2D tensor map over the pool, boxes {64 dims, min(S_pg, 64) rows}, SWIZZLE_128B)
+//    into a 4-stage ring.
+//  * warp 1 (converged, elected issue, precomputed descriptors): tcgen05.mma kind::f16 —
+//        S_t(j) = Q_t K(j)^T  (SS, K-major)        into TMEM S buffer (t, j&1) (64 columns)
+//        O_t   += P_t(j) V(j) (P from TMEM, V MN-major) into TMEM O_t (d columns)
+//    With 64-key tiles S is double-buffered per Q tile (4 x 64 + 2 x 128 = 512 columns), so
+//    S_t(j+1) is computed while the softmax works on S_t(j); S_t(j+2) reuses buffer j&1 and is
+//    issued after O_t += P_t(j) V(j) (tcgen05 MMAs of one thread execute in issue order).
+//  * warp 2: tcgen05.alloc of all 512 TMEM columns.
+//  * warps 4-7 / 8-11: softmax of Q tile 0 / 1, one thread per M row (= TMEM lane): row max
+//    with FMNMX3, x = s*scale - m with FFMA2, 2^x by MUFU.EX2 or (kPolyPairs of every 16 pairs) a
+//    polynomial on the FMA pipe, P -> TMEM over the S columns (tcgen05.st), row sum of the same
+//    bf16-rounded weights with FADD2 (R18); causal mask only on tiles crossing the diagonal;
+//    lazy rescaling of O (only when the running max grows by > 8, log2 units), after waiting for
+//    the previous PV.  Epilogue: O / l -> bf16, or fp32 partial + log2-LSE per KV split.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -40,10 +42,10 @@ namespace {
 using namespace ptx;
 
 constexpr int kBlockM = 128;   // rows per Q tile (= TMEM lanes)
-constexpr int kBlockN = 128;   // keys per tile
+constexpr int kBlockN = 64;    // keys per tile (64: S fits double-buffered per Q tile in TMEM)
 constexpr int kNQ = 2;         // Q tiles per CTA
+constexpr int kStages = 4;     // K/V smem ring depth
 constexpr int kThreads = 128 + kNQ * 128;
-constexpr int kHalfBytes = 128 * 128;  // 128 rows x 128 bytes (64 bf16) per swizzle column block
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 // Pairs (of 16 per 32-column chunk) whose exp2 runs as a polynomial on the FMA pipe instead of
@@ -57,19 +59,23 @@ constexpr int kPolyPairs = PCR_POLY_PAIRS;
 template <int D>
 struct Layout {
   static constexpr int kHalves = D / 64;
-  static constexpr int kTileBytes = kHalves * kHalfBytes;  // one Q tile, or one K or V tile
+  static constexpr int kQHalf = kBlockM * 128;                 // 128 rows x 128 B
+  static constexpr int kQTile = kHalves * kQHalf;
+  static constexpr int kKVHalf = kBlockN * 128;                // 64 keys x 128 B
+  static constexpr int kKVTile = kHalves * kKVHalf;
   static constexpr int kQ0 = 0;
-  static constexpr int kK0 = kQ0 + kNQ * kTileBytes;
-  static constexpr int kV0 = kK0 + 2 * kTileBytes;
-  static constexpr int kBar = kV0 + 2 * kTileBytes;
-  static constexpr int kBytes = kBar + 256;
+  static constexpr int kK0 = kQ0 + kNQ * kQTile;
+  static constexpr int kV0 = kK0 + kStages * kKVTile;
+  static constexpr int kBar = kV0 + kStages * kKVTile;
+  static constexpr int kBytes = kBar + 512;
   static constexpr int kAlloc = kBytes + 1024;  // slack for 1024-byte alignment
-  static constexpr uint32_t kColS = 0;          // S_t at t*128
-  static constexpr uint32_t kColO = kNQ * kBlockN;  // O_t at kColO + t*D
+  // TMEM columns: S_{t,b} (Q tile t, buffer b) at (2t+b)*64; O_t at 256 + t*D.
+  static constexpr uint32_t kColO = 2 * kNQ * kBlockN;
 };
 
 struct Bars {
-  uint64_t q_full, k_full[2], v_full[2], kv_empty[2], s_full[kNQ], p_full[kNQ], o_full;
+  uint64_t q_full, k_full[kStages], v_full[kStages], kv_empty[kStages];
+  uint64_t s_full[kNQ][2], p_full[kNQ][2], o_done[kNQ], o_full;
   uint32_t tmem_base;
 };
 
@@ -93,9 +99,6 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       : "memory");
 }
 
-
-// 136 registers x 384 threads = 52K of the SM's 64K: a 256-thread gather CTA (10K) still fits
-// beside an attention CTA, so layer l+1's host->HBM load never waits for attention SMs.
 // 2^x for a pair of x <= 0 on the FMA pipe (FA4-style MUFU offload): x = n + f with
 // n = round(x), f in [-1/2, 1/2]; 2^f by a degree-3 minimax polynomial (max relative error
 // 7.5e-5, far below the 2^-9 bf16 rounding P gets next); 2^n added to the exponent bits.
@@ -118,6 +121,8 @@ __device__ __forceinline__ void exp2_poly2(uint64_t x2, float& y0, float& y1) {
   y1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
 }
 
+// 136 registers x 384 threads = 52K of the SM's 64K: a 256-thread gather CTA (10K) still fits
+// beside an attention CTA, so layer l+1's host->HBM load never waits for attention SMs.
 template <int D>
 __global__ void __maxnreg__(136)
     suffix_attn_kernel(const __grid_constant__ CUtensorMap tmap_pool, const __grid_constant__ CUtensorMap tmap_q,
@@ -129,8 +134,7 @@ __global__ void __maxnreg__(136)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  // Longest-processing-time-first order: with causal masking the last M-blocks see the most
-  // keys, so CTA c runs M-block (n_mblocks - 1 - c / hkv) of kv head c % hkv (heads interleaved).
+  // Longest-processing-time-first order (causal: the last M-blocks see the most keys)
   const int G = p.hq / p.hkv;
   const int tok_per_tile = kBlockM / G;
   const int n_mblocks = (p.n2 + kNQ * tok_per_tile - 1) / (kNQ * tok_per_tile);
@@ -143,18 +147,20 @@ __global__ void __maxnreg__(136)
   const int j_begin = blockIdx.z * per_split;
   const int j_end = min(j_begin + per_split, n_tiles_all);
   const int n_iter = max(0, j_end - j_begin);
-  const int pages_per_tile = kBlockN / p.S;
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->q_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&bars->k_full[s], 1);
       mbar_init(&bars->v_full[s], 1);
       mbar_init(&bars->kv_empty[s], 1);
     }
     for (int t = 0; t < kNQ; ++t) {
-      mbar_init(&bars->s_full[t], 1);
-      mbar_init(&bars->p_full[t], 128);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&bars->s_full[t][b], 1);
+        mbar_init(&bars->p_full[t][b], 128);
+      }
+      mbar_init(&bars->o_done[t], 1);
     }
     mbar_init(&bars->o_full, 1);
     fence_mbar_init();
@@ -169,107 +175,90 @@ __global__ void __maxnreg__(136)
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
-    // Converged warp; one elected lane issues the copies of each stage.
-    if (n_iter > 0) {
-      if (elect_one()) {
-        mbar_arrive_expect_tx(&bars->q_full, kNQ * Lay::kTileBytes);
-        for (int t = 0; t < kNQ; ++t)
-          for (int hf = 0; hf < Lay::kHalves; ++hf)
-            tma_load_3d(smem + Lay::kQ0 + t * Lay::kTileBytes + hf * kHalfBytes, &tmap_q, hf * 64, g * G,
-                        i0 + t * tok_per_tile, &bars->q_full);
-      }
-      __syncwarp();
+    if (n_iter > 0 && elect_one()) {
+      mbar_arrive_expect_tx(&bars->q_full, kNQ * Lay::kQTile);
+      for (int t = 0; t < kNQ; ++t)
+        for (int hf = 0; hf < Lay::kHalves; ++hf)
+          tma_load_3d(smem + Lay::kQ0 + t * Lay::kQTile + hf * Lay::kQHalf, &tmap_q, hf * 64, g * G,
+                      i0 + t * tok_per_tile, &bars->q_full);
       const int64_t layer_rows = p.n_pool_pages * p.hkv * 2 * p.S;
+      const int box = min(p.S, kBlockN);  // rows per TMA box (the pool tensor map's box height)
       for (int it = 0; it < n_iter; ++it) {
-        const int j = j_begin + it;
-        const int st = it & 1;
-        if (it >= 2) mbar_wait(&bars->kv_empty[st], ((it >> 1) - 1) & 1);
-        // page rows of this tile, one per lane (pages_per_tile <= 8)
-        const int pidx = min(j * pages_per_tile + lane, p.n_req_pages - 1);  // clamp: finite, masked
-        const int64_t my_row = int64_t(p.layer) * layer_rows + ((int64_t(p.pages[pidx]) * p.hkv + g) * 2) * p.S;
-        int32_t rows[8];
+        const int st = it % kStages;
+        if (it >= kStages) mbar_wait(&bars->kv_empty[st], ((it / kStages) - 1) & 1);
+        uint8_t* ks = smem + Lay::kK0 + st * Lay::kKVTile;
+        uint8_t* vs = smem + Lay::kV0 + st * Lay::kKVTile;
+        mbar_arrive_expect_tx(&bars->k_full[st], Lay::kKVTile);
+        mbar_arrive_expect_tx(&bars->v_full[st], Lay::kKVTile);
+        for (int b0 = 0; b0 < kBlockN; b0 += box) {
+          const int key = (j_begin + it) * kBlockN + b0;
+          const bool in_req = key / p.S < p.n_req_pages;
+          const int pidx = in_req ? key / p.S : p.n_req_pages - 1;  // clamp: finite, masked
+          const int row_in_page = in_req ? key % p.S : 0;
+          const int64_t page = p.pages[pidx];
+          const int64_t row_k = int64_t(p.layer) * layer_rows + ((page * p.hkv + g) * 2 + 0) * p.S + row_in_page;
 #pragma unroll
-        for (int pp = 0; pp < 8; ++pp) rows[pp] = int32_t(__shfl_sync(0xffffffffu, my_row, pp));
-        if (elect_one()) {
-          uint8_t* ks = smem + Lay::kK0 + st * Lay::kTileBytes;
-          uint8_t* vs = smem + Lay::kV0 + st * Lay::kTileBytes;
-          mbar_arrive_expect_tx(&bars->k_full[st], Lay::kTileBytes);
-          mbar_arrive_expect_tx(&bars->v_full[st], Lay::kTileBytes);
+          for (int hf = 0; hf < Lay::kHalves; ++hf)
+            tma_load_2d(ks + hf * Lay::kKVHalf + b0 * 128, &tmap_pool, hf * 64, int32_t(row_k), &bars->k_full[st]);
 #pragma unroll
-          for (int pp = 0; pp < 8; ++pp) {
-            if (pp < pages_per_tile) {
-              const int32_t row_k = rows[pp];
-#pragma unroll
-              for (int hf = 0; hf < Lay::kHalves; ++hf)
-                tma_load_2d(ks + hf * kHalfBytes + pp * p.S * 128, &tmap_pool, hf * 64, row_k, &bars->k_full[st]);
-#pragma unroll
-              for (int hf = 0; hf < Lay::kHalves; ++hf)
-                tma_load_2d(vs + hf * kHalfBytes + pp * p.S * 128, &tmap_pool, hf * 64, row_k + p.S,
-                            &bars->v_full[st]);
-            }
-          }
+          for (int hf = 0; hf < Lay::kHalves; ++hf)
+            tma_load_2d(vs + hf * Lay::kKVHalf + b0 * 128, &tmap_pool, hf * 64, int32_t(row_k + p.S),
+                        &bars->v_full[st]);
         }
-        __syncwarp();
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    // The whole warp runs the loop (converged); one elected lane issues each MMA group.
+    // Converged warp; one elected lane issues each MMA group; descriptor bases precomputed.
     if (n_iter > 0) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(kBlockM, kBlockN, 0, 0);
       constexpr uint32_t idesc_o = idesc_bf16_f32(kBlockM, D, 0, 1);
       mbar_wait(&bars->q_full, 0);
-      // Descriptor bases computed once; a K step only adds (byte offset >> 4) to the start
-      // address field (addresses < 256 KB, so the 14-bit field never carries).
-      // (selected with ternaries, not indexed arrays, so they stay in registers)
       const uint64_t q_desc0 = smem_desc_sw128(smem_u32(smem + Lay::kQ0), 16, 1024);
-      const uint64_t q_desc1 = q_desc0 + (Lay::kTileBytes >> 4);
       const uint64_t k_desc0 = smem_desc_sw128(smem_u32(smem + Lay::kK0), 16, 1024);
-      const uint64_t k_desc1 = k_desc0 + (Lay::kTileBytes >> 4);
-      const uint64_t v_desc0 = smem_desc_sw128(smem_u32(smem + Lay::kV0), kHalfBytes, 1024);
-      const uint64_t v_desc1 = v_desc0 + (Lay::kTileBytes >> 4);
-      static_assert(kNQ == 2, "descriptor selection assumes two Q tiles");
+      const uint64_t v_desc0 = smem_desc_sw128(smem_u32(smem + Lay::kV0), Lay::kKVHalf, 1024);
       auto issue_s = [&](int t, int it) {
-        const uint64_t qd = t ? q_desc1 : q_desc0, kd = (it & 1) ? k_desc1 : k_desc0;
+        const uint64_t qd = q_desc0 + uint64_t(t * Lay::kQTile >> 4);
+        const uint64_t kd = k_desc0 + uint64_t((it % kStages) * Lay::kKVTile >> 4);
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint64_t off = ((kk >> 2) * kHalfBytes + (kk & 3) * 32) >> 4;
-            mma_bf16_ss(tmem + Lay::kColS + t * kBlockN, qd + off, kd + off, idesc_s, kk > 0);
-          }
-          mma_commit(&bars->s_full[t]);
+          for (int kk = 0; kk < D / 16; ++kk)
+            mma_bf16_ss(tmem + (2 * t + (it & 1)) * kBlockN, qd + (((kk >> 2) * Lay::kQHalf + (kk & 3) * 32) >> 4),
+                        kd + (((kk >> 2) * Lay::kKVHalf + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
+          mma_commit(&bars->s_full[t][it & 1]);
         }
         __syncwarp();
       };
       auto issue_pv = [&](int t, int it) {
-        const uint64_t vd = (it & 1) ? v_desc1 : v_desc0;
+        const uint64_t vd = v_desc0 + uint64_t((it % kStages) * Lay::kKVTile >> 4);
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < kBlockN / 16; ++kk)
-            mma_bf16_ts(tmem + Lay::kColO + t * D, tmem + Lay::kColS + t * kBlockN + kk * 8, vd + (kk * 2048 >> 4),
+            mma_bf16_ts(tmem + Lay::kColO + t * D, tmem + (2 * t + (it & 1)) * kBlockN + kk * 8, vd + (kk * 2048 >> 4),
                         idesc_o, (it > 0 || kk > 0));
-          if (t == kNQ - 1) mma_commit(&bars->kv_empty[it & 1]);
+          mma_commit(&bars->o_done[t]);
+          if (t == kNQ - 1) mma_commit(&bars->kv_empty[it % kStages]);
         }
         __syncwarp();
       };
-      mbar_wait(&bars->k_full[0], 0);
-      tc_fence_after();
-      for (int t = 0; t < kNQ; ++t) issue_s(t, 0);
+      for (int it = 0; it < min(2, n_iter); ++it) {
+        mbar_wait(&bars->k_full[it], 0);
+        tc_fence_after();
+        for (int t = 0; t < kNQ; ++t) issue_s(t, it);
+      }
       for (int it = 0; it < n_iter; ++it) {
-        const int st = it & 1;
-        const bool more = it + 1 < n_iter;
-        mbar_wait(&bars->v_full[st], (it >> 1) & 1);
+        const int st = it % kStages;
+        mbar_wait(&bars->v_full[st], (it / kStages) & 1);
         for (int t = 0; t < kNQ; ++t) {
-          mbar_wait(&bars->p_full[t], it & 1);
+          mbar_wait(&bars->p_full[t][it & 1], (it >> 1) & 1);
           tc_fence_after();
           issue_pv(t, it);
-          if (more) {
-            if (t == 0) {  // K(j+1) is only needed here, after PV_0(j) has been queued
-              mbar_wait(&bars->k_full[st ^ 1], ((it + 1) >> 1) & 1);
-              tc_fence_after();
-            }
-            issue_s(t, it + 1);
-          }
+        }
+        if (it + 2 < n_iter) {  // S(it+2) reuses buffer it&1: issued after PV(it) read P(it) from it
+          const int st2 = (it + 2) % kStages;
+          mbar_wait(&bars->k_full[st2], ((it + 2) / kStages) & 1);
+          tc_fence_after();
+          for (int t = 0; t < kNQ; ++t) issue_s(t, it + 2);
         }
       }
       if (elect_one()) mma_commit(&bars->o_full);
@@ -282,54 +271,52 @@ __global__ void __maxnreg__(136)
     const int i = i0 + t * tok_per_tile + r / G; // suffix token of this row
     const int qh = g * G + (r % G);              // local query head
     const uint32_t lane_base = tmem + (uint32_t((warp & 3) * 32) << 16);
-    const uint32_t s_col = lane_base + Lay::kColS + t * kBlockN;
     const uint32_t o_col = lane_base + Lay::kColO + t * D;
     const int limit = p.n1 + i;  // last visible key of this row
     const int tile_first_key_limit = p.n1 + i0 + t * tok_per_tile;
-    // Two passes over S in TMEM, 32 columns at a time (TMEM reads are cheap; this keeps the
-    // softmax at <= 136 registers so a gather CTA can co-reside): (1) row max with the 3-input
-    // FMNMX3; (2) P = bf16(2^(s*scale - m)) via FFMA2 + ex2, written over the S columns it came
-    // from (P chunk c -> columns [16c, 16c+16), all already read), row sum via FADD2.
+    // Per tile of 64 keys: (1) row max of S (two 32-column TMEM loads, four FMNMX3 chains);
+    // (2) P = bf16(2^(s*scale - m)) via FFMA2 + ex2 (MUFU, or a polynomial on the FMA pipe for
+    // kPolyPairs of every 16 pairs), written over the S columns it came from, and the row sum
+    // of the same bf16-rounded weights via FADD2 (R18).
     float m_raw = -INFINITY, l = 0.f;
     const uint64_t scale2 = f2_pack(p.scale_log2, p.scale_log2);
     for (int it = 0; it < n_iter; ++it) {
       const int key0 = (j_begin + it) * kBlockN;
       const bool diag = key0 + kBlockN - 1 > tile_first_key_limit;  // tile crosses this Q tile's diagonal
-      mbar_wait(&bars->s_full[t], it & 1);
+      const uint32_t s_col = lane_base + (2 * t + (it & 1)) * kBlockN;
+      mbar_wait(&bars->s_full[t][it & 1], (it >> 1) & 1);
       tc_fence_after();
-      // TMEM loads are software-pipelined: chunk c+1 is in flight while chunk c is processed.
       float va[32], vb[32];
-      // four independent max chains (a single FMNMX3 chain would be 64 dependent ops per tile)
-      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-      auto max_chunk = [&](float* v, int c) {
-        if (diag) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = (key0 + c * 32 + e <= limit) ? v[e] : -INFINITY;
-        }
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) mx4[(e >> 1) & 3] = fmax3(mx4[(e >> 1) & 3], v[e], v[e + 1]);
-      };
       tmem_ld32(s_col, va);
-      tmem_ld_wait();
       tmem_ld32(s_col + 32, vb);
-      max_chunk(va, 0);
       tmem_ld_wait();
-      tmem_ld32(s_col + 64, va);
-      max_chunk(vb, 1);
-      tmem_ld_wait();
-      tmem_ld32(s_col + 96, vb);
-      max_chunk(va, 2);
-      tmem_ld_wait();
-      max_chunk(vb, 3);
+      if (diag) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          va[e] = (key0 + e <= limit) ? va[e] : -INFINITY;
+          vb[e] = (key0 + 32 + e <= limit) ? vb[e] : -INFINITY;
+        }
+      }
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int e = 0; e < 32; e += 4) {
+        mx4[(e >> 2) & 1] = fmax3(mx4[(e >> 2) & 1], va[e], va[e + 1]);
+        mx4[((e >> 2) & 1) + 2] = fmax3(mx4[((e >> 2) & 1) + 2], va[e + 2], va[e + 3]);
+        mx4[(e >> 2) & 1] = fmax3(mx4[(e >> 2) & 1], vb[e], vb[e + 1]);
+        mx4[((e >> 2) & 1) + 2] = fmax3(mx4[((e >> 2) & 1) + 2], vb[e + 2], vb[e + 3]);
+      }
       const float rowmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
       const float m_new = fmaxf(m_raw, rowmax);
       const bool rescale = (m_new - m_raw) * p.scale_log2 > kRescaleThreshold;
       const float m_use = rescale ? m_new : m_raw;
-      const float neg_m = -m_use * p.scale_log2;
+      // a split-KV range can lie wholly past a row's causal limit: nothing visible yet
+      const float neg_m = m_use == -INFINITY ? 0.f : -m_use * p.scale_log2;
       const uint64_t negm2 = f2_pack(neg_m, neg_m);
       const float alpha = ex2(fmaf(m_raw, p.scale_log2, neg_m));
-      // O_t(j-1) is complete here (in-order MMA completion, see header): rescale if needed.
       if (it > 0 && __any_sync(0xffffffffu, rescale)) {
+        // O_t must hold PV_t(it-1) before it is rescaled
+        mbar_wait(&bars->o_done[t], (it - 1) & 1);
+        tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
           float o[32];
@@ -342,10 +329,6 @@ __global__ void __maxnreg__(136)
       }
       uint64_t sum4[4] = {0, 0, 0, 0};  // four independent FADD2 chains
       auto exp_chunk = [&](float* v, int c) {
-        if (diag) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = (key0 + c * 32 + e <= limit) ? v[e] : -INFINITY;
-        }
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
@@ -362,29 +345,19 @@ __global__ void __maxnreg__(136)
           __nv_bfloat162 b = __floats2bfloat162_rn(y0, y1);
           const uint32_t w = *reinterpret_cast<uint32_t*>(&b);
           pk[e / 2] = w;
-          // row sum of the same bf16-rounded weights (R18), two lanes per FADD2
-          sum4[(e >> 1) & 3] = fadd2(sum4[(e >> 1) & 3], f2_pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u)));
+          sum4[(e >> 1) & 3] =
+              fadd2(sum4[(e >> 1) & 3], f2_pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u)));
         }
         tmem_st16(s_col + c * 16, pk);   // P chunk c -> columns [16c, 16c+16): already read
       };
-      tmem_ld32(s_col, va);
-      tmem_ld_wait();
-      tmem_ld32(s_col + 32, vb);
       exp_chunk(va, 0);
-      tmem_ld_wait();
-      tmem_ld32(s_col + 64, va);
       exp_chunk(vb, 1);
-      tmem_ld_wait();
-      tmem_ld32(s_col + 96, vb);
-      exp_chunk(va, 2);
-      tmem_ld_wait();
-      exp_chunk(vb, 3);
       float s0, s1;
       f2_unpack(fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3])), s0, s1);
       l = l * alpha + (s0 + s1);
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&bars->p_full[t]);
+      mbar_arrive(&bars->p_full[t][it & 1]);
       m_raw = m_use;
     }
     // ---------------------------------------------------------------- epilogue
@@ -394,7 +367,7 @@ __global__ void __maxnreg__(136)
       mbar_wait(&bars->o_full, 0);
       tc_fence_after();
     }
-    const float inv_l = n_iter > 0 ? 1.f / l : 0.f;
+    const float inv_l = (n_iter > 0 && l > 0.f) ? 1.f / l : 0.f;
     if (p.n_splits == 1) {
       uint4* dst = reinterpret_cast<uint4*>(p.out + row_id * D);
 #pragma unroll
@@ -436,7 +409,7 @@ __global__ void __maxnreg__(136)
       }
       if (row_ok)
         p.ws_lse[int64_t(blockIdx.z) * rows_total + row_id] =
-            n_iter > 0 ? m_raw * p.scale_log2 + __log2f(l) : -INFINITY;
+            (n_iter > 0 && l > 0.f) ? m_raw * p.scale_log2 + __log2f(l) : -INFINITY;
     }
     tc_fence_before();
   }
@@ -524,8 +497,8 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
   const int max_tiles = (p.n1 + p.n2 + kBlockN - 1) / kBlockN;
   int splits = 1;
   if (p.ws_o && ctas < 148) {
-    splits = (148 + ctas - 1) / ctas;
-    splits = std::min(splits, std::max(1, max_tiles / 2));
+    splits = std::max(1, 148 / ctas);
+    splits = std::min(splits, std::max(1, max_tiles / 4));
     const int64_t per_split_bytes = int64_t(p.n2) * p.hq * (D + 1) * 4;
     splits = int(std::min<int64_t>(splits, std::max<int64_t>(1, p.ws_bytes / per_split_bytes)));
   }
@@ -548,7 +521,7 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
 
 }  // namespace
 
-int32_t attn_pool_box_rows(int32_t S) { return S; }
+int32_t attn_pool_box_rows(int32_t S) { return std::min(S, kBlockN); }
 
 cudaError_t launch_suffix_attn(const CUtensorMap* tmap_pool, const AttnParams& p, int32_t d, cudaStream_t stream,
                                int* launches) {

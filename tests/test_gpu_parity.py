@@ -291,3 +291,16 @@ def test_offload_third_stream_commits_real_kv():
             assert np.array_equal(got, recs[c]), (i, c)
             rig.store[plan["slots"][c]] = got          # mirror for expected_context of later hits
         rig.ctx.release(i, True)
+
+
+@pytest.mark.parametrize("n1,n2", [(0, 200), (0, 333), (64, 300), (256, 520), (512, 200), (1024, 77), (128, 1)])
+def test_split_kv_edge_sweep(n1, n2):
+    """Small grids take the split-KV path; a split can hold only keys past some rows' causal
+    limit (those rows see nothing in it).  Outputs must stay finite and within tolerance."""
+    L, Hq, Hkv, d, C, S = 1, 32, 8, 128, 64, 16
+    rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, n1, n2, seed=n1 * 7 + n2)
+    from oracle.attention import bf16_bits_to_f64
+    assert np.isfinite(bf16_bits_to_f64(out)).all()
+    kc, vc = rig.expected_context(plan, k[:, n1:], v[:, n1:], 0)
+    r, m = check_attention(out[0], q[0], kc, vc, n1, blocked=True)
+    assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (r, m)
