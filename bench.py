@@ -75,19 +75,36 @@ def geometry(name):
 
 # ------------------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region: NVML
+    (nvidia-ml-py) polled every 10 ms from a thread, so even a sub-second timed region gets tens
+    of samples; `nvidia-smi -lms 100` as the fallback."""
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4))
 
-    def __init__(self, index):
-        self.index = index
-        self.proc = None
-        self.lines = []
+    def __init__(self, index, pci_bus_id=None):
+        self.index, self.pci = index, pci_bus_id
+        self.proc = self.nvml = None
+        self.lines, self.samples = [], []
+        self.stop_ev = threading.Event()
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+            import pynvml
+            pynvml.nvmlInit()
+            h = (pynvml.nvmlDeviceGetHandleByPciBusId(self.pci) if self.pci
+                 else pynvml.nvmlDeviceGetHandleByIndex(self.index))
+            self.nvml, self.h = pynvml, h
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index),
+                                          "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                                          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                                          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
@@ -95,11 +112,34 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        nv = self.nvml
+        while not self.stop_ev.is_set():
+            try:
+                mhz = float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+                self.samples.append((mhz, rs, time.perf_counter()))
+            except Exception:
+                pass
+            self.stop_ev.wait(0.01)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def begin(self):
+        self.t_begin = time.perf_counter()
+
     def stop(self):
+        if self.nvml:
+            self.stop_ev.set()
+            self.t.join(timeout=2)
+            t0 = getattr(self, "t_begin", 0.0)
+            inside = [(m, rs) for m, rs, ts in self.samples if ts >= t0]   # timed region only
+            sm = [m for m, _ in inside]
+            reasons = sorted({n for _, rs in inside for n, bit in self.REASONS if rs & bit})
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                    "samples": len(sm), "source": "nvml, 10 ms poll"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -108,7 +148,6 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
@@ -118,11 +157,19 @@ class ClockSampler:
                 mx = float(f[1])
             except ValueError:
                 continue
-            for n, v in zip(names, f[3:7]):
+            for (n, _), v in zip(self.REASONS, f[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi -lms 100"}
+
+
+def pci_bus_id(torch, dev):
+    try:
+        pr = torch.cuda.get_device_properties(dev)
+        return f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+    except Exception:
+        return None
 
 
 # ------------------------------------------------------------------------------ oracle leg
@@ -198,7 +245,7 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------ our arm
-def h2d_peak_gbs(torch, nbytes=256 << 20, reps=5):
+def h2d_peak_gbs(torch, nbytes=256 << 20, reps=10):
     """Measured host->HBM copy-engine peak from pinned memory (the host-link roofline)."""
     h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
     h.fill_(1)
@@ -362,16 +409,18 @@ def run_ours(args):
         ctx.release(rid, False)
         return t
 
+    peak_h2d_before = h2d_peak_gbs(torch)
     for _ in range(args.warmup):
         step(q_d, k_d, v_d, out_d)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local, pci_bus_id(torch, local))
     clocks.start()
     launches0 = ctx.kernel_launches
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    clocks.begin()
     ev0.record(cs)
     ls.wait_event(ev0)
     step_ms, load_ms = [], []
@@ -447,7 +496,8 @@ def run_ours(args):
 
     load_bytes = 2 * N1 * hkv * d * 2               # algorithmic bytes per gather launch (one layer)
     attn_flops = 4 * hq * d * (N2 * N1 + N2 * (N2 + 1) // 2)
-    peak_h2d = h2d_peak_gbs(torch)
+    peak_h2d_after = h2d_peak_gbs(torch)
+    peak_h2d = max(peak_h2d_before, peak_h2d_after)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -482,7 +532,9 @@ def run_ours(args):
                  "traffic": ncu_t.get("gather", {}).get("pcie_read_bytes") if args.workload == "L8" else None,
                  "traffic_note": "PCIe read bytes per launch (ncu pcie__read_bytes x duration, L8 capture in "
                                  "profiles/ncu_traffic.json); DRAM bytes per launch ~7.7 KB: pool writes stay in L2",
-                 "peak_source": "live: cudaMemcpyAsync H2D from pinned host, 256 MiB, best of 5",
+                 "peak_source": f"live: cudaMemcpyAsync H2D from pinned host, 256 MiB, best of 10, max of a "
+                                f"measurement before the warm-up ({peak_h2d_before:.1f}) and after the timed region "
+                                f"({peak_h2d_after:.1f})",
                  "algorithmic_bytes_per_launch": load_bytes, "avg_launch_ms": gather_ms}
     rl_attn = None if attn_tflops is None else {
         "bound": "tensor", "kernel": "kv_append+suffix_attn", "achieved": attn_tflops, "peak": bf16_peak,
@@ -556,10 +608,11 @@ def run_trace_z(args):
         ctx.submit(i, t, n)
     ttft, wall, hits, chunks, toks, n1s, plan_us = [], [], 0, 0, 0, [], []
     launches0 = ctx.kernel_launches
-    clocks = ClockSampler(0)
+    clocks = ClockSampler(0, pci_bus_id(torch, 0))
     clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    clocks.begin()
     ev0.record(cs)
     for i in range(len(reqs)):
         pend = list(range(i + 1, min(len(reqs), i + 1 + args.window)))

@@ -44,7 +44,10 @@ using namespace ptx;
 constexpr int kBlockM = 128;   // rows per Q tile (= TMEM lanes)
 constexpr int kBlockN = 64;    // keys per tile (64: S fits double-buffered per Q tile in TMEM)
 constexpr int kNQ = 2;         // Q tiles per CTA
-constexpr int kStages = 4;     // K/V smem ring depth
+#ifndef PCR_KV_STAGES
+#define PCR_KV_STAGES 4
+#endif
+constexpr int kStages = PCR_KV_STAGES;  // K/V smem ring depth
 constexpr int kThreads = 128 + kNQ * 128;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
@@ -55,6 +58,20 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define PCR_POLY_PAIRS 4
 #endif
 constexpr int kPolyPairs = PCR_POLY_PAIRS;
+// Experiment knob (never set by the default build), a bit mask: 1 = skip the softmax arithmetic
+// (the warpgroups only hand the S buffers back), 2 = skip the MMAs (only commits), 4 = skip the
+// K/V TMA loads (the producer only arrives), 8 = the MMA warp does not wait for P: which side
+// bounds the pipeline.
+#ifndef PCR_ATTN_TIMING
+#define PCR_ATTN_TIMING 0
+#endif
+#ifndef PCR_ATTN_PROFILE
+#define PCR_ATTN_PROFILE 0
+#endif
+// the two softmax warpgroups alternate their exponential phases (off in the skip-softmax profile)
+#ifndef PCR_EXP_PINGPONG
+#define PCR_EXP_PINGPONG ((PCR_ATTN_PROFILE & 1) == 0)
+#endif
 
 template <int D>
 struct Layout {
@@ -74,7 +91,7 @@ struct Layout {
 };
 
 struct Bars {
-  uint64_t q_full, k_full[kStages], v_full[kStages], kv_empty[kStages];
+  uint64_t q_full, k_full[kStages], v_full[kStages], k_empty[kStages], v_empty[kStages];
   uint64_t s_full[kNQ][2], p_full[kNQ][2], o_done[kNQ], o_full;
   uint32_t tmem_base;
 };
@@ -97,6 +114,13 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 // 2^x for a pair of x <= 0 on the FMA pipe (FA4-style MUFU offload): x = n + f with
@@ -132,8 +156,9 @@ __global__ void __maxnreg__(136)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Bars* bars = reinterpret_cast<Bars*>(smem + Lay::kBar);
 
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so role branches are uniform and the MMA
+  // and TMA loops keep counters and descriptors in uniform registers (no R2UR per instruction)
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
   // Longest-processing-time-first order (causal: the last M-blocks see the most keys)
   const int G = p.hq / p.hkv;
   const int tok_per_tile = kBlockM / G;
@@ -153,7 +178,8 @@ __global__ void __maxnreg__(136)
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&bars->k_full[s], 1);
       mbar_init(&bars->v_full[s], 1);
-      mbar_init(&bars->kv_empty[s], 1);
+      mbar_init(&bars->k_empty[s], 1);
+      mbar_init(&bars->v_empty[s], 1);
     }
     for (int t = 0; t < kNQ; ++t) {
       for (int b = 0; b < 2; ++b) {
@@ -175,36 +201,76 @@ __global__ void __maxnreg__(136)
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
-    if (n_iter > 0 && elect_one()) {
-      mbar_arrive_expect_tx(&bars->q_full, kNQ * Lay::kQTile);
-      for (int t = 0; t < kNQ; ++t)
-        for (int hf = 0; hf < Lay::kHalves; ++hf)
-          tma_load_3d(smem + Lay::kQ0 + t * Lay::kQTile + hf * Lay::kQHalf, &tmap_q, hf * 64, g * G,
-                      i0 + t * tok_per_tile, &bars->q_full);
+    // Converged warp: the lanes hold the page ids of 32 consecutive pages (one coalesced load per
+    // 32 pages, read by shuffles), one elected lane issues the TMA copies.
+    if (n_iter > 0) {
+      const int lane = threadIdx.x & 31;
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&bars->q_full, kNQ * Lay::kQTile);
+        for (int t = 0; t < kNQ; ++t)
+          for (int hf = 0; hf < Lay::kHalves; ++hf)
+            tma_load_3d(smem + Lay::kQ0 + t * Lay::kQTile + hf * Lay::kQHalf, &tmap_q, hf * 64, g * G,
+                        i0 + t * tok_per_tile, &bars->q_full);
+      }
+      __syncwarp();
       const int64_t layer_rows = p.n_pool_pages * p.hkv * 2 * p.S;
       const int box = min(p.S, kBlockN);  // rows per TMA box (the pool tensor map's box height)
+      const int n_box = kBlockN / box;    // 1, 2 or 4 (S_pg >= 16)
+      int pg_base = -64, pg_val = 0;
+      // K(j) and V(j) go into stage j % kStages once their previous occupants are consumed: K after
+      // the last QK^T that read it (k_empty), V after the last PV (v_empty).
       for (int it = 0; it < n_iter; ++it) {
         const int st = it % kStages;
-        if (it >= kStages) mbar_wait(&bars->kv_empty[st], ((it / kStages) - 1) & 1);
+        const uint32_t ph = ((it / kStages) - 1) & 1;
+        int64_t row_k[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (b < n_box) {
+            const int key = (j_begin + it) * kBlockN + b * box;
+            const bool in_req = key / p.S < p.n_req_pages;
+            const int pidx = in_req ? key / p.S : p.n_req_pages - 1;  // clamp: finite, masked
+            if (pidx < pg_base || pidx >= pg_base + 32) {
+              pg_base = pidx;
+              pg_val = pidx + lane < p.n_req_pages ? p.pages[pidx + lane] : 0;
+            }
+            const int64_t page = __shfl_sync(0xffffffffu, pg_val, pidx - pg_base);
+            row_k[b] = int64_t(p.layer) * layer_rows + ((page * p.hkv + g) * 2 + 0) * p.S + (in_req ? key % p.S : 0);
+          }
+        }
         uint8_t* ks = smem + Lay::kK0 + st * Lay::kKVTile;
         uint8_t* vs = smem + Lay::kV0 + st * Lay::kKVTile;
-        mbar_arrive_expect_tx(&bars->k_full[st], Lay::kKVTile);
-        mbar_arrive_expect_tx(&bars->v_full[st], Lay::kKVTile);
-        for (int b0 = 0; b0 < kBlockN; b0 += box) {
-          const int key = (j_begin + it) * kBlockN + b0;
-          const bool in_req = key / p.S < p.n_req_pages;
-          const int pidx = in_req ? key / p.S : p.n_req_pages - 1;  // clamp: finite, masked
-          const int row_in_page = in_req ? key % p.S : 0;
-          const int64_t page = p.pages[pidx];
-          const int64_t row_k = int64_t(p.layer) * layer_rows + ((page * p.hkv + g) * 2 + 0) * p.S + row_in_page;
+        if (it >= kStages) mbar_wait(&bars->k_empty[st], ph);
+        if (elect_one()) {
+          if (PCR_ATTN_PROFILE & 4) {
+            mbar_arrive(&bars->k_full[st]);
+          } else {
+            mbar_arrive_expect_tx(&bars->k_full[st], Lay::kKVTile);
 #pragma unroll
-          for (int hf = 0; hf < Lay::kHalves; ++hf)
-            tma_load_2d(ks + hf * Lay::kKVHalf + b0 * 128, &tmap_pool, hf * 64, int32_t(row_k), &bars->k_full[st]);
+            for (int b = 0; b < 4; ++b)
 #pragma unroll
-          for (int hf = 0; hf < Lay::kHalves; ++hf)
-            tma_load_2d(vs + hf * Lay::kKVHalf + b0 * 128, &tmap_pool, hf * 64, int32_t(row_k + p.S),
-                        &bars->v_full[st]);
+              for (int hf = 0; hf < Lay::kHalves; ++hf)
+                if (b < n_box)
+                tma_load_2d(ks + hf * Lay::kKVHalf + b * box * 128, &tmap_pool, hf * 64, int32_t(row_k[b]),
+                            &bars->k_full[st]);
+          }
         }
+        __syncwarp();
+        if (it >= kStages) mbar_wait(&bars->v_empty[st], ph);
+        if (elect_one()) {
+          if (PCR_ATTN_PROFILE & 4) {
+            mbar_arrive(&bars->v_full[st]);
+          } else {
+            mbar_arrive_expect_tx(&bars->v_full[st], Lay::kKVTile);
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+#pragma unroll
+              for (int hf = 0; hf < Lay::kHalves; ++hf)
+                if (b < n_box)
+                tma_load_2d(vs + hf * Lay::kKVHalf + b * box * 128, &tmap_pool, hf * 64, int32_t(row_k[b] + p.S),
+                            &bars->v_full[st]);
+          }
+        }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
@@ -222,10 +288,11 @@ __global__ void __maxnreg__(136)
         const uint64_t kd = k_desc0 + uint64_t((it % kStages) * Lay::kKVTile >> 4);
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
+          for (int kk = 0; kk < D / 16 && (PCR_ATTN_PROFILE & 2) == 0; ++kk)
             mma_bf16_ss(tmem + (2 * t + (it & 1)) * kBlockN, qd + (((kk >> 2) * Lay::kQHalf + (kk & 3) * 32) >> 4),
                         kd + (((kk >> 2) * Lay::kKVHalf + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
           mma_commit(&bars->s_full[t][it & 1]);
+          if (t == kNQ - 1) mma_commit(&bars->k_empty[it % kStages]);
         }
         __syncwarp();
       };
@@ -233,11 +300,11 @@ __global__ void __maxnreg__(136)
         const uint64_t vd = v_desc0 + uint64_t((it % kStages) * Lay::kKVTile >> 4);
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < kBlockN / 16; ++kk)
+          for (int kk = 0; kk < kBlockN / 16 && (PCR_ATTN_PROFILE & 2) == 0; ++kk)
             mma_bf16_ts(tmem + Lay::kColO + t * D, tmem + (2 * t + (it & 1)) * kBlockN + kk * 8, vd + (kk * 2048 >> 4),
                         idesc_o, (it > 0 || kk > 0));
           mma_commit(&bars->o_done[t]);
-          if (t == kNQ - 1) mma_commit(&bars->kv_empty[it % kStages]);
+          if (t == kNQ - 1) mma_commit(&bars->v_empty[it % kStages]);
         }
         __syncwarp();
       };
@@ -246,21 +313,41 @@ __global__ void __maxnreg__(136)
         tc_fence_after();
         for (int t = 0; t < kNQ; ++t) issue_s(t, it);
       }
+      // Per Q tile: O_t += P_t(it) V(it), then S_t(it+2) into the buffer P_t(it) just left (MMAs of
+      // one thread run in issue order).  Tile 0's next S does not wait for tile 1's P, so the two
+      // softmax warpgroups settle out of phase (one in its exponentials while the other waits
+      // for S) instead of contending for MUFU in lockstep.
+#if PCR_ATTN_TIMING
+      long long mt_[5] = {0, 0, 0, 0, 0}, mc_ = clock64();
+#define PCR_MTICK(k) do { const long long n_ = clock64(); mt_[k] += n_ - mc_; mc_ = n_; } while (0)
+#else
+#define PCR_MTICK(k) do { } while (0)
+#endif
+      // The tensor pipe's instruction queue is shallow (about one MMA group): a pause between
+      // groups idles it, and every mbarrier wait costs ~100 clk even when its phase completed long
+      // ago.  So the MMA warp waits only for P: tile 0's softmax warpgroup checks that V(it) and
+      // K(it+2) have landed before it publishes P_0(it) (it has slack; the MMA warp has none).
+      //   [p_full(0,it)] PV_0(it) S_0(it+2) [p_full(1,it)] PV_1(it) S_1(it+2)
       for (int it = 0; it < n_iter; ++it) {
-        const int st = it % kStages;
-        mbar_wait(&bars->v_full[st], (it / kStages) & 1);
-        for (int t = 0; t < kNQ; ++t) {
-          mbar_wait(&bars->p_full[t][it & 1], (it >> 1) & 1);
-          tc_fence_after();
-          issue_pv(t, it);
-        }
-        if (it + 2 < n_iter) {  // S(it+2) reuses buffer it&1: issued after PV(it) read P(it) from it
-          const int st2 = (it + 2) % kStages;
-          mbar_wait(&bars->k_full[st2], ((it + 2) / kStages) & 1);
-          tc_fence_after();
-          for (int t = 0; t < kNQ; ++t) issue_s(t, it + 2);
-        }
+        const bool more = it + 2 < n_iter;
+        PCR_MTICK(2);
+        if ((PCR_ATTN_PROFILE & 8) == 0) mbar_wait(&bars->p_full[0][it & 1], (it >> 1) & 1);
+        tc_fence_after();
+        PCR_MTICK(1);
+        issue_pv(0, it);
+        if (more) issue_s(0, it + 2);
+        PCR_MTICK(2);
+        if ((PCR_ATTN_PROFILE & 8) == 0) mbar_wait(&bars->p_full[1][it & 1], (it >> 1) & 1);
+        tc_fence_after();
+        PCR_MTICK(1);
+        issue_pv(1, it);
+        if (more) issue_s(1, it + 2);
       }
+#if PCR_ATTN_TIMING
+      if ((threadIdx.x & 31) == 0 && (blockIdx.x == 0 || blockIdx.x == 300) && blockIdx.z == 0)
+        printf("MMATIMING blk %d iters %d: p-wait %lld issue %lld (clk/iter)\n", blockIdx.x, n_iter,
+               mt_[1] / max(n_iter, 1), mt_[2] / max(n_iter, 1));
+#endif
       if (elect_one()) mma_commit(&bars->o_full);
       __syncwarp();
     }
@@ -279,17 +366,38 @@ __global__ void __maxnreg__(136)
     // kPolyPairs of every 16 pairs), written over the S columns it came from, and the row sum
     // of the same bf16-rounded weights via FADD2 (R18).
     float m_raw = -INFINITY, l = 0.f;
+#if PCR_EXP_PINGPONG
+    if (t == 1 && n_iter > 0) named_bar_arrive(1, 256);  // tile 0 takes the first turn
+#endif
     const uint64_t scale2 = f2_pack(p.scale_log2, p.scale_log2);
+#if PCR_ATTN_TIMING
+    long long tm_[6] = {0, 0, 0, 0, 0, 0}, tc_ = clock64();
+#define PCR_TICK(k) do { const long long n_ = clock64(); tm_[k] += n_ - tc_; tc_ = n_; } while (0)
+#else
+#define PCR_TICK(k) do { } while (0)
+#endif
     for (int it = 0; it < n_iter; ++it) {
       const int key0 = (j_begin + it) * kBlockN;
       const bool diag = key0 + kBlockN - 1 > tile_first_key_limit;  // tile crosses this Q tile's diagonal
       const uint32_t s_col = lane_base + (2 * t + (it & 1)) * kBlockN;
+      PCR_TICK(5);
       mbar_wait(&bars->s_full[t][it & 1], (it >> 1) & 1);
       tc_fence_after();
+      PCR_TICK(0);
+      if (PCR_ATTN_PROFILE & 1) {
+        tc_fence_before();
+        if (t == 0) {
+          mbar_wait(&bars->v_full[it % kStages], (it / kStages) & 1);
+          if (it + 2 < n_iter) mbar_wait(&bars->k_full[(it + 2) % kStages], ((it + 2) / kStages) & 1);
+        }
+        mbar_arrive(&bars->p_full[t][it & 1]);
+        continue;
+      }
       float va[32], vb[32];
       tmem_ld32(s_col, va);
       tmem_ld32(s_col + 32, vb);
       tmem_ld_wait();
+      PCR_TICK(1);
       if (diag) {
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
@@ -312,7 +420,9 @@ __global__ void __maxnreg__(136)
       // a split-KV range can lie wholly past a row's causal limit: nothing visible yet
       const float neg_m = m_use == -INFINITY ? 0.f : -m_use * p.scale_log2;
       const uint64_t negm2 = f2_pack(neg_m, neg_m);
-      const float alpha = ex2(fmaf(m_raw, p.scale_log2, neg_m));
+      // alpha = 2^((m_raw - m_use) * scale) is exactly 1 unless this row rescales: no MUFU op in the
+      // common case (it would queue behind the other warpgroup's exponentials)
+      const float alpha = rescale ? ex2(fmaf(m_raw, p.scale_log2, neg_m)) : 1.f;
       if (it > 0 && __any_sync(0xffffffffu, rescale)) {
         // O_t must hold PV_t(it-1) before it is rescaled
         mbar_wait(&bars->o_done[t], (it - 1) & 1);
@@ -327,9 +437,11 @@ __global__ void __maxnreg__(136)
           tmem_st32(o_col + c * 32, o);
         }
       }
-      uint64_t sum4[4] = {0, 0, 0, 0};  // four independent FADD2 chains
+      PCR_TICK(2);
+      // P = bf16(2^(s*scale - m)) (MUFU, or the FMA-pipe polynomial for kPolyPairs of every 16
+      // pairs), written over the S columns it came from
+      uint32_t pk[2][16];
       auto exp_chunk = [&](float* v, int c) {
-        uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           const uint64_t x2 = ffma2(f2_pack(v[e], v[e + 1]), scale2, negm2);
@@ -343,23 +455,56 @@ __global__ void __maxnreg__(136)
             y1 = ex2(x1);
           }
           __nv_bfloat162 b = __floats2bfloat162_rn(y0, y1);
-          const uint32_t w = *reinterpret_cast<uint32_t*>(&b);
-          pk[e / 2] = w;
-          sum4[(e >> 1) & 3] =
-              fadd2(sum4[(e >> 1) & 3], f2_pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u)));
+          pk[c][e / 2] = *reinterpret_cast<uint32_t*>(&b);
         }
-        tmem_st16(s_col + c * 16, pk);   // P chunk c -> columns [16c, 16c+16): already read
+        tmem_st16(s_col + c * 16, pk[c]);   // P chunk c -> columns [16c, 16c+16): already read
       };
+#if PCR_EXP_PINGPONG
+      // The two warpgroups take turns on the exponentials (they share each SMSP's MUFU): wait for
+      // the other one to finish its exp phase, run ours, hand the turn back.  Tile 0 first checks
+      // that V(it) and K(it+2) have landed (the MMA warp issues PV(it) and S(it+2) on P_0(it) alone);
+      // those waits hide inside the wait for the turn.
+      if (t == 0) {
+        mbar_wait(&bars->v_full[it % kStages], (it / kStages) & 1);
+        if (it + 2 < n_iter) mbar_wait(&bars->k_full[(it + 2) % kStages], ((it + 2) / kStages) & 1);
+      }
+      named_bar_sync(1 + t, 256);
+#endif
       exp_chunk(va, 0);
       exp_chunk(vb, 1);
-      float s0, s1;
-      f2_unpack(fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3])), s0, s1);
-      l = l * alpha + (s0 + s1);
+#if PCR_EXP_PINGPONG
+      if (!(t == 1 && it == n_iter - 1)) named_bar_arrive(2 - t, 256);
+#endif
+      PCR_TICK(3);
       tmem_st_wait();
       tc_fence_before();
+#if !PCR_EXP_PINGPONG
+      if (t == 0) {  // the MMA warp issues PV(it) and S(it+2) on P_0(it) alone
+        mbar_wait(&bars->v_full[it % kStages], (it / kStages) & 1);
+        if (it + 2 < n_iter) mbar_wait(&bars->k_full[(it + 2) % kStages], ((it + 2) / kStages) & 1);
+      }
+#endif
       mbar_arrive(&bars->p_full[t][it & 1]);
+      // row sum of the same bf16-rounded weights (R18), off the MMA warp's critical path:
+      // fp32 += bf16 (FHADD.BF16), four independent chains
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
+              "add.rn.f32.bf16 %0, lo, %0;\n\tadd.rn.f32.bf16 %1, hi, %1;\n\t}"
+              : "+f"(acc[(e & 1) * 2]), "+f"(acc[(e & 1) * 2 + 1]) : "r"(pk[c][e]));
+      l = l * alpha + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+      PCR_TICK(4);
       m_raw = m_use;
     }
+#if PCR_ATTN_TIMING
+    if ((threadIdx.x & 31) == 0 && (blockIdx.x == 0 || blockIdx.x == 300) && blockIdx.z == 0)
+      printf("TIMING blk %d warp %d iters %d: wait %lld ld %lld max %lld exp %lld st+arrive %lld loop %lld (clk/iter)\n",
+             blockIdx.x, threadIdx.x >> 5, n_iter, tm_[0] / max(n_iter, 1), tm_[1] / max(n_iter, 1),
+             tm_[2] / max(n_iter, 1), tm_[3] / max(n_iter, 1), tm_[4] / max(n_iter, 1), tm_[5] / max(n_iter, 1));
+#endif
     // ---------------------------------------------------------------- epilogue
     const bool row_ok = i < p.n2;
     const int64_t row_id = int64_t(i) * p.hq + qh;

@@ -7,6 +7,7 @@ import argparse
 import json
 import os
 import sys
+import threading
 
 import numpy as np
 import torch
@@ -42,22 +43,40 @@ def run(n1, n2, hq, hkv, d=128, L=4, iters=20, C=256, S=64):
     ctx.run_prefill(1, q, k, v, o, cs, ls)   # loads the pool, warms up
     cs.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = []
+    stop = threading.Event()
+
+    def poll():
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(0)
+            while not stop.is_set():
+                clk.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                stop.wait(0.005)
+        except Exception:
+            pass
+    th = threading.Thread(target=poll, daemon=True)
+    th.start()
     a.record(cs)
     for _ in range(iters):
         for l in range(L):
             ctx.prefill_attn_layer(1, l, q[l], k[l], v[l], o[l], cs)
     b.record(cs)
     b.synchronize()
+    stop.set()
+    th.join()
     ms = a.elapsed_time(b) / (iters * L)
     flops = 4 * hq * d * (n2 * n1 + n2 * (n2 + 1) // 2)
     ctx.release(1, False)
     ctx.close()
-    return dict(n1=n1, n2=n2, hq=hq, hkv=hkv, ms_per_layer=ms, tflops=flops / ms / 1e9)
+    return dict(n1=n1, n2=n2, hq=hq, hkv=hkv, ms_per_layer=ms, tflops=flops / ms / 1e9,
+                sm_mhz=sorted(clk)[len(clk) // 2] if clk else None)
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--iters", type=int, default=40)
     args = ap.parse_args()
     for n1, n2, hq, hkv in [(0, 8320, 32, 8), (4096, 4224, 32, 8), (6144, 2176, 32, 8), (4096, 128, 32, 8),
                             (8192, 8320, 64, 8)]:
