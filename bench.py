@@ -21,6 +21,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import shutil
 import statistics
 import subprocess
 import sys
@@ -380,7 +381,7 @@ def run_ours(args):
         cs.wait_stream(ls)
         return None
 
-    def step(q, k, v, out, times=False, load_events=None):
+    def step(q, k, v, out, times=False, load_events=None, step_mode=None):
         """One request.  The caller's stream sync precedes pcr_release (pages are reused)."""
         rid = req_counter[0]
         req_counter[0] += 1
@@ -396,7 +397,8 @@ def run_ours(args):
         elif world > 1 and lib_comm:
             t = ctx.run_prefill_sharded(rid, q, k, v, out, gathered, cs, ls, xs, mode=mode, layer_times=times)
         else:
-            t = ctx.run_prefill(rid, q, k, v, out, cs, ls, mode=mode, layer_times=times)
+            t = ctx.run_prefill(rid, q, k, v, out, cs, ls, mode=mode if step_mode is None else step_mode,
+                                layer_times=times)
             if world > 1:   # fallback re-assembly (rank-major [P][L][N2][Hq/P][d] instead of per layer)
                 with torch.cuda.stream(cs):
                     dist.all_gather_into_tensor(gathered.view(-1), out.view(-1))
@@ -454,8 +456,12 @@ def run_ours(args):
         lt = np.array([step(q_d, k_d, v_d, out_d, times=True) for _ in range(max(1, args.profile_steps))])
         attn_ms = float(lt[:, :, 1].mean())
         gather_ms_evented = float(lt[:, :, 0].mean())
+        # the same kernels with nothing running beside them (SYNC order: gather, then attention)
+        lt_iso = np.array([step(q_d, k_d, v_d, out_d, times=True, step_mode=MODE_SYNC)
+                           for _ in range(max(1, args.profile_steps))]) if world == 1 else None
+        attn_ms_iso = float(lt_iso[:, :, 1].mean()) if lt_iso is not None else float("nan")
     else:   # per-layer events are not recorded on the layer-body path
-        attn_ms = gather_ms_evented = float("nan")
+        attn_ms = gather_ms_evented = attn_ms_iso = float("nan")
 
     # e2e: the same step through the C-ABI with HOST buffers (H2D of q/k/v, D2H of out, per step)
     e2e = None
@@ -541,7 +547,12 @@ def run_ours(args):
         "unit": "TFLOP/s", "frac": attn_tflops / bf16_peak,
         "traffic": ncu_t.get("attn_M7_r05", {}).get("dram_bytes") if (args.workload, args.ratio) == ("M7", 0.5) else None,
         "peak_source": bf16_src,
-        "algorithmic_flops_per_launch": attn_flops, "avg_launch_ms": attn_ms}
+        "algorithmic_flops_per_launch": attn_flops, "avg_launch_ms": attn_ms,
+        "note": "append+attention per layer as it runs in the pipeline (beside the next layer's gather "
+                "in OVERLAP mode); isolated = the same launches with nothing beside them",
+        "isolated": None if attn_ms_iso != attn_ms_iso else {
+            "avg_launch_ms": attn_ms_iso, "achieved": attn_flops / (attn_ms_iso * 1e-3) / 1e12,
+            "frac": attn_flops / (attn_ms_iso * 1e-3) / 1e12 / bf16_peak}}
     line = {
         "metric": f"reuse-prefill tokens/s ({args.workload}: context tokens N1+N2 per second; TTFT in ttft_ms)",
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -593,6 +604,13 @@ def run_trace_z(args):
     pool = torch.empty(2 * pages_req * page_elems + page_elems, dtype=torch.int16, device="cuda")
     t0 = time.perf_counter()
     ssd_chunks = int(args.ssd_frac * len(distinct))
+    if ssd_chunks:
+        # the tier file is pre-sized: refuse (loudly) rather than fill the disk
+        rec = L * Hkv * 2 * C * d * 2
+        free = shutil.disk_usage(os.path.dirname(os.path.abspath(args.ssd_path))).free
+        if ssd_chunks * rec > 0.8 * free:
+            sys.exit(f"bench: SSD tier of {ssd_chunks} x {rec >> 20} MiB = {ssd_chunks * rec / 1e9:.0f} GB does not "
+                     f"fit in 80% of the {free / 1e9:.0f} GB free under {args.ssd_path}; lower --ssd-frac or --requests")
     ctx = Context(L, Hq, Hkv, d, C, S, cap, args.window, device=0, pool=pool, max_tokens=max_n,
                   gather_ctas=args.gather_ctas, ssd_path=args.ssd_path if ssd_chunks else None,
                   ssd_chunks=ssd_chunks)

@@ -94,7 +94,9 @@ typedef struct pcr_config {
   /* SSD tier (§8 f2): a file of ssd_chunks chunk records behind the DRAM store.
    * Committed chunks are written back asynchronously; chunks of requests in the
    * look-ahead window that are only on the SSD are prefetched into DRAM by an I/O thread
-   * (P:456); a scheduled request's SSD-only chunks are loaded on demand.  NULL / 0 = no SSD. */
+   * (P:456); a scheduled request's SSD-only chunks are loaded on demand.  NULL / 0 = no SSD.
+   * The library creates (truncates) the file at pcr_create and removes it at pcr_destroy: the
+   * records are meaningless without the context's in-memory index. */
   const char* ssd_path;
   int64_t ssd_chunks;
 } pcr_config;

@@ -9,7 +9,8 @@
 
 namespace pcr {
 
-SsdIo::SsdIo(const std::string& path, int64_t n_slots, int64_t record_bytes) : record_bytes_(record_bytes) {
+SsdIo::SsdIo(const std::string& path, int64_t n_slots, int64_t record_bytes)
+    : record_bytes_(record_bytes), path_(path) {
   // O_DIRECT (true device reads, no page cache) when records are block aligned; buffered otherwise.
   if (record_bytes % 4096 == 0) {
     fd_ = ::open(path.c_str(), O_RDWR | O_CREAT | O_TRUNC | O_DIRECT, 0600);
@@ -36,7 +37,10 @@ SsdIo::~SsdIo() {
   }
   cv_task_.notify_all();
   if (worker_.joinable()) worker_.join();
-  if (fd_ >= 0) ::close(fd_);
+  if (fd_ >= 0) {
+    ::close(fd_);
+    ::unlink(path_.c_str());   // the records are meaningless without this context's index
+  }
 }
 
 int64_t SsdIo::read(int64_t slot, void* dst) {

@@ -41,6 +41,7 @@ class SsdIo {
   bool direct_ = false;
   int64_t record_bytes_ = 0;
   std::string err_;
+  std::string path_;   // created (truncated) at construction, removed at destruction
   std::mutex mu_;
   std::condition_variable cv_task_, cv_done_;
   std::deque<Task> q_;

@@ -75,3 +75,12 @@ def test_zipf_trace_with_ssd_tier(tmp_path):
     reqs, _, ndoc = zipf_trace(seed=4, n_requests=300, C=256)
     st = _run(tmp_path, reqs, 256, 64, 120, 1000, 4, tag="z", n_cacheable=ndoc)
     assert st["prefetch"] > 0 and st["writeback"] > 0
+
+
+def test_ssd_file_lifecycle(tmp_path):
+    """pcr_create creates the tier file (sized for ssd_chunks records); pcr_destroy removes it."""
+    lib = _ctx(tmp_path, 4, 4, 4, 16, 0, tag="life")
+    f = tmp_path / "ssd_life.bin"
+    assert f.exists() and f.stat().st_size == 16 * lib.slot_bytes
+    lib.close()
+    assert not f.exists()

@@ -2,20 +2,33 @@
 # Workload coverage: Z trace (W sweep, DRAM only / + SSD tier), f3 layer body, L70, T.
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-OUT=gpurun_out/workloads.jsonl; : > $OUT
+OUT=gpurun_out/workloads.jsonl; [ -n "$APPEND" ] || : > $OUT
+# SECTIONS (default all): z ssd f3 l70 t
+rm -f /tmp/pcr_ssd_tier.bin   # a leftover tier file from an interrupted run
 df -h /tmp | tail -1 > gpurun_out/disk.txt
+S=" ${SECTIONS:-z ssd f3 l70 t} "
+if [[ $S == *" z "* ]]; then
 for W in 0 4; do
   timeout 900 python bench.py --workload Z --window $W >> $OUT 2>> gpurun_out/workloads.err; echo "Z W=$W rc=$?"
 done
-timeout 900 python bench.py --workload Z --window 4 --store-frac 0.03 --ssd-frac 0.25 >> $OUT 2>> gpurun_out/workloads.err; echo "Z ssd rc=$?"
-timeout 900 python bench.py --workload Z --window 0 --store-frac 0.03 --ssd-frac 0.25 >> $OUT 2>> gpurun_out/workloads.err; echo "Z ssd W0 rc=$?"
+fi
+if [[ $S == *" ssd "* ]]; then
+timeout 900 python bench.py --workload Z --window 4 --requests 300 --store-frac 0.03 --ssd-frac 0.25 >> $OUT 2>> gpurun_out/workloads.err; echo "Z ssd rc=$?"
+timeout 900 python bench.py --workload Z --window 0 --requests 300 --store-frac 0.03 --ssd-frac 0.25 >> $OUT 2>> gpurun_out/workloads.err; echo "Z ssd W0 rc=$?"
+fi
+if [[ $S == *" f3 "* ]]; then
 timeout 300 python bench.py --steps 10 --warmup 2 --no-e2e --no-cpu-baseline --layer-body >> $OUT 2>> gpurun_out/workloads.err; echo "f3 L8 rc=$?"
 timeout 300 python bench.py --workload M7 --ratio 0.5 --steps 10 --warmup 2 --no-e2e --no-cpu-baseline --layer-body >> $OUT 2>> gpurun_out/workloads.err; echo "f3 M7 rc=$?"
 timeout 300 python bench.py --workload M7 --ratio 1.0 --steps 10 --warmup 2 --no-e2e --no-cpu-baseline --layer-body >> $OUT 2>> gpurun_out/workloads.err; echo "f3 M7 r1 rc=$?"
+fi
+if [[ $S == *" l70 "* ]]; then
 for r in 0.5 1.0; do
   timeout 600 python bench.py --workload L70 --ratio $r --steps 5 --warmup 2 --no-e2e --no-cpu-baseline >> $OUT 2>> gpurun_out/workloads.err; echo "L70 $r rc=$?"
 done
+fi
+if [[ $S == *" t "* ]]; then
 timeout 300 python bench.py --workload T --steps 20 --warmup 3 --no-e2e --no-cpu-baseline >> $OUT 2>> gpurun_out/workloads.err; echo "T rc=$?"
+fi
 python - <<'PY'
 import json
 for l in open("gpurun_out/workloads.jsonl"):
