@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define PCR_ABI_VERSION 2
+#define PCR_ABI_VERSION 3
 
 typedef struct pcr_ctx pcr_ctx;
 
@@ -270,11 +270,17 @@ typedef struct pcr_run_opts {
   void* gathered_all;      /* nullable: per-layer NCCL all-gather target (pcr_run_prefill_sharded) */
   float* layer_times_ms;   /* nullable: [3L] per-layer gather, append+attention, offload (ms); blocks */
   int32_t mode;            /* 0 OVERLAP, 1 SYNC (everything in order on compute_stream) */
-  int32_t reserved0;
+  int32_t host_io;         /* 1: q_all/k_all/v_all/out_all are PAGE-LOCKED HOST buffers (cudaHostAlloc /
+                            * cudaHostRegister; PCR_E_INVAL otherwise).  Layer l's q/k/v are copied
+                            * into a library-owned double-buffered device staging area on an
+                            * internal stream ahead of its attention and its output is copied back
+                            * right after it, so the host I/O overlaps the layer pipeline.  Not
+                            * combinable with gathered_all. */
 } pcr_run_opts;
 
 /* The full per-request pipeline: pcr_run_prefill + (optional) offload on a third stream, the
- * per-layer event chain being load(l) -> append+attn(l) -> offload(l) (and -> all-gather(l)). */
+ * per-layer event chain being load(l) -> append+attn(l) -> offload(l) (and -> all-gather(l));
+ * with host_io, [H2D q/k/v(l)] -> append+attn(l) -> [D2H out(l)] on internal copy streams. */
 pcr_status pcr_run_prefill_ex(pcr_ctx* ctx, int64_t req_id, const void* q_all, const void* k_all,
                               const void* v_all, void* out_all, const pcr_run_opts* opts);
 

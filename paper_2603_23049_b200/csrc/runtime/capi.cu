@@ -62,6 +62,12 @@ struct pcr_ctx {
   std::vector<cudaEvent_t> ev_attn;
   cudaEvent_t ev_comm = nullptr;
   cudaEvent_t ev_off = nullptr;
+  // host_io staging (pcr_run_opts.host_io): [2][q | k | v | out] of one layer, grown on demand
+  uint16_t* io_buf = nullptr;
+  int64_t io_buf_elems = 0;
+  cudaStream_t io_h2d = nullptr, io_d2h = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_outdone;   // per layer: inputs staged / output copied back
+  cudaEvent_t ev_io_join = nullptr;
 };
 
 namespace {
@@ -248,6 +254,43 @@ pcr_status enqueue_offload(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s
   return PCR_OK;
 }
 
+bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();   // clear the sticky-free error of an unknown pointer
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// host_io: streams, per-layer events and a [2][q | k | v | out] staging area for one layer.
+pcr_status ensure_host_io(pcr_ctx* c, int64_t layer_elems) {
+  if (!c->io_h2d) {
+    int lo = 0, hi = 0;
+    CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->io_h2d, cudaStreamNonBlocking, hi));
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->io_d2h, cudaStreamNonBlocking));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_io_join, cudaEventDisableTiming));
+    for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
+      cudaEvent_t a, b;
+      CUDA_TRY(c, cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      c->ev_in.push_back(a);
+      CUDA_TRY(c, cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      c->ev_outdone.push_back(b);
+    }
+  }
+  if (2 * layer_elems > c->io_buf_elems) {
+    if (c->io_buf) {
+      CUDA_TRY(c, cudaDeviceSynchronize());   // rare: the staging area grows to the largest N2 seen
+      CUDA_TRY(c, cudaFree(c->io_buf));
+      c->io_buf = nullptr;
+    }
+    CUDA_TRY(c, cudaMalloc(reinterpret_cast<void**>(&c->io_buf), 2 * layer_elems * sizeof(uint16_t)));
+    c->io_buf_elems = 2 * layer_elems;
+  }
+  return PCR_OK;
+}
+
 pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const void* k_all, const void* v_all,
                             void* out_all, const pcr_run_opts& o, int times_stride) {
   if (!c) return PCR_E_INVAL;
@@ -262,6 +305,10 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
     return fail(c, PCR_E_INVAL, "OVERLAP mode needs a load stream distinct from the compute stream");
   if (o.gathered_all && (!o.comm_stream || !c->nccl_comm))
     return fail(c, o.comm_stream ? PCR_E_STATE : PCR_E_INVAL, "all-gather needs pcr_comm_init and a comm stream");
+  if (o.host_io != 0 && o.host_io != 1) return fail(c, PCR_E_INVAL, "host_io must be 0 or 1");
+  if (o.host_io && o.gathered_all) return fail(c, PCR_E_INVAL, "host_io cannot be combined with gathered_all");
+  if (o.host_io && !(is_pinned_host(q_all) && is_pinned_host(k_all) && is_pinned_host(v_all) && is_pinned_host(out_all)))
+    return fail(c, PCR_E_INVAL, "host_io needs page-locked host q/k/v/out buffers");
   cudaStream_t cs = static_cast<cudaStream_t>(o.compute_stream);
   cudaStream_t ls = o.mode == 0 ? static_cast<cudaStream_t>(o.load_stream) : cs;
   cudaStream_t os = o.offload_stream ? (o.mode == 0 ? static_cast<cudaStream_t>(o.offload_stream) : cs) : nullptr;
@@ -273,6 +320,35 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
   if (o.gathered_all && !api) return fail(c, PCR_E_UNSUPPORTED, "libnccl.so.2 not loadable");
   if ((st = ensure_tables(c, r, ls)) != PCR_OK) return st;
   if (o.mode == 0) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->region_ev[r->plan.region], 0));
+  // host_io: layer l's inputs/outputs go through staging buffer l % 2 (q | k | v | out)
+  const int64_t io_layer = 2 * q_layer + 2 * kv_layer;
+  cudaStream_t hs = cs, ds = cs;
+  if (o.host_io) {
+    if ((st = ensure_host_io(c, io_layer)) != PCR_OK) return st;
+    if (o.mode == 0) {
+      hs = c->io_h2d;
+      ds = c->io_d2h;
+      CUDA_TRY(c, cudaEventRecord(c->ev_io_join, cs));    // staging may still be read by earlier work
+      CUDA_TRY(c, cudaStreamWaitEvent(hs, c->ev_io_join, 0));
+      CUDA_TRY(c, cudaStreamWaitEvent(ds, c->ev_io_join, 0));
+    }
+  }
+  auto stage = [&](int32_t l) -> pcr_status {   // H2D of layer l's q/k/v into buffer l % 2
+    uint16_t* b = c->io_buf + (l & 1) * io_layer;
+    if (o.mode == 0 && l >= 2) CUDA_TRY(c, cudaStreamWaitEvent(hs, c->ev_attn[l - 2], 0));  // buffer free
+    CUDA_TRY(c, cudaMemcpyAsync(b, static_cast<const uint16_t*>(q_all) + l * q_layer, q_layer * 2,
+                                cudaMemcpyHostToDevice, hs));
+    CUDA_TRY(c, cudaMemcpyAsync(b + q_layer, static_cast<const uint16_t*>(k_all) + l * kv_layer, kv_layer * 2,
+                                cudaMemcpyHostToDevice, hs));
+    CUDA_TRY(c, cudaMemcpyAsync(b + q_layer + kv_layer, static_cast<const uint16_t*>(v_all) + l * kv_layer,
+                                kv_layer * 2, cudaMemcpyHostToDevice, hs));
+    if (o.mode == 0) CUDA_TRY(c, cudaEventRecord(c->ev_in[l], hs));
+    return PCR_OK;
+  };
+  if (o.host_io && o.mode == 0) {
+    for (int32_t l = 0; l < std::min<int32_t>(2, c->cfg.n_layers); ++l)
+      if ((st = stage(l)) != PCR_OK) return st;
+  }
   for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
     cudaEvent_t* et = &c->ev_t[6 * l];
     if (times) CUDA_TRY(c, cudaEventRecord(et[0], ls));
@@ -282,14 +358,37 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
       CUDA_TRY(c, cudaEventRecord(c->ev_load[l], ls));
       CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_load[l], 0));
     }
-    if (times) CUDA_TRY(c, cudaEventRecord(et[2], cs));
+    const uint16_t *q_l = static_cast<const uint16_t*>(q_all) + l * q_layer,
+                   *k_l = static_cast<const uint16_t*>(k_all) + l * kv_layer,
+                   *v_l = static_cast<const uint16_t*>(v_all) + l * kv_layer;
     uint16_t* out_l = static_cast<uint16_t*>(out_all) + l * q_layer;
-    st = enqueue_attn(c, r, l, static_cast<const uint16_t*>(q_all) + l * q_layer,
-                      static_cast<const uint16_t*>(k_all) + l * kv_layer,
-                      static_cast<const uint16_t*>(v_all) + l * kv_layer, out_l, cs);
+    if (o.host_io) {
+      uint16_t* b = c->io_buf + (l & 1) * io_layer;
+      if (o.mode == 1 && (st = stage(l)) != PCR_OK) return st;
+      if (o.mode == 0) {
+        CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_in[l], 0));
+        if (l >= 2) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_outdone[l - 2], 0));  // out buffer drained
+      }
+      q_l = b;
+      k_l = b + q_layer;
+      v_l = b + q_layer + kv_layer;
+      out_l = b + q_layer + 2 * kv_layer;
+    }
+    if (times) CUDA_TRY(c, cudaEventRecord(et[2], cs));
+    st = enqueue_attn(c, r, l, q_l, k_l, v_l, out_l, cs);
     if (st != PCR_OK) return st;
     if (times) CUDA_TRY(c, cudaEventRecord(et[3], cs));
-    if (os || o.gathered_all) CUDA_TRY(c, cudaEventRecord(c->ev_attn[l], cs));
+    if (os || o.gathered_all || o.host_io) CUDA_TRY(c, cudaEventRecord(c->ev_attn[l], cs));
+    if (o.host_io) {
+      // D2H of this layer's output while the next layers run; then stage layer l+2's inputs
+      if (ds != cs) CUDA_TRY(c, cudaStreamWaitEvent(ds, c->ev_attn[l], 0));
+      CUDA_TRY(c, cudaMemcpyAsync(static_cast<uint16_t*>(out_all) + l * q_layer, out_l, q_layer * 2,
+                                  cudaMemcpyDeviceToHost, ds));
+      if (o.mode == 0) {
+        CUDA_TRY(c, cudaEventRecord(c->ev_outdone[l], ds));
+        if (l + 2 < c->cfg.n_layers && (st = stage(l + 2)) != PCR_OK) return st;
+      }
+    }
     if (os) {
       // layer-wise offload of the new chunks right after this layer's KV exists
       if (os != cs) CUDA_TRY(c, cudaStreamWaitEvent(os, c->ev_attn[l], 0));
@@ -317,6 +416,12 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
   if (o.gathered_all) {
     CUDA_TRY(c, cudaEventRecord(c->ev_comm, xs));
     CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_comm, 0));
+  }
+  if (o.host_io && o.mode == 0) {   // the last outputs have reached the host buffer
+    CUDA_TRY(c, cudaEventRecord(c->ev_io_join, ds));
+    CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_io_join, 0));
+    CUDA_TRY(c, cudaEventRecord(c->ev_io_join, hs));
+    CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_io_join, 0));
   }
   if (times) {
     CUDA_TRY(c, cudaStreamSynchronize(cs));
@@ -468,6 +573,12 @@ void pcr_destroy(pcr_ctx* c) {
     if (c->ev_comm) cudaEventDestroy(c->ev_comm);
     if (c->ev_off) cudaEventDestroy(c->ev_off);
     for (auto e : c->ev_attn) cudaEventDestroy(e);
+    for (auto e : c->ev_in) cudaEventDestroy(e);
+    for (auto e : c->ev_outdone) cudaEventDestroy(e);
+    if (c->ev_io_join) cudaEventDestroy(c->ev_io_join);
+    if (c->io_h2d) cudaStreamDestroy(c->io_h2d);
+    if (c->io_d2h) cudaStreamDestroy(c->io_d2h);
+    if (c->io_buf) cudaFree(c->io_buf);
     if (c->nccl_comm) {
       if (const pcr::NcclApi* api = pcr::nccl_api()) api->comm_destroy(c->nccl_comm);
     }

@@ -124,6 +124,35 @@ def test_overlap_sync_and_per_layer_api_are_bitwise_identical():
     assert np.array_equal(to_host(o), out)
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+def test_host_io_matches_device_buffers(mode):
+    """pcr_run_prefill_ex with host_io: page-locked HOST q/k/v/out, staged per layer by the library
+    on its own copy streams, gives the device-buffer result bit for bit (OVERLAP and SYNC); 5 layers
+    so the double-buffered staging wraps; pageable host memory is refused."""
+    L, n1, n2 = 5, 1024, 130
+    rig, plan, q, k, v, out = _single_request("iid", L, 32, 8, 128, 256, 64, n1, n2, seed=9)
+    rig.ctx.release(1, True)
+    rng = make_rng(9)
+    doc = rng.integers(0, 1000, n1, dtype=np.uint32)
+    toks = np.concatenate([doc, rng.integers(0, 1000, n2, dtype=np.uint32)])
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).pin_memory()  # noqa: E731
+    qh, kh, vh = pin(q), pin(k[:, n1:]), pin(v[:, n1:])
+    oh = torch.zeros_like(qh).pin_memory()
+    for rid in (2, 3):
+        rig.ctx.submit(rid, toks, n_cacheable=n1)
+        assert rig.ctx.match_prefix(rid, [])["n1"] == n1
+        rig.ctx.run_prefill_ex(rid, qh, kh, vh, oh, rig.cs, rig.ls, mode=mode, host_io=True)
+        rig.cs.synchronize()
+        assert np.array_equal(oh.numpy().view(np.uint16), out), rid
+        rig.ctx.release(rid, True)
+        oh.zero_()
+    rig.ctx.submit(4, toks, n_cacheable=n1)
+    rig.ctx.match_prefix(4, [])
+    with pytest.raises(Exception):
+        rig.ctx.run_prefill_ex(4, torch.from_numpy(q.view(np.int16)), kh, vh, oh, rig.cs, rig.ls, mode=mode,
+                               host_io=True)
+
+
 def test_page_size_does_not_change_results():
     outs = []
     for S in (16, 32, 64, 128):
