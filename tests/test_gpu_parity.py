@@ -35,20 +35,25 @@ def _warm_prefix(rig, req_id, doc_tokens, k_ctx, v_ctx, n_chunks):
     rig.ctx.release(req_id, True)
 
 
-def _single_request(kind, L, Hq, Hkv, d, C, S, N1, N2, seed, mode=0, world=1, rank=0, **ctx_kw):
-    """Warm N1 tokens, then run one request [doc | query] and return everything to compare."""
+def _single_request(kind, L, Hq, Hkv, d, C, S, N1, N2, seed, mode=0, world=1, rank=0, local_only=False,
+                    **ctx_kw):
+    """Warm N1 tokens, then run one request [doc | query] and return everything to compare.
+    local_only: draw only this rank's heads (full-size sharded shapes) instead of slicing them out
+    of all heads."""
     rng = make_rng(seed)
     Hkv_l, Hq_l = Hkv // world, Hq // world
     q, k, v = [], [], []
     for l in range(L):
-        ql, kl, vl = stress_values(kind, seed * 100 + l, N1, N2, Hq, Hkv, d)
+        ql, kl, vl = stress_values(kind, seed * 100 + l, N1, N2, Hq_l if local_only else Hq,
+                                   Hkv_l if local_only else Hkv, d)
         q.append(ql)
         k.append(kl)
         v.append(vl)
     q, k, v = np.stack(q), np.stack(k), np.stack(v)       # [L][N2][Hq][d], [L][N][Hkv][d]
-    hs = slice(rank * Hkv_l, (rank + 1) * Hkv_l)
-    qs = slice(rank * Hq_l, (rank + 1) * Hq_l)
-    q, k, v = q[:, :, qs], k[:, :, hs], v[:, :, hs]
+    if not local_only:
+        hs = slice(rank * Hkv_l, (rank + 1) * Hkv_l)
+        qs = slice(rank * Hq_l, (rank + 1) * Hq_l)
+        q, k, v = q[:, :, qs], k[:, :, hs], v[:, :, hs]
     n_pages = (N1 + N2) // S + 8
     rig = Rig(L, Hq, Hkv, d, C, S, store_chunks=max(1, N1 // C) + 2, n_pool_pages=n_pages + N1 // S + 2,
               rank=rank, world=world, **ctx_kw)
@@ -247,6 +252,36 @@ def test_l8_full_size_sampled():
         kc, vc = rig.expected_context(plan, k[:, N1:], v[:, N1:], l)
         r, m = check_attention(out[l], q[l], kc, vc, N1, rows=rows)
         assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (l, r, m)
+
+
+def _check_sampled(rig, plan, q, k, v, out, N1, N2, C, S, layers, seed):
+    rows = sample_rows(N2, N1, C, S, k=48, seed=seed)
+    pool = rig.pool_np()
+    for l in layers:
+        exp_pool = rig.expected_pool(plan, k[:, N1:], v[:, N1:], l)
+        assert np.array_equal(pool[l][plan["pages"]], exp_pool[l][plan["pages"]]), l
+        kc, vc = rig.expected_context(plan, k[:, N1:], v[:, N1:], l)
+        r, m = check_attention(out[l], q[l], kc, vc, N1, rows=rows)
+        assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (l, r, m)
+
+
+def test_m7_half_hit_full_size_sampled():
+    """configs[2] (Mistral-7B shape, 8k-token document context) at 50% prefix hit, full size,
+    OVERLAP: 32 layers, N1 = 4096 cached + N2 = 4224 computed (multi-wave attention grid, no KV
+    split); sampled rows vs the oracle and the pool bit-exact on layers 0, 17, 31."""
+    L, Hq, Hkv, d, C, S, N1, N2 = 32, 32, 8, 128, 256, 64, 4096, 4224
+    rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, N1, N2, seed=4)
+    _check_sampled(rig, plan, q, k, v, out, N1, N2, C, S, (0, 17, 31), seed=4)
+
+
+def test_l70_rank_slice_full_size_sampled():
+    """configs[3] (Llama-3-70B shape, 80 layers, 64/8 heads) KV-head-sharded over 8 GPUs: the
+    per-GPU workload of rank 5 (8 query heads, 1 KV head) at 16k context, 50% hit -- N1 = 8192
+    cached + N2 = 8320 computed; sampled rows and pool on layers 0, 41, 79."""
+    L, Hq, Hkv, d, C, S, N1, N2 = 80, 64, 8, 128, 256, 64, 8192, 8320
+    rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, N1, N2, seed=6, world=8, rank=5,
+                                              local_only=True)
+    _check_sampled(rig, plan, q, k, v, out, N1, N2, C, S, (0, 41, 79), seed=6)
 
 
 def test_sharded_run_with_nccl_allgather_world1():
