@@ -371,7 +371,7 @@ __global__ void __maxnreg__(136)
 #endif
     const uint64_t scale2 = f2_pack(p.scale_log2, p.scale_log2);
 #if PCR_ATTN_TIMING
-    long long tm_[6] = {0, 0, 0, 0, 0, 0}, tc_ = clock64();
+    long long tm_[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tc_ = clock64();
 #define PCR_TICK(k) do { const long long n_ = clock64(); tm_[k] += n_ - tc_; tc_ = n_; } while (0)
 #else
 #define PCR_TICK(k) do { } while (0)
@@ -468,7 +468,9 @@ __global__ void __maxnreg__(136)
         mbar_wait(&bars->v_full[it % kStages], (it / kStages) & 1);
         if (it + 2 < n_iter) mbar_wait(&bars->k_full[(it + 2) % kStages], ((it + 2) / kStages) & 1);
       }
+      PCR_TICK(6);
       named_bar_sync(1 + t, 256);
+      PCR_TICK(7);
 #endif
       exp_chunk(va, 0);
       exp_chunk(vb, 1);
@@ -501,9 +503,10 @@ __global__ void __maxnreg__(136)
     }
 #if PCR_ATTN_TIMING
     if ((threadIdx.x & 31) == 0 && (blockIdx.x == 0 || blockIdx.x == 300) && blockIdx.z == 0)
-      printf("TIMING blk %d warp %d iters %d: wait %lld ld %lld max %lld exp %lld st+arrive %lld loop %lld (clk/iter)\n",
+      printf("TIMING blk %d warp %d iters %d: wait %lld ld %lld max+kvwait %lld turn %lld exp %lld post %lld loop %lld\n",
              blockIdx.x, threadIdx.x >> 5, n_iter, tm_[0] / max(n_iter, 1), tm_[1] / max(n_iter, 1),
-             tm_[2] / max(n_iter, 1), tm_[3] / max(n_iter, 1), tm_[4] / max(n_iter, 1), tm_[5] / max(n_iter, 1));
+             (tm_[2] + tm_[6]) / max(n_iter, 1), tm_[7] / max(n_iter, 1),
+             tm_[3] / max(n_iter, 1), tm_[4] / max(n_iter, 1), tm_[5] / max(n_iter, 1));
 #endif
     // ---------------------------------------------------------------- epilogue
     const bool row_ok = i < p.n2;

@@ -1,0 +1,48 @@
+// Probe: MUFU.EX2 and FFMA2 throughput per SM on this B200 (warps per SMSP = blockDim/128).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/mufu_probe.cu -o tools/mufu_probe
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int OP>
+__global__ void k(float* out, int iters, long long* clk) {
+  float a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = -0.001f * (threadIdx.x + i);
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (OP == 0) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+      if (OP == 1) asm volatile("fma.rn.f32 %0, %0, 0f3F7FF000, 0fBA800000;" : "+f"(a[i]));
+    }
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 12345.f) out[0] = s;
+}
+
+template <int OP>
+void run(const char* name, int threads) {
+  float* o; long long* clk; cudaMalloc(&o, 4); cudaMalloc(&clk, 148 * 8);
+  const int iters = 4096;
+  k<OP><<<148, threads>>>(o, 16, clk);
+  cudaDeviceSynchronize();
+  k<OP><<<148, threads>>>(o, iters, clk);
+  cudaDeviceSynchronize();
+  long long c[148]; cudaMemcpy(c, clk, sizeof(c), cudaMemcpyDeviceToHost);
+  double ops = double(threads) * iters * 8;
+  printf("{\"op\": \"%s\", \"threads_per_sm\": %d, \"ops_per_clk_per_sm\": %.2f}\n", name, threads, ops / double(c[0]));
+  fflush(stdout);
+  cudaFree(o); cudaFree(clk);
+}
+
+int main() {
+  for (int t : {128, 256, 512}) run<0>("MUFU.EX2", t);
+  for (int t : {128, 256, 512}) run<1>("FFMA", t);
+  return 0;
+}
