@@ -77,6 +77,9 @@ CASES = [
     (2, 4, 2, 64, 64, 16, 256, 64),        # preset T geometry
     (1, 32, 8, 128, 256, 128, 0, 333),     # N1 = 0: plain causal self-attention
     (1, 32, 8, 128, 256, 64, 2048, 1),     # N2 = 1: decode-like row
+    (1, 8, 2, 64, 64, 16, 512, 700),       # d = 64, several M blocks, ragged
+    (1, 4, 2, 64, 64, 16, 4096, 32),       # d = 64 with KV splits (small grid, long prefix)
+    (1, 32, 8, 128, 512, 128, 1024, 100),  # 512-token chunks, 128-token pages
 ]
 
 
