@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define PCR_ABI_VERSION 3
+#define PCR_ABI_VERSION 4
 
 typedef struct pcr_ctx pcr_ctx;
 
@@ -90,7 +90,11 @@ typedef struct pcr_config {
                             baselines of the paper's copy path (fig:api), no SMs used:
                             1 = copy engine, one cudaMemcpyBatchAsync per layer over all page
                             segments; 2 = copy engine, one cudaMemcpyAsync per page segment;
-                            3 = experiment: TMA bulk copies host -> smem -> pool page */
+                            3 = experiment: TMA bulk copies host -> smem -> pool page;
+                            4 = hybrid: the copy engines move the first load_ce_fraction of the
+                            matched chunks (one cudaMemcpyBatchAsync on a library stream) while
+                            the gather kernel moves the rest, both over the same host link */
+  float load_ce_fraction;  /* load_mode 4 only: share of the chunks for the copy engines, [0, 1] */
   /* SSD tier (§8 f2): a file of ssd_chunks chunk records behind the DRAM store.
    * Committed chunks are written back asynchronously; chunks of requests in the
    * look-ahead window that are only on the SSD are prefetched into DRAM by an I/O thread

@@ -67,6 +67,9 @@ struct pcr_ctx {
   int64_t io_buf_elems = 0;
   cudaStream_t io_h2d = nullptr, io_d2h = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_outdone;   // per layer: inputs staged / output copied back
+  // load_mode 4: the copy-engine share of the gather runs on this stream, forked/joined per layer
+  cudaStream_t ce_stream = nullptr;
+  cudaEvent_t ev_ce_fork = nullptr, ev_ce_join = nullptr;
   cudaEvent_t ev_io_join = nullptr;
 };
 
@@ -168,18 +171,20 @@ pcr_status device_ready(pcr_ctx* c) {
 
 // Copy-engine baselines of a2 (the paper's path): the same page segments as the gather
 // kernel — for each matched chunk, kv head, K/V and page of the chunk, S_pg*d*2 contiguous bytes.
-pcr_status enqueue_ce_copy(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s) {
+pcr_status enqueue_ce_copy(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s, int32_t ch0, int32_t ch1,
+                           bool batch) {
   const pcr_config& k = c->cfg;
   const int64_t seg = int64_t(k.page_tokens) * k.head_dim * 2;
   const int32_t pages_per_chunk = k.chunk_tokens / k.page_tokens;
-  const int64_t n = int64_t(r->plan.n_matched) * c->hkv * 2 * pages_per_chunk;
+  const int64_t n = int64_t(ch1 - ch0) * c->hkv * 2 * pages_per_chunk;
+  if (n == 0) return PCR_OK;
   c->ce_dst.resize(n);
   c->ce_src.resize(n);
   c->ce_size.assign(n, static_cast<size_t>(seg));
   int64_t i = 0;
   uint8_t* pool = static_cast<uint8_t*>(k.pool);
   uint8_t* store = static_cast<uint8_t*>(c->store);
-  for (int32_t ch = 0; ch < r->plan.n_matched; ++ch)
+  for (int32_t ch = ch0; ch < ch1; ++ch)
     for (int32_t h = 0; h < c->hkv; ++h)
       for (int32_t kv = 0; kv < 2; ++kv)
         for (int32_t pp = 0; pp < pages_per_chunk; ++pp, ++i) {
@@ -188,7 +193,7 @@ pcr_status enqueue_ce_copy(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s
                          ((int64_t(layer) * c->hkv + h) * 2 + kv) * int64_t(k.chunk_tokens) * k.head_dim * 2 + pp * seg;
           c->ce_dst[i] = pool + (((int64_t(layer) * c->n_pool_pages + page) * c->hkv + h) * 2 + kv) * seg;
         }
-  if (k.load_mode == 1) {
+  if (batch) {
     cudaMemcpyAttributes attr{};
     attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
     attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
@@ -210,10 +215,35 @@ pcr_status enqueue_gather(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s)
     c->launches += 1;
     return PCR_OK;
   }
-  if (c->cfg.load_mode != 0) return enqueue_ce_copy(c, r, layer, s);
-  CUDA_TRY(c, pcr::launch_kv_gather(c->store_dev, c->cfg.pool, d_slots_of(c, r), d_pages_of(c, r),
-                                    r->plan.n_matched, layer, c->geom, c->gather_ctas, s));
-  c->launches += 1;
+  if (c->cfg.load_mode == 1 || c->cfg.load_mode == 2)
+    return enqueue_ce_copy(c, r, layer, s, 0, r->plan.n_matched, c->cfg.load_mode == 1);
+  int32_t n_ce = 0;
+  if (c->cfg.load_mode == 4) {
+    // hybrid: chunks [0, n_ce) by the copy engines on ce_stream, the rest by the gather kernel on s
+    n_ce = std::min(r->plan.n_matched, std::max(0, static_cast<int32_t>(std::lround(
+                                                       c->cfg.load_ce_fraction * r->plan.n_matched))));
+    if (n_ce > 0) {
+      if (!c->ce_stream) {
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->ce_stream, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_ce_fork, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_ce_join, cudaEventDisableTiming));
+      }
+      CUDA_TRY(c, cudaEventRecord(c->ev_ce_fork, s));
+      CUDA_TRY(c, cudaStreamWaitEvent(c->ce_stream, c->ev_ce_fork, 0));
+      pcr_status st = enqueue_ce_copy(c, r, layer, c->ce_stream, 0, n_ce, true);
+      if (st != PCR_OK) return st;
+    }
+  }
+  if (n_ce < r->plan.n_matched) {
+    const int32_t ppc = c->cfg.chunk_tokens / c->cfg.page_tokens;
+    CUDA_TRY(c, pcr::launch_kv_gather(c->store_dev, c->cfg.pool, d_slots_of(c, r) + n_ce, d_pages_of(c, r) + n_ce * ppc,
+                                      r->plan.n_matched - n_ce, layer, c->geom, c->gather_ctas, s));
+    c->launches += 1;
+  }
+  if (n_ce > 0) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_ce_join, c->ce_stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_ce_join, 0));
+  }
   return PCR_OK;
 }
 
@@ -458,7 +488,8 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
       k.head_dim < 8 || k.head_dim % 8 || k.world < 1 || k.rank < 0 || k.rank >= k.world ||
       k.n_kv_heads % k.world || k.chunk_tokens < 1 || k.page_tokens < 1 || k.chunk_tokens % k.page_tokens ||
       k.store_chunks < 1 || k.window < 0 || k.pool_bytes < 0 || k.max_inflight < 0 || k.max_tokens < 0 ||
-      k.gather_ctas < 0 || k.load_mode < 0 || k.load_mode > 3 || k.ssd_chunks < 0 ||
+      k.gather_ctas < 0 || k.load_mode < 0 || k.load_mode > 4 || k.ssd_chunks < 0 ||
+      !(k.load_ce_fraction >= 0.f && k.load_ce_fraction <= 1.f) ||
       (k.ssd_chunks > 0 && !k.ssd_path))
     return PCR_E_INVAL;
   auto c = std::make_unique<pcr_ctx>();
@@ -579,6 +610,9 @@ void pcr_destroy(pcr_ctx* c) {
     if (c->io_h2d) cudaStreamDestroy(c->io_h2d);
     if (c->io_d2h) cudaStreamDestroy(c->io_d2h);
     if (c->io_buf) cudaFree(c->io_buf);
+    if (c->ev_ce_fork) cudaEventDestroy(c->ev_ce_fork);
+    if (c->ev_ce_join) cudaEventDestroy(c->ev_ce_join);
+    if (c->ce_stream) cudaStreamDestroy(c->ce_stream);
     if (c->nccl_comm) {
       if (const pcr::NcclApi* api = pcr::nccl_api()) api->comm_destroy(c->nccl_comm);
     }

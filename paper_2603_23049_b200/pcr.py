@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libpcr.so")
 STATUS = {0: "OK", -1: "INVAL", -2: "NOMEM", -3: "CUDA", -4: "STATE", -5: "NOREQ", -6: "INTERNAL",
           -7: "UNSUPPORTED"}
 MODE_OVERLAP, MODE_SYNC = 0, 1
-LOAD_SM_GATHER, LOAD_CE_BATCH, LOAD_CE_BLOCKS = 0, 1, 2
+LOAD_SM_GATHER, LOAD_CE_BATCH, LOAD_CE_BLOCKS, LOAD_TMA, LOAD_HYBRID = 0, 1, 2, 3, 4
 
 
 class PcrError(RuntimeError):
@@ -36,7 +36,7 @@ class PcrConfig(ctypes.Structure):
                 ("store_chunks", ctypes.c_int64), ("window", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("pool", ctypes.c_void_p), ("pool_bytes", ctypes.c_int64), ("max_inflight", ctypes.c_int32),
                 ("max_tokens", ctypes.c_int32), ("gather_ctas", ctypes.c_int32), ("load_mode", ctypes.c_int32),
-                ("ssd_path", ctypes.c_char_p), ("ssd_chunks", ctypes.c_int64)]
+                ("load_ce_fraction", ctypes.c_float), ("ssd_path", ctypes.c_char_p), ("ssd_chunks", ctypes.c_int64)]
 
 
 class PcrPlan(ctypes.Structure):
@@ -148,7 +148,7 @@ class Context:
 
     def __init__(self, n_layers, n_q_heads, n_kv_heads, head_dim, chunk_tokens, page_tokens, store_chunks,
                  window, device=-1, pool=None, pool_bytes=None, rank=0, world=1, max_inflight=0, max_tokens=0,
-                 gather_ctas=0, load_mode=LOAD_SM_GATHER, ssd_path=None, ssd_chunks=0):
+                 gather_ctas=0, load_mode=LOAD_SM_GATHER, ssd_path=None, ssd_chunks=0, load_ce_fraction=0.0):
         self.lib = load_library()
         if pool_bytes is None:
             pool_bytes = pool.numel() * pool.element_size() if hasattr(pool, "numel") else 0
@@ -156,7 +156,7 @@ class Context:
         self._ssd_path = ssd_path.encode() if isinstance(ssd_path, str) else ssd_path
         cfg = PcrConfig(n_layers, n_q_heads, n_kv_heads, head_dim, rank, world, chunk_tokens, page_tokens,
                         store_chunks, window, device, _ptr(pool), int(pool_bytes), max_inflight, max_tokens,
-                        gather_ctas, load_mode, self._ssd_path, ssd_chunks)
+                        gather_ctas, load_mode, float(load_ce_fraction), self._ssd_path, ssd_chunks)
         h = ctypes.c_void_p()
         st = self.lib.pcr_create(ctypes.byref(cfg), ctypes.byref(h))
         if st != 0:

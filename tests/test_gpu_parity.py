@@ -310,13 +310,13 @@ def test_sharded_run_with_nccl_allgather_world1():
     assert np.array_equal(to_host(gathered)[:, 0], out)
 
 
-@pytest.mark.parametrize("load_mode", [1, 2, 3])
-def test_copy_engine_baselines_match_gather(load_mode):
-    """f4 baselines (the paper's cudaMemcpyBatchAsync / block-by-block path) produce the
-    same pool bits and outputs as the SM gather kernel."""
+@pytest.mark.parametrize("load_mode,frac", [(1, 0.0), (2, 0.0), (3, 0.0), (4, 0.34), (4, 1.0)])
+def test_copy_engine_baselines_match_gather(load_mode, frac):
+    """f4 baselines (the paper's cudaMemcpyBatchAsync / block-by-block path) and the hybrid
+    copy-engine + gather-kernel load produce the same pool bits and outputs as the SM gather kernel."""
     args = ("kout", 2, 32, 8, 128, 256, 16, 768, 90)
     rig0, plan0, q, k, v, out0 = _single_request(*args, seed=44)
-    rig1, plan1, _, _, _, out1 = _single_request(*args, seed=44, load_mode=load_mode)
+    rig1, plan1, _, _, _, out1 = _single_request(*args, seed=44, load_mode=load_mode, load_ce_fraction=frac)
     assert plan0["pages"] == plan1["pages"] and plan0["slots"] == plan1["slots"]
     assert np.array_equal(out0, out1)
     p0, p1 = rig0.pool_np(), rig1.pool_np()

@@ -28,7 +28,7 @@ def test_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(pcr.PROTOTYPES) == declared
-    assert lib.pcr_abi_version() == 3
+    assert lib.pcr_abi_version() == 4
 
 
 def test_blake2b_rfc7693_vectors():
