@@ -303,7 +303,8 @@ __global__ void __maxnreg__(136)
           for (int kk = 0; kk < kBlockN / 16 && (PCR_ATTN_PROFILE & 2) == 0; ++kk)
             mma_bf16_ts(tmem + Lay::kColO + t * D, tmem + (2 * t + (it & 1)) * kBlockN + kk * 8, vd + (kk * 2048 >> 4),
                         idesc_o, (it > 0 || kk > 0));
-          mma_commit(&bars->o_done[t]);
+          // O_t rescale fence for the last tile only (earlier rescales wait on s_full, below)
+          if (it == n_iter - 2) mma_commit(&bars->o_done[t]);
           if (t == kNQ - 1) mma_commit(&bars->v_empty[it % kStages]);
         }
         __syncwarp();
@@ -424,8 +425,13 @@ __global__ void __maxnreg__(136)
       // common case (it would queue behind the other warpgroup's exponentials)
       const float alpha = rescale ? ex2(fmaf(m_raw, p.scale_log2, neg_m)) : 1.f;
       if (it > 0 && __any_sync(0xffffffffu, rescale)) {
-        // O_t must hold PV_t(it-1) before it is rescaled
-        mbar_wait(&bars->o_done[t], (it - 1) & 1);
+        // O_t must hold PV_t(it-1) before it is rescaled.  S_t(it+1) is issued right after
+        // PV_t(it-1) and its commit covers every earlier MMA, so its s_full phase (which this
+        // warpgroup waits for next iteration anyway) certifies PV_t(it-1); the last tile has no
+        // S_t(it+1) and waits on o_done, committed once after PV_t(n_iter-2).  Every barrier
+        // phase thus has a waiter (compute-sanitizer synccheck clean).
+        if (it + 1 < n_iter) mbar_wait(&bars->s_full[t][(it + 1) & 1], ((it + 1) >> 1) & 1);
+        else mbar_wait(&bars->o_done[t], 0);
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
