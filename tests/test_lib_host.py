@@ -173,3 +173,48 @@ def test_invalid_configs():
         pcr.Context(2, 4, 2, 64, 64, 48, 4, 0, device=-1, pool_bytes=0)     # S does not divide C
     with pytest.raises(pcr.PcrError):
         pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, rank=1, world=4)  # world !| Hkv
+    with pytest.raises(pcr.PcrError):
+        pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=5)          # no such load path
+    with pytest.raises(pcr.PcrError):
+        pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=4, load_ce_fraction=1.5)
+    pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=4, load_ce_fraction=0.5).close()
+
+
+def test_pcr_run_opts_layout_matches_header():
+    """The binding's ctypes structs mirror include/pcr.h (ABI v4): field order and offsets that the
+    C side reads (host_io in pcr_run_opts, load_ce_fraction in pcr_config)."""
+    import ctypes
+    assert [f for f, _ in pcr.PcrRunOpts._fields_][-2:] == ["mode", "host_io"]
+    assert pcr.PcrConfig.load_ce_fraction.offset == pcr.PcrConfig.load_mode.offset + 4
+    assert pcr.PcrConfig.ssd_path.offset % ctypes.alignment(ctypes.c_void_p) == 0
+
+
+def test_binding_struct_offsets_match_header(tmp_path):
+    """Every field offset and struct size of the ctypes mirrors equals what a C compiler derives
+    from include/pcr.h (gcc on the host): the binding cannot drift from the header."""
+    import ctypes
+    import os
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc") or shutil.which("cc")
+    if gcc is None:
+        pytest.skip("no C compiler")
+    structs = {"pcr_config": pcr.PcrConfig, "pcr_plan": pcr.PcrPlan, "pcr_stats": pcr.PcrStats,
+               "pcr_run_opts": pcr.PcrRunOpts}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "pcr.h"', "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'  printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for f, _ in cls._fields_:
+            lines.append(f'  printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "offsets.c"
+    src.write_text("\n".join(lines))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "offsets"
+    subprocess.run([gcc, "-std=c99", "-I", os.path.join(root, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    for line in filter(None, out):
+        cname, field, val = line.split()
+        cls = structs[cname]
+        got = ctypes.sizeof(cls) if field == "sizeof" else getattr(cls, field).offset
+        assert got == int(val), (cname, field, got, val)
