@@ -65,7 +65,7 @@ def parse():
     ap.add_argument("--ssd-frac", type=float, default=0.0, help="Z: SSD tier size / distinct chunks (0 = none)")
     ap.add_argument("--ssd-path", default="/tmp/pcr_ssd_tier.bin", help="Z: SSD tier file")
     ap.add_argument("--ce-frac", type=float, default=0.5, help="--load-mode hybrid: copy-engine share of the chunks")
-    ap.add_argument("--load-mode", default="sm", choices=["sm", "ce_batch", "ce_blocks", "tma", "hybrid"],
+    ap.add_argument("--load-mode", default="auto", choices=["sm", "ce_batch", "ce_blocks", "tma", "hybrid", "auto"],
                     help="a2 implementation: sm_100a gather kernel, or the paper's copy-engine paths")
     return ap.parse_args()
 
@@ -324,7 +324,7 @@ def run_ours(args):
     page_elems = L * hkv * 2 * S * d
     pool = torch.empty(n_pool_pages * page_elems, dtype=torch.int16, device="cuda")
     store_chunks = n_doc // C + 4
-    load_mode = {"sm": 0, "ce_batch": 1, "ce_blocks": 2, "tma": 3, "hybrid": 4}[args.load_mode]
+    load_mode = {"sm": 0, "ce_batch": 1, "ce_blocks": 2, "tma": 3, "hybrid": 4, "auto": 5}[args.load_mode]
     ctx = Context(L, Hq, Hkv, d, C, S, store_chunks, 4, device=local, pool=pool, rank=rank, world=world,
                   gather_ctas=args.gather_ctas, load_mode=load_mode, load_ce_fraction=args.ce_frac)
 
@@ -449,6 +449,7 @@ def run_ours(args):
     clocks = ClockSampler(local, pci_bus_id(torch, local))
     clocks.start()
     launches0 = ctx.kernel_launches
+    stats0 = ctx.stats
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     clocks.begin()
@@ -469,6 +470,9 @@ def run_ours(args):
     torch.cuda.synchronize()
     total_ms = ev0.elapsed_time(ev1)
     launches = ctx.kernel_launches - launches0
+    stats1 = ctx.stats
+    ce_layers = stats1["ce_layer_loads"] - stats0["ce_layer_loads"]
+    ce_copies_per_layer = (stats1["ce_copies"] - stats0["ce_copies"]) / max(1, ce_layers)
     clk = clocks.stop()
     if world > 1:
         tt = torch.tensor([total_ms], device="cuda")
@@ -491,6 +495,28 @@ def run_ours(args):
         attn_ms_iso = float(lt_iso[:, :, 1].mean()) if lt_iso is not None else float("nan")
     else:   # per-layer events are not recorded on the layer-body path
         attn_ms = gather_ms_evented = attn_ms_iso = float("nan")
+
+    # When the copy engines carried the timed loads (auto on long runs), time the SM gather
+    # kernel on the same steps too (same events, load stream busy time per layer).
+    sm_leg = None
+    if ce_layers and N1 and body is None:
+        ctx.set_load_mode(0)
+        for _ in range(2):
+            step(q_d, k_d, v_d, out_d)
+        sm_ms, sm_ld = [], []
+        for _ in range(max(5, min(args.steps, 15))):
+            e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            l_a, l_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e_a.record(cs)
+            ls.wait_event(e_a)
+            step(q_d, k_d, v_d, out_d, load_events=(l_a, l_b))
+            e_b.record(cs)
+            e_b.synchronize()
+            sm_ms.append(e_a.elapsed_time(e_b))
+            sm_ld.append(l_a.elapsed_time(l_b))
+        ctx.set_load_mode(load_mode, args.ce_frac)
+        sm_leg = {"ttft_ms": statistics.median(sm_ms), "avg_launch_ms": float(np.mean(sm_ld)) / L,
+                  "steps": len(sm_ms)}
 
     # e2e: the same step through the C-ABI with HOST buffers: q/k/v/out are page-locked host
     # tensors handed to pcr_run_prefill_ex(host_io=1); the library stages each layer's inputs
@@ -577,10 +603,17 @@ def run_ours(args):
         ncu_t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
     except Exception:
         ncu_t = {}
-    rl_gather = {"bound": "host-link", "kernel": {0: "kv_gather", 4: f"kv_gather + copy engines ({args.ce_frac:.2f} of the chunks)"}.get(
-                     load_mode, f"copy engine ({args.load_mode})"), "achieved": gather_gbs, "peak": peak_h2d,
+    if ce_layers:
+        load_kernel = (f"kv_load on the copy engines: one cudaMemcpyBatchAsync per layer, "
+                       f"{ce_copies_per_layer:.0f} runs of {load_bytes / ce_copies_per_layer / 2**10:.0f} KiB "
+                       f"(load_mode {args.load_mode})")
+    else:
+        load_kernel = {4: f"kv_gather + copy engines ({args.ce_frac:.2f} of the chunks)", 3: "kv_gather_tma"}.get(
+            load_mode, "kv_gather")
+    rl_gather = {"bound": "host-link", "kernel": load_kernel, "achieved": gather_gbs, "peak": peak_h2d,
                  "unit": "GB/s", "frac": gather_gbs / peak_h2d,
-                 "traffic": ncu_t.get("gather", {}).get("pcie_read_bytes") if args.workload == "L8" else None,
+                 "traffic": ncu_t.get("gather", {}).get("pcie_read_bytes") if args.workload == "L8" and not ce_layers
+                 else None,
                  "traffic_note": "PCIe read bytes per launch (ncu pcie__read_bytes x duration, L8 capture in "
                                  "profiles/ncu_traffic.json); DRAM bytes per launch ~7.7 KB: pool writes stay in L2",
                  "peak_source": f"live: cudaMemcpyAsync H2D, 256 MiB, best of 10 from torch-pinned and from "
@@ -588,6 +621,15 @@ def run_ours(args):
                                 f"measurement before the warm-up ({peak_h2d_before:.1f}) and after the timed region "
                                 f"({peak_h2d_after:.1f})",
                  "algorithmic_bytes_per_launch": load_bytes, "avg_launch_ms": gather_ms}
+    rl_sm = None
+    if sm_leg is not None:
+        sm_gbs = load_bytes / (sm_leg["avg_launch_ms"] * 1e-3) / 1e9
+        rl_sm = {"bound": "host-link", "kernel": "kv_gather (sm_100a 16-byte gather kernel, load_mode sm)",
+                 "achieved": sm_gbs, "peak": peak_h2d, "unit": "GB/s", "frac": sm_gbs / peak_h2d,
+                 "traffic": ncu_t.get("gather", {}).get("pcie_read_bytes") if args.workload == "L8" else None,
+                 "algorithmic_bytes_per_launch": load_bytes, "avg_launch_ms": sm_leg["avg_launch_ms"],
+                 "ttft_ms": sm_leg["ttft_ms"], "steps": sm_leg["steps"],
+                 "note": "the same steps re-timed with the SM gather kernel after the timed region"}
     rl_attn = None if attn_tflops is None else {
         "bound": "tensor", "kernel": "kv_append+suffix_attn", "achieved": attn_tflops, "peak": bf16_peak,
         "unit": "TFLOP/s", "frac": attn_tflops / bf16_peak,
@@ -618,6 +660,9 @@ def run_ours(args):
         "gpu_launches": launches,
         "roofline": rl_gather if dominant == "kv_gather" else rl_attn,
         "roofline_attn": rl_attn,
+        "roofline_gather_sm": rl_sm,
+        "load_path": {"ce_layer_loads": ce_layers, "sm_layer_loads": stats1["sm_layer_loads"] - stats0["sm_layer_loads"],
+                      "ce_copies_per_layer": ce_copies_per_layer if ce_layers else 0},
         "clocks": clk,
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -659,7 +704,9 @@ def run_trace_z(args):
                      f"fit in 80% of the {free / 1e9:.0f} GB free under {args.ssd_path}; lower --ssd-frac or --requests")
     ctx = Context(L, Hq, Hkv, d, C, S, cap, args.window, device=0, pool=pool, max_tokens=max_n,
                   gather_ctas=args.gather_ctas, ssd_path=args.ssd_path if ssd_chunks else None,
-                  ssd_chunks=ssd_chunks)
+                  ssd_chunks=ssd_chunks,
+                  load_mode={"sm": 0, "ce_batch": 1, "ce_blocks": 2, "tma": 3, "hybrid": 4, "auto": 5}[args.load_mode],
+                  load_ce_fraction=args.ce_frac)
     t_pin = time.perf_counter() - t0
     rng = make_rng(11)
     max_n2 = max_n

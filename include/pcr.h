@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define PCR_ABI_VERSION 4
+#define PCR_ABI_VERSION 5
 
 typedef struct pcr_ctx pcr_ctx;
 
@@ -93,7 +93,12 @@ typedef struct pcr_config {
                             3 = experiment: TMA bulk copies host -> smem -> pool page;
                             4 = hybrid: the copy engines move the first load_ce_fraction of the
                             matched chunks (one cudaMemcpyBatchAsync on a library stream) while
-                            the gather kernel moves the rest, both over the same host link */
+                            the gather kernel moves the rest, both over the same host link;
+                            5 = auto: per request, mode 1 when the chunk-layer copies merge into
+                            runs of >= 256 KiB on average (consecutive pool pages of a chunk are
+                            one run), else mode 0 — the copy engines reach ~98% of the host
+                            link on long runs, the SM gather ~90% at any run length
+                            (profiles/r01_ce_probe.txt) */
   float load_ce_fraction;  /* load_mode 4 only: share of the chunks for the copy engines, [0, 1] */
   /* SSD tier (§8 f2): a file of ssd_chunks chunk records behind the DRAM store.
    * Committed chunks are written back asynchronously; chunks of requests in the
@@ -179,7 +184,9 @@ pcr_status pcr_match_prefix(pcr_ctx* ctx, int64_t req_id, const int64_t* pending
 pcr_status pcr_release(pcr_ctx* ctx, int64_t req_id, int32_t commit);
 
 /* Copy one chunk record ([L][Hkv_loc][2][C][d] bf16, pcr_slot_bytes bytes) into / out of
- * the pinned DRAM store.  Host memcpy; PCR_E_INVAL on a bad slot or null pointer. */
+ * the pinned DRAM store.  Host memcpy; PCR_E_INVAL on a bad slot or null pointer.  The store
+ * keeps slots page-major internally ([L][C/S_pg][Hkv_loc][2][S_pg][d]: the images of the pool
+ * pages the chunk fills) and converts here, so the record layout callers see is unchanged. */
 pcr_status pcr_store_write(pcr_ctx* ctx, int32_t slot, const void* src);
 pcr_status pcr_store_read(const pcr_ctx* ctx, int32_t slot, void* dst);
 
@@ -191,6 +198,9 @@ typedef struct pcr_stats {
   int64_t ssd_evictions;    /* SSD records overwritten (LRU) */
   int64_t dram_evictions;   /* DRAM leaves evicted */
   int64_t ssd_bytes_read, ssd_bytes_written;
+  int64_t ce_copies;        /* copy-engine copies enqueued for a2 loads (load_mode 1/2/4/5) */
+  int64_t ce_layer_loads;   /* layer loads done by the copy engines (load_mode 1/2/5) */
+  int64_t sm_layer_loads;   /* layer loads done by the SM gather kernel (load_mode 0/3/4/5) */
 } pcr_stats;
 pcr_status pcr_get_stats(const pcr_ctx* ctx, pcr_stats* out);
 
@@ -290,6 +300,11 @@ pcr_status pcr_run_prefill_ex(pcr_ctx* ctx, int64_t req_id, const void* q_all, c
 
 /* Count of kernels launched by this ctx since creation (bench `gpu_launches`). */
 int64_t pcr_kernel_launches(const pcr_ctx* ctx);
+
+/* Switch the a2 load path (pcr_config.load_mode / load_ce_fraction, same ranges) for layer loads
+ * enqueued after this call; call it between requests (a load_mode 5 request keeps the choice it
+ * made at its first load).  PCR_E_INVAL on an out-of-range value (nothing changes). */
+pcr_status pcr_set_load_mode(pcr_ctx* ctx, int32_t load_mode, float load_ce_fraction);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,11 @@ struct KvGeom {
   int64_t slot_elems;               // elements of one store slot = L*Hkv*2*C*d
 };
 
-// a2: pool[layer][pages[t/S]][h][kv][t%S] = store[slots[t/C]][layer][h][kv][t%C], t < n_matched*C.
+// Store slots are page-major: slot[layer][t/S % (C/S)][h][kv][t%S][d] (= the images of the pool
+// pages the chunk fills), so a chunk-layer with consecutive pool pages is one contiguous run.
+// pcr_store_write/read convert from/to the API layout [L][Hkv][2][C][d].
+
+// a2: pool[layer][pages[t/S]][h][kv][t%S] = store[slots[t/C]][layer][(t%C)/S][h][kv][t%S], t < n_matched*C.
 // `store` is the device (UVA) view of the mapped pinned host store; 16-byte loads/stores.
 cudaError_t launch_kv_gather(const void* store, void* pool, const int32_t* d_slots, const int32_t* d_pages,
                              int32_t n_matched, int32_t layer, const KvGeom& g, int32_t target_ctas,
@@ -23,7 +27,7 @@ cudaError_t launch_kv_gather(const void* store, void* pool, const int32_t* d_slo
 cudaError_t launch_kv_gather_tma(const void* store, void* pool, const int32_t* d_slots, const int32_t* d_pages,
                                  int32_t n_matched, int32_t layer, const KvGeom& g, int32_t ctas, cudaStream_t stream);
 
-// f1: store[slots[c]][layer][h][kv][t%C] = pool[layer][pages[t/S]][h][kv][t%S] for the chain
+// f1: store[slots[c]][layer][(t%C)/S][h][kv][t%S] = pool[layer][pages[t/S]][h][kv][t%S] for the chain
 // chunks c in [chunk0, chunk0+n_chunks) (the request's reserved chunks), into the mapped store.
 cudaError_t launch_kv_scatter(const void* pool, void* store, const int32_t* d_slots, const int32_t* d_pages,
                               int32_t chunk0, int32_t n_chunks, int32_t layer, const KvGeom& g, int32_t target_ctas,

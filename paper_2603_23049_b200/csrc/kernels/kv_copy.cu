@@ -28,21 +28,26 @@ __device__ __forceinline__ uint4 ld_host_stream(const uint4* p) {
   return v;
 }
 
-// The copy is a list of page segments: for chunk c (chain index), kv head h, K/V and page pp of
-// the chunk, S*d*2 contiguous bytes in the store slot map to S*d*2 contiguous bytes of one pool
-// page.  Each warp copies whole segments (address math once per segment, not per 16 bytes), every
-// lane keeping kUnroll independent 16-byte loads in flight.  grid-stride over segments.
+// The copy is a list of page segments.  A store slot is laid out page-major, as the pool pages it
+// fills: [L][C/S][Hkv][2][S][d], so for chunk c (chain index) and page pp of the chunk, layer l
+// of the slot holds one Hkv*2*S*d*2-byte image of pool page pages[c*C/S + pp].  A segment is one
+// (chunk, page of the chunk, kv head, K|V): S*d*2 contiguous bytes on both sides.  Consecutive
+// segments are consecutive in the store.  Each warp copies whole segments (address math once per
+// segment, not per 16 bytes), every lane keeping kUnroll independent 16-byte loads in flight;
+// grid-stride over segments.
 __device__ __forceinline__ void segment_addrs(int64_t seg, int32_t chunk0, int32_t layer, const KvGeom& g,
                                               int32_t ppc_log2, int32_t row16_log2, const int32_t* slots,
                                               const int32_t* pages, int64_t& store16, int64_t& pool16) {
-  const int32_t pp = int32_t(seg & ((1 << ppc_log2) - 1));
-  const int64_t hk = (seg >> ppc_log2) % (int64_t(g.Hkv) * 2);           // h*2 + kv
-  const int32_t c = chunk0 + int32_t((seg >> ppc_log2) / (int64_t(g.Hkv) * 2));
+  const int64_t hk2 = int64_t(g.Hkv) * 2;
+  const int64_t hk = seg % hk2;                                           // h*2 + kv
+  const int64_t cp = seg / hk2;                                           // chunk-local page index
+  const int32_t pp = int32_t(cp & ((1 << ppc_log2) - 1));
+  const int32_t c = chunk0 + int32_t(cp >> ppc_log2);
   const int64_t seg16 = int64_t(g.S) << row16_log2;                       // 16-byte units per segment
-  store16 = (int64_t(slots[c]) * g.slot_elems + int64_t(layer) * g.Hkv * 2 * g.C * g.d) / 8 +
-            (hk * g.C << row16_log2) + pp * seg16;
+  const int64_t page16 = hk2 * seg16;                                     // one page image
+  store16 = int64_t(slots[c]) * (g.slot_elems / 8) + ((int64_t(layer) << ppc_log2) + pp) * page16 + hk * seg16;
   const int64_t page = pages[(int64_t(c) << ppc_log2) + pp];
-  pool16 = ((int64_t(layer) * g.n_pool_pages + page) * g.Hkv * 2 + hk) * seg16;
+  pool16 = (int64_t(layer) * g.n_pool_pages + page) * page16 + hk * seg16;
 }
 
 __global__ void __launch_bounds__(kThreads, 6) kv_gather_kernel(const uint4* __restrict__ store,
@@ -163,14 +168,14 @@ __global__ void __launch_bounds__(32) kv_gather_tma_kernel(const uint8_t* __rest
     const uint32_t sbar = static_cast<uint32_t>(__cvta_generic_to_shared(&full[st]));
     if (it >= kTmaStages)  // the store that last read this buffer must have finished reading it
       asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTmaStages - 1) : "memory");
-    // segment i -> (chunk, h, kv, page-in-chunk)
-    const int32_t pp = int32_t(i % ppc);
-    const int64_t hk = (i / ppc) % (g.Hkv * 2);
+    // segment i -> (chunk, page-in-chunk, h, kv), page-major slot layout (see segment_addrs)
+    const int64_t hk = i % (g.Hkv * 2);
+    const int32_t pp = int32_t((i / (g.Hkv * 2)) % ppc);
     const int32_t c = int32_t(i / (ppc * g.Hkv * 2));
-    const uint8_t* src = store + (int64_t(slots[c]) * g.slot_elems + int64_t(layer) * g.Hkv * 2 * g.C * g.d) * 2 +
-                         hk * int64_t(g.C) * g.d * 2 + pp * seg;
+    const int64_t page_bytes = int64_t(g.Hkv) * 2 * seg;
+    const uint8_t* src = store + int64_t(slots[c]) * g.slot_elems * 2 + (int64_t(layer) * ppc + pp) * page_bytes + hk * seg;
     const int64_t page = pages[c * ppc + pp];
-    uint8_t* dst = pool + ((int64_t(layer) * g.n_pool_pages + page) * g.Hkv * 2 + hk) * seg;
+    uint8_t* dst = pool + (int64_t(layer) * g.n_pool_pages + page) * page_bytes + hk * seg;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(uint32_t(seg)) : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sbuf),
                  "l"(src), "r"(uint32_t(seg)), "r"(sbar)

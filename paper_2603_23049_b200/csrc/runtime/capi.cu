@@ -47,6 +47,7 @@ struct pcr_ctx {
   std::vector<cudaEvent_t> ev_t;  // timing: 4 per layer
   std::string err;
   int64_t launches = 0;
+  int64_t ce_copies = 0, ce_layer_loads = 0, sm_layer_loads = 0;   // a2 load-path counters (pcr_stats)
   pcr::KvGeom geom{};
   int32_t gather_ctas = 16;
   // split-KV workspace: ws_floats partial-O floats followed by ws_floats/d LSE floats
@@ -169,30 +170,40 @@ pcr_status device_ready(pcr_ctx* c) {
   return PCR_OK;
 }
 
-// Copy-engine baselines of a2 (the paper's path): the same page segments as the gather
-// kernel — for each matched chunk, kv head, K/V and page of the chunk, S_pg*d*2 contiguous bytes.
-pcr_status enqueue_ce_copy(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s, int32_t ch0, int32_t ch1,
-                           bool batch) {
+// Copy-engine path of a2 (the paper's API).  Each matched chunk's layer-l image is C/S
+// pool-page images in the page-major store slot; a page image maps to one pool page.  Adjacent
+// images whose pool pages are also adjacent are merged into one run, so a chunk whose pages are
+// consecutive is one Hkv*2*C*d*2-byte copy (1 MiB for L8).  batch: one cudaMemcpyBatchAsync over
+// the runs; otherwise one cudaMemcpyAsync per page image (the paper's block-by-block baseline).
+int64_t build_ce_runs(pcr_ctx* c, const Request* r, int32_t layer, int32_t ch0, int32_t ch1, bool merge) {
   const pcr_config& k = c->cfg;
-  const int64_t seg = int64_t(k.page_tokens) * k.head_dim * 2;
-  const int32_t pages_per_chunk = k.chunk_tokens / k.page_tokens;
-  const int64_t n = int64_t(ch1 - ch0) * c->hkv * 2 * pages_per_chunk;
-  if (n == 0) return PCR_OK;
-  c->ce_dst.resize(n);
-  c->ce_src.resize(n);
-  c->ce_size.assign(n, static_cast<size_t>(seg));
-  int64_t i = 0;
+  const int32_t ppc = k.chunk_tokens / k.page_tokens;
+  const size_t page_img = static_cast<size_t>(c->hkv) * 2 * k.page_tokens * k.head_dim * 2;
+  c->ce_dst.clear();
+  c->ce_src.clear();
+  c->ce_size.clear();
   uint8_t* pool = static_cast<uint8_t*>(k.pool);
   uint8_t* store = static_cast<uint8_t*>(c->store);
   for (int32_t ch = ch0; ch < ch1; ++ch)
-    for (int32_t h = 0; h < c->hkv; ++h)
-      for (int32_t kv = 0; kv < 2; ++kv)
-        for (int32_t pp = 0; pp < pages_per_chunk; ++pp, ++i) {
-          const int64_t page = r->plan.pages[ch * pages_per_chunk + pp];
-          c->ce_src[i] = store + r->plan.slots[ch] * c->slot_bytes +
-                         ((int64_t(layer) * c->hkv + h) * 2 + kv) * int64_t(k.chunk_tokens) * k.head_dim * 2 + pp * seg;
-          c->ce_dst[i] = pool + (((int64_t(layer) * c->n_pool_pages + page) * c->hkv + h) * 2 + kv) * seg;
-        }
+    for (int32_t pp = 0; pp < ppc; ++pp) {
+      uint8_t* src = store + r->plan.slots[ch] * c->slot_bytes + (int64_t(layer) * ppc + pp) * page_img;
+      uint8_t* dst = pool + (int64_t(layer) * c->n_pool_pages + r->plan.pages[ch * ppc + pp]) * page_img;
+      if (merge && !c->ce_src.empty() && static_cast<uint8_t*>(c->ce_src.back()) + c->ce_size.back() == src &&
+          static_cast<uint8_t*>(c->ce_dst.back()) + c->ce_size.back() == dst) {
+        c->ce_size.back() += page_img;
+      } else {
+        c->ce_src.push_back(src);
+        c->ce_dst.push_back(dst);
+        c->ce_size.push_back(page_img);
+      }
+    }
+  return static_cast<int64_t>(c->ce_src.size());
+}
+
+pcr_status enqueue_ce_copy(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s, int32_t ch0, int32_t ch1,
+                           bool batch) {
+  const int64_t n = build_ce_runs(c, r, layer, ch0, ch1, batch);
+  if (n == 0) return PCR_OK;
   if (batch) {
     cudaMemcpyAttributes attr{};
     attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
@@ -202,9 +213,29 @@ pcr_status enqueue_ce_copy(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s
                                      &fail_idx, s));
   } else {
     for (int64_t j = 0; j < n; ++j)
-      CUDA_TRY(c, cudaMemcpyAsync(c->ce_dst[j], c->ce_src[j], seg, cudaMemcpyHostToDevice, s));
+      CUDA_TRY(c, cudaMemcpyAsync(c->ce_dst[j], c->ce_src[j], c->ce_size[j], cudaMemcpyHostToDevice, s));
   }
+  c->ce_copies += n;
   return PCR_OK;
+}
+
+// load_mode 5 (auto): the copy engines when the request's runs average >= kCeMinRun bytes, else
+// the SM gather.  tools/ce_probe.cu on this pool's B200 (profiles/r01_ce_probe.txt), one 16 MiB
+// layer in runs of 16 KiB / 64 KiB / 256 KiB / 1 MiB: copy engine 25.9 / 43.4 / 51.5 / 53.9 GB/s
+// (54.7 GB/s over 32 back-to-back layers of 256 KiB runs) against 50.1 GB/s for the SM gather at
+// any run size: PCIe reads issued by SMs complete in 128-byte payloads, the copy engines' in
+// larger ones, so only the copy engines reach the link's ~55.6 GB/s, and only for long runs.
+constexpr int64_t kCeMinRun = 256 << 10;
+
+bool use_copy_engines(pcr_ctx* c, const Request* r) {
+  if (c->cfg.load_mode == 1 || c->cfg.load_mode == 2) return true;
+  if (c->cfg.load_mode != 5) return false;
+  if (r->load_auto < 0) {
+    const int64_t n = build_ce_runs(c, r, 0, 0, r->plan.n_matched, true);
+    const int64_t bytes = int64_t(r->plan.n_matched) * c->slot_bytes / c->cfg.n_layers;
+    const_cast<Request*>(r)->load_auto = (n > 0 && bytes / n >= kCeMinRun) ? 1 : 0;
+  }
+  return r->load_auto == 1;
 }
 
 pcr_status enqueue_gather(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s) {
@@ -213,10 +244,14 @@ pcr_status enqueue_gather(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s)
     CUDA_TRY(c, pcr::launch_kv_gather_tma(c->store_dev, c->cfg.pool, d_slots_of(c, r), d_pages_of(c, r),
                                           r->plan.n_matched, layer, c->geom, 4 * c->gather_ctas, s));
     c->launches += 1;
+    c->sm_layer_loads += 1;
     return PCR_OK;
   }
-  if (c->cfg.load_mode == 1 || c->cfg.load_mode == 2)
-    return enqueue_ce_copy(c, r, layer, s, 0, r->plan.n_matched, c->cfg.load_mode == 1);
+  if (use_copy_engines(c, r)) {
+    c->ce_layer_loads += 1;
+    return enqueue_ce_copy(c, r, layer, s, 0, r->plan.n_matched, c->cfg.load_mode != 2);
+  }
+  c->sm_layer_loads += 1;
   int32_t n_ce = 0;
   if (c->cfg.load_mode == 4) {
     // hybrid: chunks [0, n_ce) by the copy engines on ce_stream, the rest by the gather kernel on s
@@ -480,6 +515,15 @@ int64_t pcr_pool_pages(const pcr_ctx* ctx) { return ctx ? ctx->n_pool_pages : -1
 int64_t pcr_slot_bytes(const pcr_ctx* ctx) { return ctx ? ctx->slot_bytes : -1; }
 int64_t pcr_kernel_launches(const pcr_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
+pcr_status pcr_set_load_mode(pcr_ctx* c, int32_t load_mode, float load_ce_fraction) {
+  if (!c) return PCR_E_INVAL;
+  if (load_mode < 0 || load_mode > 5 || !(load_ce_fraction >= 0.f && load_ce_fraction <= 1.f))
+    return fail(c, PCR_E_INVAL, "pcr_set_load_mode: load_mode in [0, 5], load_ce_fraction in [0, 1]");
+  c->cfg.load_mode = load_mode;
+  c->cfg.load_ce_fraction = load_ce_fraction;
+  return PCR_OK;
+}
+
 pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
   if (!cfg || !out) return PCR_E_INVAL;
   *out = nullptr;
@@ -488,7 +532,7 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
       k.head_dim < 8 || k.head_dim % 8 || k.world < 1 || k.rank < 0 || k.rank >= k.world ||
       k.n_kv_heads % k.world || k.chunk_tokens < 1 || k.page_tokens < 1 || k.chunk_tokens % k.page_tokens ||
       k.store_chunks < 1 || k.window < 0 || k.pool_bytes < 0 || k.max_inflight < 0 || k.max_tokens < 0 ||
-      k.gather_ctas < 0 || k.load_mode < 0 || k.load_mode > 4 || k.ssd_chunks < 0 ||
+      k.gather_ctas < 0 || k.load_mode < 0 || k.load_mode > 5 || k.ssd_chunks < 0 ||
       !(k.load_ce_fraction >= 0.f && k.load_ce_fraction <= 1.f) ||
       (k.ssd_chunks > 0 && !k.ssd_path))
     return PCR_E_INVAL;
@@ -714,20 +758,41 @@ pcr_status pcr_get_stats(const pcr_ctx* c, pcr_stats* out) {
   out->dram_evictions = t.dram_evict;
   out->ssd_bytes_read = c->ssd ? c->ssd->bytes_read() : 0;
   out->ssd_bytes_written = c->ssd ? c->ssd->bytes_written() : 0;
+  out->ce_copies = c->ce_copies;
+  out->ce_layer_loads = c->ce_layer_loads;
+  out->sm_layer_loads = c->sm_layer_loads;
   return PCR_OK;
+}
+
+// API slot layout [L][Hkv][2][C][d] <-> the store's page-major layout [L][C/S][Hkv][2][S][d].
+void slot_permute(const pcr_ctx* c, uint8_t* dst, const uint8_t* src, bool to_store) {
+  const pcr_config& k = c->cfg;
+  const int32_t ppc = k.chunk_tokens / k.page_tokens;
+  const size_t seg = static_cast<size_t>(k.page_tokens) * k.head_dim * 2;
+  for (int32_t l = 0; l < k.n_layers; ++l)
+    for (int32_t h = 0; h < c->hkv; ++h)
+      for (int32_t kv = 0; kv < 2; ++kv)
+        for (int32_t pp = 0; pp < ppc; ++pp) {
+          const size_t api = ((static_cast<size_t>(l) * c->hkv + h) * 2 + kv) * ppc + pp;
+          const size_t sto = ((static_cast<size_t>(l) * ppc + pp) * c->hkv + h) * 2 + kv;
+          if (to_store) std::memcpy(dst + sto * seg, src + api * seg, seg);
+          else std::memcpy(dst + api * seg, src + sto * seg, seg);
+        }
 }
 
 pcr_status pcr_store_write(pcr_ctx* c, int32_t slot, const void* src) {
   if (!c || !src) return c ? fail(c, PCR_E_INVAL, "pcr_store_write: null source") : PCR_E_INVAL;
   if (slot < 0 || slot >= c->cfg.store_chunks) return fail(c, PCR_E_INVAL, "pcr_store_write: slot out of range");
-  std::memcpy(static_cast<uint8_t*>(c->store) + static_cast<size_t>(slot) * c->slot_bytes, src, c->slot_bytes);
+  slot_permute(c, static_cast<uint8_t*>(c->store) + static_cast<size_t>(slot) * c->slot_bytes,
+               static_cast<const uint8_t*>(src), true);
   return PCR_OK;
 }
 
 pcr_status pcr_store_read(const pcr_ctx* c, int32_t slot, void* dst) {
   if (!c || !dst) return c ? fail(c, PCR_E_INVAL, "pcr_store_read: null destination") : PCR_E_INVAL;
   if (slot < 0 || slot >= c->cfg.store_chunks) return fail(c, PCR_E_INVAL, "pcr_store_read: slot out of range");
-  std::memcpy(dst, static_cast<const uint8_t*>(c->store) + static_cast<size_t>(slot) * c->slot_bytes, c->slot_bytes);
+  slot_permute(c, static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(c->store) + static_cast<size_t>(slot) * c->slot_bytes,
+               false);
   return PCR_OK;
 }
 

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libpcr.so")
 STATUS = {0: "OK", -1: "INVAL", -2: "NOMEM", -3: "CUDA", -4: "STATE", -5: "NOREQ", -6: "INTERNAL",
           -7: "UNSUPPORTED"}
 MODE_OVERLAP, MODE_SYNC = 0, 1
-LOAD_SM_GATHER, LOAD_CE_BATCH, LOAD_CE_BLOCKS, LOAD_TMA, LOAD_HYBRID = 0, 1, 2, 3, 4
+LOAD_SM_GATHER, LOAD_CE_BATCH, LOAD_CE_BLOCKS, LOAD_TMA, LOAD_HYBRID, LOAD_AUTO = 0, 1, 2, 3, 4, 5
 
 
 class PcrError(RuntimeError):
@@ -52,7 +52,8 @@ class PcrStats(ctypes.Structure):
     _fields_ = [("prefetch_loads", ctypes.c_int64), ("ondemand_loads", ctypes.c_int64),
                 ("writebacks", ctypes.c_int64), ("ssd_evictions", ctypes.c_int64),
                 ("dram_evictions", ctypes.c_int64), ("ssd_bytes_read", ctypes.c_int64),
-                ("ssd_bytes_written", ctypes.c_int64)]
+                ("ssd_bytes_written", ctypes.c_int64), ("ce_copies", ctypes.c_int64),
+                ("ce_layer_loads", ctypes.c_int64), ("sm_layer_loads", ctypes.c_int64)]
 
 
 class PcrRunOpts(ctypes.Structure):
@@ -82,6 +83,7 @@ PROTOTYPES = {
     "pcr_prefill_attn_layer": (_I32, [_VP, _I64, _I32, _VP, _VP, _VP, _VP, _VP]),
     "pcr_run_prefill": (_I32, [_VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _I32, _P(ctypes.c_float)]),
     "pcr_kernel_launches": (_I64, [_VP]),
+    "pcr_set_load_mode": (_I32, [_VP, _I32, ctypes.c_float]),
     "pcr_comm_unique_id": (_I32, [_P(ctypes.c_uint8)]),
     "pcr_comm_init": (_I32, [_VP, _P(ctypes.c_uint8)]),
     "pcr_run_prefill_sharded": (_I32, [_VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32,
@@ -194,6 +196,9 @@ class Context:
         st = PcrStats()
         self._check(self.lib.pcr_get_stats(self.h, ctypes.byref(st)), "pcr_get_stats")
         return {f: getattr(st, f) for f, _ in PcrStats._fields_}
+
+    def set_load_mode(self, load_mode, load_ce_fraction=0.0):
+        self._check(self.lib.pcr_set_load_mode(self.h, int(load_mode), float(load_ce_fraction)), "pcr_set_load_mode")
 
     @property
     def kernel_launches(self):

@@ -36,7 +36,7 @@ def _warm_prefix(rig, req_id, doc_tokens, k_ctx, v_ctx, n_chunks):
 
 
 def _single_request(kind, L, Hq, Hkv, d, C, S, N1, N2, seed, mode=0, world=1, rank=0, local_only=False,
-                    **ctx_kw):
+                    fragment=False, **ctx_kw):
     """Warm N1 tokens, then run one request [doc | query] and return everything to compare.
     local_only: draw only this rank's heads (full-size sharded shapes) instead of slicing them out
     of all heads."""
@@ -60,6 +60,13 @@ def _single_request(kind, L, Hq, Hkv, d, C, S, N1, N2, seed, mode=0, world=1, ra
     doc = rng.integers(0, 1000, N1, dtype=np.uint32)
     if N1:
         _warm_prefix(rig, 1000, doc, k[:, :N1], v[:, :N1], N1 // C)
+    if fragment:
+        # two one-page requests hold pool pages 0 and 1; releasing the first leaves a hole, so
+        # the request's pages are [0, 2, 3, ...]: its first chunk's pages are not consecutive
+        for hid in (2000, 2001):
+            rig.ctx.submit(hid, rng.integers(5000, 6000, S, dtype=np.uint32), n_cacheable=0)
+            assert rig.ctx.match_prefix(hid, [])["pages"] == [hid - 2000]
+        rig.ctx.release(2000, False)
     toks = np.concatenate([doc, rng.integers(0, 1000, N2, dtype=np.uint32)])
     rig.ctx.submit(1, toks, n_cacheable=N1)
     plan = rig.ctx.match_prefix(1, [])
@@ -310,17 +317,48 @@ def test_sharded_run_with_nccl_allgather_world1():
     assert np.array_equal(to_host(gathered)[:, 0], out)
 
 
-@pytest.mark.parametrize("load_mode,frac", [(1, 0.0), (2, 0.0), (3, 0.0), (4, 0.34), (4, 1.0)])
-def test_copy_engine_baselines_match_gather(load_mode, frac):
-    """f4 baselines (the paper's cudaMemcpyBatchAsync / block-by-block path) and the hybrid
-    copy-engine + gather-kernel load produce the same pool bits and outputs as the SM gather kernel."""
+@pytest.mark.parametrize("fragment", [False, True])
+@pytest.mark.parametrize("load_mode,frac", [(1, 0.0), (2, 0.0), (3, 0.0), (4, 0.34), (4, 1.0), (5, 0.0)])
+def test_copy_engine_baselines_match_gather(load_mode, frac, fragment):
+    """f4 baselines (the paper's cudaMemcpyBatchAsync / block-by-block path), the hybrid
+    copy-engine + gather-kernel load and the auto choice produce the same pool bits and outputs as
+    the SM gather kernel, and both equal the oracle's pool (O3) -- with the request's pages
+    consecutive (copy-engine runs merge to whole chunk-layers) and with a hole in them."""
     args = ("kout", 2, 32, 8, 128, 256, 16, 768, 90)
-    rig0, plan0, q, k, v, out0 = _single_request(*args, seed=44)
-    rig1, plan1, _, _, _, out1 = _single_request(*args, seed=44, load_mode=load_mode, load_ce_fraction=frac)
+    rig0, plan0, q, k, v, out0 = _single_request(*args, seed=44, fragment=fragment)
+    rig1, plan1, _, _, _, out1 = _single_request(*args, seed=44, fragment=fragment, load_mode=load_mode,
+                                                 load_ce_fraction=frac)
     assert plan0["pages"] == plan1["pages"] and plan0["slots"] == plan1["slots"]
+    if fragment:
+        assert plan1["pages"][:3] == [0, 2, 3]
     assert np.array_equal(out0, out1)
     p0, p1 = rig0.pool_np(), rig1.pool_np()
     assert np.array_equal(p0[:, plan0["pages"]], p1[:, plan1["pages"]])
+    for layer in range(2):
+        exp = rig1.expected_pool(plan1, k[:, 768:], v[:, 768:], layer)
+        assert np.array_equal(p1[layer][plan1["pages"]], exp[layer][plan1["pages"]])
+    st = rig1.ctx.stats
+    if load_mode in (1, 2):
+        assert st["ce_layer_loads"] == 2 and st["sm_layer_loads"] == 0
+    if load_mode == 1:   # 3 chunks x 16 page images; merged to one run per chunk unless fragmented
+        assert st["ce_copies"] == 2 * (3 if not fragment else 4)
+    if load_mode == 2:
+        assert st["ce_copies"] == 2 * 3 * 16
+    if load_mode == 5:   # 8 kv heads x 2 x 16 x 128 x 2 B = 64 KiB page images, 1 MiB chunk-layers
+        assert st["ce_layer_loads"] == 2 and st["sm_layer_loads"] == 0
+
+
+def test_auto_load_mode_picks_the_gather_for_short_runs():
+    """load_mode 5 takes the SM gather when the copy runs are short (T geometry: 2 kv heads x
+    64-token chunks = 32 KiB chunk-layers) and the pool still matches the oracle bit for bit."""
+    args = ("iid", 2, 4, 2, 64, 64, 16, 256, 64)
+    rig, plan, q, k, v, out = _single_request(*args, seed=45, load_mode=5)
+    st = rig.ctx.stats
+    assert st["sm_layer_loads"] == 2 and st["ce_layer_loads"] == 0 and st["ce_copies"] == 0
+    p = rig.pool_np()
+    for layer in range(2):
+        exp = rig.expected_pool(plan, k[:, 256:], v[:, 256:], layer)
+        assert np.array_equal(p[layer][plan["pages"]], exp[layer][plan["pages"]])
 
 
 def test_offload_third_stream_commits_real_kv():

@@ -28,7 +28,7 @@ def test_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(pcr.PROTOTYPES) == declared
-    assert lib.pcr_abi_version() == 4
+    assert lib.pcr_abi_version() == 5
 
 
 def test_blake2b_rfc7693_vectors():
@@ -174,7 +174,7 @@ def test_invalid_configs():
     with pytest.raises(pcr.PcrError):
         pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, rank=1, world=4)  # world !| Hkv
     with pytest.raises(pcr.PcrError):
-        pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=5)          # no such load path
+        pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=6)          # no such load path
     with pytest.raises(pcr.PcrError):
         pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=4, load_ce_fraction=1.5)
     pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=4, load_ce_fraction=0.5).close()
