@@ -286,15 +286,16 @@ typedef struct pcr_run_opts {
   int32_t mode;            /* 0 OVERLAP, 1 SYNC (everything in order on compute_stream) */
   int32_t host_io;         /* 1: q_all/k_all/v_all/out_all are PAGE-LOCKED HOST buffers (cudaHostAlloc /
                             * cudaHostRegister; PCR_E_INVAL otherwise).  Layer l's q/k/v are copied
-                            * into a library-owned double-buffered device staging area on an
-                            * internal stream ahead of its attention and its output is copied back
-                            * right after it, so the host I/O overlaps the layer pipeline.  Not
+                            * into a library-owned ring of device staging buffers (as many layers
+                            * as fit 512 MiB, >= 2) on the load stream just ahead of layer l's KV
+                            * load, and its output is copied back on an internal stream right after
+                            * its attention, so the host I/O overlaps the layer pipeline.  Not
                             * combinable with gathered_all. */
 } pcr_run_opts;
 
 /* The full per-request pipeline: pcr_run_prefill + (optional) offload on a third stream, the
  * per-layer event chain being load(l) -> append+attn(l) -> offload(l) (and -> all-gather(l));
- * with host_io, [H2D q/k/v(l)] -> append+attn(l) -> [D2H out(l)] on internal copy streams. */
+ * with host_io, [H2D q/k/v(l) -> load(l)] -> append+attn(l) -> [D2H out(l)] (internal stream). */
 pcr_status pcr_run_prefill_ex(pcr_ctx* ctx, int64_t req_id, const void* q_all, const void* k_all,
                               const void* v_all, void* out_all, const pcr_run_opts* opts);
 

@@ -66,8 +66,8 @@ struct pcr_ctx {
   // host_io staging (pcr_run_opts.host_io): [2][q | k | v | out] of one layer, grown on demand
   uint16_t* io_buf = nullptr;
   int64_t io_buf_elems = 0;
-  cudaStream_t io_h2d = nullptr, io_d2h = nullptr;
-  std::vector<cudaEvent_t> ev_in, ev_outdone;   // per layer: inputs staged / output copied back
+  cudaStream_t io_d2h = nullptr;
+  std::vector<cudaEvent_t> ev_outdone;   // per layer: output copied back
   // load_mode 4: the copy-engine share of the gather runs on this stream, forked/joined per layer
   cudaStream_t ce_stream = nullptr;
   cudaEvent_t ev_ce_fork = nullptr, ev_ce_join = nullptr;
@@ -200,9 +200,24 @@ int64_t build_ce_runs(pcr_ctx* c, const Request* r, int32_t layer, int32_t ch0, 
   return static_cast<int64_t>(c->ce_src.size());
 }
 
+// Extra host->device copies that ride in the same copy-engine batch as a layer's KV load
+// (host_io: the layer's q/k/v inputs).
+struct H2dCopies {
+  int32_t n = 0;
+  void* dst[3];
+  const void* src[3];
+  size_t bytes[3];
+};
+
 pcr_status enqueue_ce_copy(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s, int32_t ch0, int32_t ch1,
-                           bool batch) {
-  const int64_t n = build_ce_runs(c, r, layer, ch0, ch1, batch);
+                           bool batch, const H2dCopies* extra = nullptr) {
+  build_ce_runs(c, r, layer, ch0, ch1, batch);
+  for (int32_t i = 0; extra && i < extra->n; ++i) {
+    c->ce_dst.push_back(extra->dst[i]);
+    c->ce_src.push_back(const_cast<void*>(extra->src[i]));
+    c->ce_size.push_back(extra->bytes[i]);
+  }
+  const int64_t n = static_cast<int64_t>(c->ce_src.size());
   if (n == 0) return PCR_OK;
   if (batch) {
     cudaMemcpyAttributes attr{};
@@ -238,7 +253,18 @@ bool use_copy_engines(pcr_ctx* c, const Request* r) {
   return r->load_auto == 1;
 }
 
-pcr_status enqueue_gather(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s) {
+pcr_status enqueue_gather(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s, const H2dCopies* extra = nullptr) {
+  if (extra && extra->n > 0) {
+    if (r->plan.n_matched > 0 && use_copy_engines(c, r)) {   // one batch: inputs + KV runs
+      c->ce_layer_loads += 1;
+      return enqueue_ce_copy(c, r, layer, s, 0, r->plan.n_matched, c->cfg.load_mode != 2, extra);
+    }
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t idx = 0, fail_idx = 0;
+    CUDA_TRY(c, cudaMemcpyBatchAsync(const_cast<void**>(extra->dst), const_cast<void**>(extra->src),
+                                     const_cast<size_t*>(extra->bytes), extra->n, &attr, &idx, 1, &fail_idx, s));
+  }
   if (r->plan.n_matched == 0) return PCR_OK;
   if (c->cfg.load_mode == 3) {
     CUDA_TRY(c, pcr::launch_kv_gather_tma(c->store_dev, c->cfg.pool, d_slots_of(c, r), d_pages_of(c, r),
@@ -328,30 +354,31 @@ bool is_pinned_host(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-// host_io: streams, per-layer events and a [2][q | k | v | out] staging area for one layer.
-pcr_status ensure_host_io(pcr_ctx* c, int64_t layer_elems) {
-  if (!c->io_h2d) {
-    int lo = 0, hi = 0;
-    CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->io_h2d, cudaStreamNonBlocking, hi));
+// host_io: the D2H stream, per-layer events and a ring of R staging buffers [q | k | v | out] of one
+// layer each.  R = as many layers as fit kIoRingBytes (at least 2, at most L), so the inputs of
+// layer l+R-1 can already be crossing the link while layer l computes.
+constexpr int64_t kIoRingBytes = int64_t(512) << 20;
+
+pcr_status ensure_host_io(pcr_ctx* c, int64_t layer_elems, int32_t* ring) {
+  if (!c->io_d2h) {
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->io_d2h, cudaStreamNonBlocking));
     CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_io_join, cudaEventDisableTiming));
     for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
-      cudaEvent_t a, b;
-      CUDA_TRY(c, cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
-      c->ev_in.push_back(a);
+      cudaEvent_t b;
       CUDA_TRY(c, cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
       c->ev_outdone.push_back(b);
     }
   }
-  if (2 * layer_elems > c->io_buf_elems) {
+  const int64_t r = std::max<int64_t>(2, std::min<int64_t>(c->cfg.n_layers, kIoRingBytes / std::max<int64_t>(1, 2 * layer_elems)));
+  *ring = static_cast<int32_t>(r);
+  if (r * layer_elems > c->io_buf_elems) {
     if (c->io_buf) {
       CUDA_TRY(c, cudaDeviceSynchronize());   // rare: the staging area grows to the largest N2 seen
       CUDA_TRY(c, cudaFree(c->io_buf));
       c->io_buf = nullptr;
     }
-    CUDA_TRY(c, cudaMalloc(reinterpret_cast<void**>(&c->io_buf), 2 * layer_elems * sizeof(uint16_t)));
-    c->io_buf_elems = 2 * layer_elems;
+    CUDA_TRY(c, cudaMalloc(reinterpret_cast<void**>(&c->io_buf), r * layer_elems * sizeof(uint16_t)));
+    c->io_buf_elems = r * layer_elems;
   }
   return PCR_OK;
 }
@@ -385,39 +412,54 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
   if (o.gathered_all && !api) return fail(c, PCR_E_UNSUPPORTED, "libnccl.so.2 not loadable");
   if ((st = ensure_tables(c, r, ls)) != PCR_OK) return st;
   if (o.mode == 0) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->region_ev[r->plan.region], 0));
-  // host_io: layer l's inputs/outputs go through staging buffer l % 2 (q | k | v | out)
+  // host_io: layer l's inputs/outputs go through staging buffer l % R (q | k | v | out).  In
+  // OVERLAP mode the inputs are copied on the LOAD stream, in the same copy batch as layer l's KV
+  // load (or just ahead of the gather kernel): one FIFO of host->device traffic in the order the
+  // layers need it, so the link never splits between streams and small input copies do not pay
+  // per-copy overhead (tools/bidir_probe.cu, tools/ce_probe.cu); layer l+R's inputs wait for
+  // attention(l) to release the buffer.  Outputs return on the D2H stream (the other direction).
   const int64_t io_layer = 2 * q_layer + 2 * kv_layer;
-  cudaStream_t hs = cs, ds = cs;
+  int32_t ring = 2;
+  cudaStream_t ds = cs;
   if (o.host_io) {
-    if ((st = ensure_host_io(c, io_layer)) != PCR_OK) return st;
+    if ((st = ensure_host_io(c, io_layer, &ring)) != PCR_OK) return st;
     if (o.mode == 0) {
-      hs = c->io_h2d;
       ds = c->io_d2h;
       CUDA_TRY(c, cudaEventRecord(c->ev_io_join, cs));    // staging may still be read by earlier work
-      CUDA_TRY(c, cudaStreamWaitEvent(hs, c->ev_io_join, 0));
+      CUDA_TRY(c, cudaStreamWaitEvent(ls, c->ev_io_join, 0));
       CUDA_TRY(c, cudaStreamWaitEvent(ds, c->ev_io_join, 0));
     }
   }
-  auto stage = [&](int32_t l) -> pcr_status {   // H2D of layer l's q/k/v into buffer l % 2
-    uint16_t* b = c->io_buf + (l & 1) * io_layer;
-    if (o.mode == 0 && l >= 2) CUDA_TRY(c, cudaStreamWaitEvent(hs, c->ev_attn[l - 2], 0));  // buffer free
+  auto buf_of = [&](int32_t l) { return c->io_buf + (l % ring) * io_layer; };
+  auto stage = [&](int32_t l) -> pcr_status {   // SYNC mode: H2D of layer l's q/k/v into buffer l % R
+    uint16_t* b = buf_of(l);
     CUDA_TRY(c, cudaMemcpyAsync(b, static_cast<const uint16_t*>(q_all) + l * q_layer, q_layer * 2,
-                                cudaMemcpyHostToDevice, hs));
+                                cudaMemcpyHostToDevice, cs));
     CUDA_TRY(c, cudaMemcpyAsync(b + q_layer, static_cast<const uint16_t*>(k_all) + l * kv_layer, kv_layer * 2,
-                                cudaMemcpyHostToDevice, hs));
+                                cudaMemcpyHostToDevice, cs));
     CUDA_TRY(c, cudaMemcpyAsync(b + q_layer + kv_layer, static_cast<const uint16_t*>(v_all) + l * kv_layer,
-                                kv_layer * 2, cudaMemcpyHostToDevice, hs));
-    if (o.mode == 0) CUDA_TRY(c, cudaEventRecord(c->ev_in[l], hs));
+                                kv_layer * 2, cudaMemcpyHostToDevice, cs));
     return PCR_OK;
   };
-  if (o.host_io && o.mode == 0) {
-    for (int32_t l = 0; l < std::min<int32_t>(2, c->cfg.n_layers); ++l)
-      if ((st = stage(l)) != PCR_OK) return st;
-  }
   for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
     cudaEvent_t* et = &c->ev_t[6 * l];
+    H2dCopies in;
+    if (o.host_io && o.mode == 0) {   // layer l's inputs join its KV load batch
+      uint16_t* b = buf_of(l);
+      if (l >= ring) CUDA_TRY(c, cudaStreamWaitEvent(ls, c->ev_attn[l - ring], 0));  // buffer free
+      in.n = 3;
+      in.dst[0] = b;
+      in.src[0] = static_cast<const uint16_t*>(q_all) + l * q_layer;
+      in.bytes[0] = q_layer * 2;
+      in.dst[1] = b + q_layer;
+      in.src[1] = static_cast<const uint16_t*>(k_all) + l * kv_layer;
+      in.bytes[1] = kv_layer * 2;
+      in.dst[2] = b + q_layer + kv_layer;
+      in.src[2] = static_cast<const uint16_t*>(v_all) + l * kv_layer;
+      in.bytes[2] = kv_layer * 2;
+    }
     if (times) CUDA_TRY(c, cudaEventRecord(et[0], ls));
-    if ((st = enqueue_gather(c, r, l, ls)) != PCR_OK) return st;
+    if ((st = enqueue_gather(c, r, l, ls, &in)) != PCR_OK) return st;
     if (times) CUDA_TRY(c, cudaEventRecord(et[1], ls));
     if (o.mode == 0) {
       CUDA_TRY(c, cudaEventRecord(c->ev_load[l], ls));
@@ -428,11 +470,10 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
                    *v_l = static_cast<const uint16_t*>(v_all) + l * kv_layer;
     uint16_t* out_l = static_cast<uint16_t*>(out_all) + l * q_layer;
     if (o.host_io) {
-      uint16_t* b = c->io_buf + (l & 1) * io_layer;
+      uint16_t* b = buf_of(l);
       if (o.mode == 1 && (st = stage(l)) != PCR_OK) return st;
-      if (o.mode == 0) {
-        CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_in[l], 0));
-        if (l >= 2) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_outdone[l - 2], 0));  // out buffer drained
+      if (o.mode == 0) {   // (the inputs precede the load on ls, whose event cs already waits for)
+        if (l >= ring) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_outdone[l - ring], 0));  // out buffer drained
       }
       q_l = b;
       k_l = b + q_layer;
@@ -449,10 +490,7 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
       if (ds != cs) CUDA_TRY(c, cudaStreamWaitEvent(ds, c->ev_attn[l], 0));
       CUDA_TRY(c, cudaMemcpyAsync(static_cast<uint16_t*>(out_all) + l * q_layer, out_l, q_layer * 2,
                                   cudaMemcpyDeviceToHost, ds));
-      if (o.mode == 0) {
-        CUDA_TRY(c, cudaEventRecord(c->ev_outdone[l], ds));
-        if (l + 2 < c->cfg.n_layers && (st = stage(l + 2)) != PCR_OK) return st;
-      }
+      if (o.mode == 0) CUDA_TRY(c, cudaEventRecord(c->ev_outdone[l], ds));
     }
     if (os) {
       // layer-wise offload of the new chunks right after this layer's KV exists
@@ -484,8 +522,6 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
   }
   if (o.host_io && o.mode == 0) {   // the last outputs have reached the host buffer
     CUDA_TRY(c, cudaEventRecord(c->ev_io_join, ds));
-    CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_io_join, 0));
-    CUDA_TRY(c, cudaEventRecord(c->ev_io_join, hs));
     CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_io_join, 0));
   }
   if (times) {
@@ -648,10 +684,8 @@ void pcr_destroy(pcr_ctx* c) {
     if (c->ev_comm) cudaEventDestroy(c->ev_comm);
     if (c->ev_off) cudaEventDestroy(c->ev_off);
     for (auto e : c->ev_attn) cudaEventDestroy(e);
-    for (auto e : c->ev_in) cudaEventDestroy(e);
     for (auto e : c->ev_outdone) cudaEventDestroy(e);
     if (c->ev_io_join) cudaEventDestroy(c->ev_io_join);
-    if (c->io_h2d) cudaStreamDestroy(c->io_h2d);
     if (c->io_d2h) cudaStreamDestroy(c->io_d2h);
     if (c->io_buf) cudaFree(c->io_buf);
     if (c->ev_ce_fork) cudaEventDestroy(c->ev_ce_fork);
