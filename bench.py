@@ -65,6 +65,10 @@ def parse():
     ap.add_argument("--ssd-frac", type=float, default=0.0, help="Z: SSD tier size / distinct chunks (0 = none)")
     ap.add_argument("--ssd-path", default="/tmp/pcr_ssd_tier.bin", help="Z: SSD tier file")
     ap.add_argument("--ce-frac", type=float, default=0.5, help="--load-mode hybrid: copy-engine share of the chunks")
+    ap.add_argument("--rank-slice", type=int, default=1,
+                    help="single process doing the per-GPU work of rank 0 of a P-GPU KV-head-sharded run "
+                         "(its head slice of the load and attention, no all-gather): a one-GPU estimate of "
+                         "the per-rank critical path at P GPUs")
     ap.add_argument("--load-mode", default="auto", choices=["sm", "ce_batch", "ce_blocks", "tma", "hybrid", "auto"],
                     help="a2 implementation: sm_100a gather kernel, or the paper's copy-engine paths")
     return ap.parse_args()
@@ -311,7 +315,11 @@ def run_ours(args):
     geo = geometry(wl_geo)
     L, Hq, Hkv, d, C, S = geo["L"], geo["Hq"], geo["Hkv"], geo["d"], geo["C"], geo["S_pg"]
     assert Hkv % world == 0, "KV-head sharding needs world | Hkv"
-    hkv, hq = Hkv // world, Hq // world
+    shard = world
+    if args.rank_slice > 1:
+        assert world == 1 and Hkv % args.rank_slice == 0, "--rank-slice P: one process, P | Hkv"
+        shard = args.rank_slice
+    hkv, hq = Hkv // shard, Hq // shard
     N1 = int(round(args.ratio * (n_doc // C))) * C
     N = n_doc + n_query
     N2 = N - N1
@@ -325,7 +333,7 @@ def run_ours(args):
     pool = torch.empty(n_pool_pages * page_elems, dtype=torch.int16, device="cuda")
     store_chunks = n_doc // C + 4
     load_mode = {"sm": 0, "ce_batch": 1, "ce_blocks": 2, "tma": 3, "hybrid": 4, "auto": 5}[args.load_mode]
-    ctx = Context(L, Hq, Hkv, d, C, S, store_chunks, 4, device=local, pool=pool, rank=rank, world=world,
+    ctx = Context(L, Hq, Hkv, d, C, S, store_chunks, 4, device=local, pool=pool, rank=rank, world=shard,
                   gather_ctas=args.gather_ctas, load_mode=load_mode, load_ce_fraction=args.ce_frac)
 
     # warm the DRAM store: commit a request whose first n_chunks chunks are the cached docs
@@ -649,7 +657,10 @@ def run_ours(args):
         "config": {"workload": f"{args.workload}: {L}L {Hq}/{Hkv} heads d={d}, N1={N1} cached (host DRAM) + "
                                f"N2={N2} computed, B=1, C={C}, S_pg={S}, mode={args.mode}, load={args.load_mode}"
                                + (", +layer body (f3)" if body is not None else ""),
-                   "N1": N1, "N2": N2, "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
+                   "N1": N1, "N2": N2,
+                   "parallelism": f"kv-head shard x{world}" if world > 1 else (
+                       f"rank 0 of a kv-head shard x{shard}, emulated on one GPU (its head slice of load and "
+                       f"attention; no all-gather)" if shard > 1 else "single GPU"),
                    "l2": f"inputs > L2: {L * load_bytes / 2**20:.0f} MiB of prefix KV streamed from host per step"},
         "ttft_ms": statistics.median(step_ms), "ttft_ms_p90": float(np.percentile(step_ms, 90)),
         "ttft_pred_ms": ttft_pred, "sync_bound_ms": L * (gather_ms + attn_ms) if attn_tflops else None,

@@ -95,7 +95,7 @@ typedef struct pcr_config {
                             matched chunks (one cudaMemcpyBatchAsync on a library stream) while
                             the gather kernel moves the rest, both over the same host link;
                             5 = auto: per request, mode 1 when the chunk-layer copies merge into
-                            runs of >= 256 KiB on average (consecutive pool pages of a chunk are
+                            runs of >= 128 KiB on average (consecutive pool pages of a chunk are
                             one run), else mode 0 — the copy engines reach ~98% of the host
                             link on long runs, the SM gather ~90% at any run length
                             (profiles/r01_ce_probe.txt) */

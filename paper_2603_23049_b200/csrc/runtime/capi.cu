@@ -239,8 +239,11 @@ pcr_status enqueue_ce_copy(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s
 // layer in runs of 16 KiB / 64 KiB / 256 KiB / 1 MiB: copy engine 25.9 / 43.4 / 51.5 / 53.9 GB/s
 // (54.7 GB/s over 32 back-to-back layers of 256 KiB runs) against 50.1 GB/s for the SM gather at
 // any run size: PCIe reads issued by SMs complete in 128-byte payloads, the copy engines' in
-// larger ones, so only the copy engines reach the link's ~55.6 GB/s, and only for long runs.
-constexpr int64_t kCeMinRun = 256 << 10;
+// larger ones, so only the copy engines reach the link's ~55.6 GB/s, and only for long runs.  In
+// the pipeline at the per-rank geometry of an 8-GPU L8 run (one KV head: 2 MiB per layer in
+// 128 KiB runs) the copy engines still win: 43 us vs 52 us per layer (the gather kernel's ramp-up
+// and tail weigh on a 2 MiB load), profiles/r01_rankslice.jsonl.
+constexpr int64_t kCeMinRun = 128 << 10;
 
 bool use_copy_engines(pcr_ctx* c, const Request* r) {
   if (c->cfg.load_mode == 1 || c->cfg.load_mode == 2) return true;
