@@ -10,7 +10,7 @@ timeout 240 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; tail -1
 timeout 400 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?"
 timeout 400 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
 OUT=gpurun_out/modes.jsonl; : > $OUT
-for m in sm ce_batch ce_blocks tma; do
+for m in auto sm ce_batch ce_blocks tma; do
   timeout 200 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --load-mode $m >> $OUT 2>> gpurun_out/modes.err
   timeout 300 python bench.py --workload M7 --ratio 0.5 --steps 10 --warmup 2 --no-e2e --no-cpu-baseline --load-mode $m >> $OUT 2>> gpurun_out/modes.err
 done
@@ -21,8 +21,10 @@ for r in 0.0 0.25 0.5 0.75 1.0; do
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_L8.csv \
     python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --profile-steps 1 > /dev/null 2> gpurun_out/ncu_launch.err; echo "ncu launches rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_L8_sm.csv \
+    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --profile-steps 1 --load-mode sm > /dev/null 2>> gpurun_out/ncu_launch.err; echo "ncu launches sm rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:kv_gather -s 40 -c 1 -o gpurun_out/prof_gather -f \
-    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --profile-steps 1 > /dev/null 2> gpurun_out/ncu_gather.err; echo "ncu gather rc=$?"
+    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --profile-steps 1 --load-mode sm > /dev/null 2> gpurun_out/ncu_gather.err; echo "ncu gather rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:suffix_attn -s 40 -c 1 -o gpurun_out/prof_attn_M7 -f \
     python bench.py --workload M7 --ratio 0.5 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --profile-steps 1 > /dev/null 2> gpurun_out/ncu_attn.err; echo "ncu attn rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:suffix_attn -s 6 -c 1 -o gpurun_out/prof_attn_micro -f \
