@@ -62,6 +62,11 @@ constexpr int kPolyPairs = PCR_POLY_PAIRS;
 // (the warpgroups only hand the S buffers back), 2 = skip the MMAs (only commits), 4 = skip the
 // K/V TMA loads (the producer only arrives), 8 = the MMA warp does not wait for P: which side
 // bounds the pipeline.
+// Split-KV: every split keeps at least this many key tiles (small N2 grids are latency bound:
+// fewer tiles per CTA shorten the serial QK -> softmax -> PV chain).
+#ifndef PCR_SPLIT_MIN_TILES
+#define PCR_SPLIT_MIN_TILES 4
+#endif
 #ifndef PCR_ATTN_TIMING
 #define PCR_ATTN_TIMING 0
 #endif
@@ -652,7 +657,7 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
   int splits = 1;
   if (p.ws_o && ctas < 148) {
     splits = std::max(1, 148 / ctas);
-    splits = std::min(splits, std::max(1, max_tiles / 4));
+    splits = std::min(splits, std::max(1, max_tiles / PCR_SPLIT_MIN_TILES));
     const int64_t per_split_bytes = int64_t(p.n2) * p.hq * (D + 1) * 4;
     splits = int(std::min<int64_t>(splits, std::max<int64_t>(1, p.ws_bytes / per_split_bytes)));
   }
