@@ -218,6 +218,24 @@ def cpu_cores():
         return os.cpu_count()
 
 
+def metric_name(workload):
+    return f"reuse-prefill tokens/s ({workload}: context tokens N1+N2 per second; TTFT in ttft_ms)"
+
+
+def workload_config(args, geo, N1, N2, world=1, shard=1):
+    """The `config` object both arms print (the workload, not the implementation)."""
+    L, Hq, Hkv, d, C, S = geo["L"], geo["Hq"], geo["Hkv"], geo["d"], geo["C"], geo["S_pg"]
+    load_bytes = 2 * N1 * (Hkv // shard) * d * 2
+    return {"workload": f"{args.workload}: {L}L {Hq}/{Hkv} heads d={d}, N1={N1} cached (host DRAM) + "
+                        f"N2={N2} computed, B=1, C={C}, S_pg={S}"
+                        + (", +layer body (f3)" if getattr(args, "layer_body", False) else ""),
+            "N1": N1, "N2": N2,
+            "parallelism": f"kv-head shard x{world}" if world > 1 else (
+                f"rank 0 of a kv-head shard x{shard}, emulated on one GPU (its head slice of load and "
+                f"attention; no all-gather)" if shard > 1 else "single GPU"),
+            "l2": f"inputs > L2: {L * load_bytes / 2**20:.0f} MiB of prefix KV streamed from host per step"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -236,12 +254,11 @@ def run_reference(args):
     t_step = statistics.mean(times)
     value = (N1 + N2) / t_step
     line = {
-        "impl": "reference", "metric": f"reuse-prefill tokens/s ({args.workload})", "value": value,
+        "impl": "reference", "metric": metric_name(args.workload), "value": value,
         "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: {geo['L']}L {geo['Hq']}/{geo['Hkv']} heads d={geo['d']}, "
-                               f"N1={N1} cached + N2={N2} computed", "N1": N1, "N2": N2},
+        "config": workload_config(args, geo, N1, N2, world=max(1, args.gpus)),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
                          "sample": "1 of L layers per step (load + append + fp64 suffix attention, all heads), "
                                    "time x L"},
@@ -650,18 +667,12 @@ def run_ours(args):
             "avg_launch_ms": attn_ms_iso, "achieved": attn_flops / (attn_ms_iso * 1e-3) / 1e12,
             "frac": attn_flops / (attn_ms_iso * 1e-3) / 1e12 / bf16_peak}}
     line = {
-        "metric": f"reuse-prefill tokens/s ({args.workload}: context tokens N1+N2 per second; TTFT in ttft_ms)",
+        "metric": metric_name(args.workload),
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) bf16 KV/Q, random token ids)",
-        "config": {"workload": f"{args.workload}: {L}L {Hq}/{Hkv} heads d={d}, N1={N1} cached (host DRAM) + "
-                               f"N2={N2} computed, B=1, C={C}, S_pg={S}, mode={args.mode}, load={args.load_mode}"
-                               + (", +layer body (f3)" if body is not None else ""),
-                   "N1": N1, "N2": N2,
-                   "parallelism": f"kv-head shard x{world}" if world > 1 else (
-                       f"rank 0 of a kv-head shard x{shard}, emulated on one GPU (its head slice of load and "
-                       f"attention; no all-gather)" if shard > 1 else "single GPU"),
-                   "l2": f"inputs > L2: {L * load_bytes / 2**20:.0f} MiB of prefix KV streamed from host per step"},
+        "config": workload_config(args, geo, N1, N2, world=world, shard=shard),
+        "pipeline": {"mode": args.mode, "load_mode": args.load_mode},
         "ttft_ms": statistics.median(step_ms), "ttft_ms_p90": float(np.percentile(step_ms, 90)),
         "ttft_pred_ms": ttft_pred, "sync_bound_ms": L * (gather_ms + attn_ms) if attn_tflops else None,
         "gather_ms_per_layer": gather_ms,

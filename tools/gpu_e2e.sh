@@ -10,5 +10,5 @@ python - <<'PY'
 import json
 for l in open("gpurun_out/e2e.jsonl"):
     j=json.loads(l)
-    print(j["config"]["workload"][-25:], "val %.0f ttft %.3f e2e %.0f"%(j["value"], j["ttft_ms"], j["e2e"]["value"]), j["clocks"]["reasons"])
+    print(j["config"]["workload"][:3], j.get("pipeline"), "val %.0f ttft %.3f e2e %.0f"%(j["value"], j["ttft_ms"], j["e2e"]["value"]), j["clocks"]["reasons"])
 PY

@@ -11,5 +11,5 @@ import json
 for f in ["gpurun_out/bench_auto.json","gpurun_out/m7.jsonl"]:
     for l in open(f):
         j=json.loads(l)
-        print(j["config"]["workload"][-50:], "val %.0f ttft %.3f"%(j["value"], j["ttft_ms"]), "load %.1fus"%(j["gather_ms_per_layer"]*1e3), "attn %.1fus"%(j["attn_ms_per_layer"]*1e3), j["roofline"]["kernel"][:60], "frac %.3f"%j["roofline"]["frac"], j.get("load_path"), (j.get("roofline_gather_sm") or {}).get("frac"), (j.get("e2e") or {}).get("value"))
+        print(j["config"]["workload"][:3], j.get("pipeline"), "val %.0f ttft %.3f"%(j["value"], j["ttft_ms"]), "load %.1fus"%(j["gather_ms_per_layer"]*1e3), "attn %.1fus"%(j["attn_ms_per_layer"]*1e3), j["roofline"]["kernel"][:60], "frac %.3f"%j["roofline"]["frac"], j.get("load_path"), (j.get("roofline_gather_sm") or {}).get("frac"), (j.get("e2e") or {}).get("value"))
 PY

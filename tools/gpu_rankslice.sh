@@ -10,5 +10,5 @@ python - <<'PY'
 import json
 for l in open("gpurun_out/rankslice.jsonl"):
     j=json.loads(l)
-    print(j["config"]["parallelism"][:28], j["config"]["workload"][-9:], "ttft %.3f ms"%j["ttft_ms"], "ms/step %.3f"%j["ms_per_step"], "load %.1fus %.1f GB/s (%.3f)"%(j["gather_ms_per_layer"]*1e3, j["roofline"]["achieved"] if j["roofline"]["unit"]=="GB/s" else -1, j["roofline"]["frac"]), "attn %.1fus"%(j["attn_ms_per_layer"]*1e3), j["load_path"])
+    print(j["config"]["parallelism"][:28], j.get("pipeline"), "ttft %.3f ms"%j["ttft_ms"], "ms/step %.3f"%j["ms_per_step"], "load %.1fus %.1f GB/s (%.3f)"%(j["gather_ms_per_layer"]*1e3, j["roofline"]["achieved"] if j["roofline"]["unit"]=="GB/s" else -1, j["roofline"]["frac"]), "attn %.1fus"%(j["attn_ms_per_layer"]*1e3), j["load_path"])
 PY

@@ -33,7 +33,7 @@ python - <<'PY'
 import json
 for l in open("gpurun_out/modes.jsonl"):
     j=json.loads(l)
-    print(j["config"]["workload"][:40], j["config"]["workload"][-30:], "ttft %.2f"%j["ttft_ms"], "load/layer %.1fus"%(j["gather_ms_per_layer"]*1e3), "attn/layer %.1fus %.0f TF/s (%.1f%%)"%(j["attn_ms_per_layer"]*1e3, j["roofline_attn"]["achieved"], 100*j["roofline_attn"]["frac"]))
+    print(j["config"]["workload"][:40], j.get("pipeline"), "ttft %.2f"%j["ttft_ms"], "load/layer %.1fus"%(j["gather_ms_per_layer"]*1e3), "attn/layer %.1fus %.0f TF/s (%.1f%%)"%(j["attn_ms_per_layer"]*1e3, j["roofline_attn"]["achieved"], 100*j["roofline_attn"]["frac"]))
 PY
 cat gpurun_out/bench_default.json
 timeout 300 python tools/attn_bench.py > gpurun_out/attn_micro.jsonl 2> gpurun_out/attn_micro.err; cat gpurun_out/attn_micro.jsonl
