@@ -49,6 +49,13 @@ constexpr int kNQ = 2;         // Q tiles per CTA
 #endif
 constexpr int kStages = PCR_KV_STAGES;  // K/V smem ring depth
 constexpr int kThreads = 128 + kNQ * 128;
+// Experiment (PCR_Q_TMEM=1): Q lives in TMEM and QK^T runs as a TS MMA (A = Q from TMEM, only K
+// is read from shared memory: the 64-key SS QK^T is bound by shared-memory operand bandwidth).
+// The 128 TMEM columns for two Q tiles come from single-buffering S per Q tile.
+#ifndef PCR_Q_TMEM
+#define PCR_Q_TMEM 0
+#endif
+constexpr int kSBuf = PCR_Q_TMEM ? 1 : 2;   // S buffers per Q tile
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 // Pairs (of 16 per 32-column chunk) whose exp2 runs as a polynomial on the FMA pipe instead of
@@ -86,13 +93,16 @@ struct Layout {
   static constexpr int kKVHalf = kBlockN * 128;                // 64 keys x 128 B
   static constexpr int kKVTile = kHalves * kKVHalf;
   static constexpr int kQ0 = 0;
-  static constexpr int kK0 = kQ0 + kNQ * kQTile;
+  static constexpr int kK0 = kQ0 + (PCR_Q_TMEM ? 0 : kNQ * kQTile);   // (Q in TMEM: no smem Q)
   static constexpr int kV0 = kK0 + kStages * kKVTile;
   static constexpr int kBar = kV0 + kStages * kKVTile;
   static constexpr int kBytes = kBar + 512;
   static constexpr int kAlloc = kBytes + 1024;  // slack for 1024-byte alignment
-  // TMEM columns: S_{t,b} (Q tile t, buffer b) at (2t+b)*64; O_t at 256 + t*D.
-  static constexpr uint32_t kColO = 2 * kNQ * kBlockN;
+  // TMEM columns: S_{t,b} (Q tile t, buffer b) at (kSBuf*t+b)*64; [Q_t at kColQ + t*D/2 (bf16
+  // pairs), PCR_Q_TMEM]; O_t at kColO + t*D.
+  static constexpr uint32_t kColQ = kSBuf * kNQ * kBlockN;
+  static constexpr uint32_t kColO = kColQ + (PCR_Q_TMEM ? kNQ * D / 2 : 0);
+  static_assert(kColO + kNQ * D <= kTmemCols, "TMEM columns");
 };
 
 struct Bars {
@@ -179,7 +189,7 @@ __global__ void __maxnreg__(136)
   const int n_iter = max(0, j_end - j_begin);
 
   if (threadIdx.x == 0) {
-    mbar_init(&bars->q_full, 1);
+    mbar_init(&bars->q_full, PCR_Q_TMEM ? kNQ * 128 : 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&bars->k_full[s], 1);
       mbar_init(&bars->v_full[s], 1);
@@ -210,7 +220,7 @@ __global__ void __maxnreg__(136)
     // 32 pages, read by shuffles), one elected lane issues the TMA copies.
     if (n_iter > 0) {
       const int lane = threadIdx.x & 31;
-      if (elect_one()) {
+      if (!PCR_Q_TMEM && elect_one()) {
         mbar_arrive_expect_tx(&bars->q_full, kNQ * Lay::kQTile);
         for (int t = 0; t < kNQ; ++t)
           for (int hf = 0; hf < Lay::kHalves; ++hf)
@@ -293,10 +303,16 @@ __global__ void __maxnreg__(136)
         const uint64_t kd = k_desc0 + uint64_t((it % kStages) * Lay::kKVTile >> 4);
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < D / 16 && (PCR_ATTN_PROFILE & 2) == 0; ++kk)
-            mma_bf16_ss(tmem + (2 * t + (it & 1)) * kBlockN, qd + (((kk >> 2) * Lay::kQHalf + (kk & 3) * 32) >> 4),
-                        kd + (((kk >> 2) * Lay::kKVHalf + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
-          mma_commit(&bars->s_full[t][it & 1]);
+          for (int kk = 0; kk < D / 16 && (PCR_ATTN_PROFILE & 2) == 0; ++kk) {
+            if (PCR_Q_TMEM)
+              mma_bf16_ts(tmem + (kSBuf * t + (it % kSBuf)) * kBlockN, tmem + Lay::kColQ + t * (D / 2) + kk * 8,
+                          kd + (((kk >> 2) * Lay::kKVHalf + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
+            else
+              mma_bf16_ss(tmem + (kSBuf * t + (it % kSBuf)) * kBlockN,
+                          qd + (((kk >> 2) * Lay::kQHalf + (kk & 3) * 32) >> 4),
+                          kd + (((kk >> 2) * Lay::kKVHalf + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
+          }
+          mma_commit(&bars->s_full[t][it % kSBuf]);
           if (t == kNQ - 1) mma_commit(&bars->k_empty[it % kStages]);
         }
         __syncwarp();
@@ -306,15 +322,16 @@ __global__ void __maxnreg__(136)
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < kBlockN / 16 && (PCR_ATTN_PROFILE & 2) == 0; ++kk)
-            mma_bf16_ts(tmem + Lay::kColO + t * D, tmem + (2 * t + (it & 1)) * kBlockN + kk * 8, vd + (kk * 2048 >> 4),
-                        idesc_o, (it > 0 || kk > 0));
-          // O_t rescale fence for the last tile only (earlier rescales wait on s_full, below)
-          if (it == n_iter - 2) mma_commit(&bars->o_done[t]);
+            mma_bf16_ts(tmem + Lay::kColO + t * D, tmem + (kSBuf * t + (it % kSBuf)) * kBlockN + kk * 8,
+                        vd + (kk * 2048 >> 4), idesc_o, (it > 0 || kk > 0));
+          // O_t rescale fence for the last tile only (earlier rescales wait on s_full, below); with
+          // one S buffer the wait for S_t(it) already covers PV_t(it-1)
+          if (kSBuf == 2 && it == n_iter - 2) mma_commit(&bars->o_done[t]);
           if (t == kNQ - 1) mma_commit(&bars->v_empty[it % kStages]);
         }
         __syncwarp();
       };
-      for (int it = 0; it < min(2, n_iter); ++it) {
+      for (int it = 0; it < min(kSBuf, n_iter); ++it) {
         mbar_wait(&bars->k_full[it], 0);
         tc_fence_after();
         for (int t = 0; t < kNQ; ++t) issue_s(t, it);
@@ -335,19 +352,19 @@ __global__ void __maxnreg__(136)
       // K(it+2) have landed before it publishes P_0(it) (it has slack; the MMA warp has none).
       //   [p_full(0,it)] PV_0(it) S_0(it+2) [p_full(1,it)] PV_1(it) S_1(it+2)
       for (int it = 0; it < n_iter; ++it) {
-        const bool more = it + 2 < n_iter;
+        const bool more = it + kSBuf < n_iter;
         PCR_MTICK(2);
-        if ((PCR_ATTN_PROFILE & 8) == 0) mbar_wait(&bars->p_full[0][it & 1], (it >> 1) & 1);
+        if ((PCR_ATTN_PROFILE & 8) == 0) mbar_wait(&bars->p_full[0][it % kSBuf], (it / kSBuf) & 1);
         tc_fence_after();
         PCR_MTICK(1);
         issue_pv(0, it);
-        if (more) issue_s(0, it + 2);
+        if (more) issue_s(0, it + kSBuf);
         PCR_MTICK(2);
-        if ((PCR_ATTN_PROFILE & 8) == 0) mbar_wait(&bars->p_full[1][it & 1], (it >> 1) & 1);
+        if ((PCR_ATTN_PROFILE & 8) == 0) mbar_wait(&bars->p_full[1][it % kSBuf], (it / kSBuf) & 1);
         tc_fence_after();
         PCR_MTICK(1);
         issue_pv(1, it);
-        if (more) issue_s(1, it + 2);
+        if (more) issue_s(1, it + kSBuf);
       }
 #if PCR_ATTN_TIMING
       if ((threadIdx.x & 31) == 0 && (blockIdx.x == 0 || blockIdx.x == 300) && blockIdx.z == 0)
@@ -372,6 +389,22 @@ __global__ void __maxnreg__(136)
     // kPolyPairs of every 16 pairs), written over the S columns it came from, and the row sum
     // of the same bf16-rounded weights via FADD2 (R18).
     float m_raw = -INFINITY, l = 0.f;
+#if PCR_Q_TMEM
+    if (n_iter > 0) {
+      // this row's q (D bf16, zero past N2) -> TMEM columns kColQ + t*D/2 .. (bf16 pairs, lane = row)
+      const uint4* src = reinterpret_cast<const uint4*>(p.q + (int64_t(i) * p.hq + qh) * D);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        uint4 v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = i < p.n2 ? src[c * 8 + e] : make_uint4(0, 0, 0, 0);
+        tmem_st32(lane_base + Lay::kColQ + t * (D / 2) + c * 32, reinterpret_cast<const float*>(v));
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bars->q_full);
+    }
+#endif
 #if PCR_EXP_PINGPONG
     if (t == 1 && n_iter > 0) named_bar_arrive(1, 256);  // tile 0 takes the first turn
 #endif
@@ -385,18 +418,19 @@ __global__ void __maxnreg__(136)
     for (int it = 0; it < n_iter; ++it) {
       const int key0 = (j_begin + it) * kBlockN;
       const bool diag = key0 + kBlockN - 1 > tile_first_key_limit;  // tile crosses this Q tile's diagonal
-      const uint32_t s_col = lane_base + (2 * t + (it & 1)) * kBlockN;
+      const uint32_t s_col = lane_base + (kSBuf * t + (it % kSBuf)) * kBlockN;
       PCR_TICK(5);
-      mbar_wait(&bars->s_full[t][it & 1], (it >> 1) & 1);
+      mbar_wait(&bars->s_full[t][it % kSBuf], (it / kSBuf) & 1);
       tc_fence_after();
       PCR_TICK(0);
       if (PCR_ATTN_PROFILE & 1) {
         tc_fence_before();
         if (t == 0) {
           mbar_wait(&bars->v_full[it % kStages], (it / kStages) & 1);
-          if (it + 2 < n_iter) mbar_wait(&bars->k_full[(it + 2) % kStages], ((it + 2) / kStages) & 1);
+          if (it + kSBuf < n_iter)
+            mbar_wait(&bars->k_full[(it + kSBuf) % kStages], ((it + kSBuf) / kStages) & 1);
         }
-        mbar_arrive(&bars->p_full[t][it & 1]);
+        mbar_arrive(&bars->p_full[t][it % kSBuf]);
         continue;
       }
       float va[32], vb[32];
@@ -435,9 +469,11 @@ __global__ void __maxnreg__(136)
         // warpgroup waits for next iteration anyway) certifies PV_t(it-1); the last tile has no
         // S_t(it+1) and waits on o_done, committed once after PV_t(n_iter-2).  Every barrier
         // phase thus has a waiter (compute-sanitizer synccheck clean).
-        if (it + 1 < n_iter) mbar_wait(&bars->s_full[t][(it + 1) & 1], ((it + 1) >> 1) & 1);
-        else mbar_wait(&bars->o_done[t], 0);
-        tc_fence_after();
+        if (kSBuf == 2) {
+          if (it + 1 < n_iter) mbar_wait(&bars->s_full[t][(it + 1) & 1], ((it + 1) >> 1) & 1);
+          else mbar_wait(&bars->o_done[t], 0);
+          tc_fence_after();
+        }
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
           float o[32];
@@ -477,7 +513,7 @@ __global__ void __maxnreg__(136)
       // those waits hide inside the wait for the turn.
       if (t == 0) {
         mbar_wait(&bars->v_full[it % kStages], (it / kStages) & 1);
-        if (it + 2 < n_iter) mbar_wait(&bars->k_full[(it + 2) % kStages], ((it + 2) / kStages) & 1);
+        if (it + kSBuf < n_iter) mbar_wait(&bars->k_full[(it + kSBuf) % kStages], ((it + kSBuf) / kStages) & 1);
       }
       PCR_TICK(6);
       named_bar_sync(1 + t, 256);
@@ -492,12 +528,12 @@ __global__ void __maxnreg__(136)
       tmem_st_wait();
       tc_fence_before();
 #if !PCR_EXP_PINGPONG
-      if (t == 0) {  // the MMA warp issues PV(it) and S(it+2) on P_0(it) alone
+      if (t == 0) {  // the MMA warp issues PV(it) and S(it+kSBuf) on P_0(it) alone
         mbar_wait(&bars->v_full[it % kStages], (it / kStages) & 1);
-        if (it + 2 < n_iter) mbar_wait(&bars->k_full[(it + 2) % kStages], ((it + 2) / kStages) & 1);
+        if (it + kSBuf < n_iter) mbar_wait(&bars->k_full[(it + kSBuf) % kStages], ((it + kSBuf) / kStages) & 1);
       }
 #endif
-      mbar_arrive(&bars->p_full[t][it & 1]);
+      mbar_arrive(&bars->p_full[t][it % kSBuf]);
       // row sum of the same bf16-rounded weights (R18), off the MMA warp's critical path:
       // fp32 += bf16 (FHADD.BF16), four independent chains
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
