@@ -291,6 +291,8 @@ typedef struct pcr_run_opts {
                             * load, and its output is copied back on an internal stream right after
                             * its attention, so the host I/O overlaps the layer pipeline.  Not
                             * combinable with gathered_all. */
+  int32_t io_ring_layers;  /* host_io staging ring depth in layers: 0 = as many as fit 512 MiB
+                            * (clamped to [2, L]); otherwise clamped to [2, L]. */
 } pcr_run_opts;
 
 /* The full per-request pipeline: pcr_run_prefill + (optional) offload on a third stream, the

@@ -362,7 +362,7 @@ bool is_pinned_host(const void* p) {
 // layer l+R-1 can already be crossing the link while layer l computes.
 constexpr int64_t kIoRingBytes = int64_t(512) << 20;
 
-pcr_status ensure_host_io(pcr_ctx* c, int64_t layer_elems, int32_t* ring) {
+pcr_status ensure_host_io(pcr_ctx* c, int64_t layer_elems, int32_t want, int32_t* ring) {
   if (!c->io_d2h) {
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->io_d2h, cudaStreamNonBlocking));
     CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_io_join, cudaEventDisableTiming));
@@ -372,7 +372,8 @@ pcr_status ensure_host_io(pcr_ctx* c, int64_t layer_elems, int32_t* ring) {
       c->ev_outdone.push_back(b);
     }
   }
-  const int64_t r = std::max<int64_t>(2, std::min<int64_t>(c->cfg.n_layers, kIoRingBytes / std::max<int64_t>(1, 2 * layer_elems)));
+  const int64_t fit = want > 0 ? want : kIoRingBytes / std::max<int64_t>(1, 2 * layer_elems);
+  const int64_t r = std::max<int64_t>(2, std::min<int64_t>(c->cfg.n_layers, fit));
   *ring = static_cast<int32_t>(r);
   if (r * layer_elems > c->io_buf_elems) {
     if (c->io_buf) {
@@ -425,7 +426,7 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
   int32_t ring = 2;
   cudaStream_t ds = cs;
   if (o.host_io) {
-    if ((st = ensure_host_io(c, io_layer, &ring)) != PCR_OK) return st;
+    if ((st = ensure_host_io(c, io_layer, o.io_ring_layers, &ring)) != PCR_OK) return st;
     if (o.mode == 0) {
       ds = c->io_d2h;
       CUDA_TRY(c, cudaEventRecord(c->ev_io_join, cs));    // staging may still be read by earlier work

@@ -60,7 +60,7 @@ class PcrRunOpts(ctypes.Structure):
     _fields_ = [("compute_stream", ctypes.c_void_p), ("load_stream", ctypes.c_void_p),
                 ("offload_stream", ctypes.c_void_p), ("comm_stream", ctypes.c_void_p),
                 ("gathered_all", ctypes.c_void_p), ("layer_times_ms", ctypes.POINTER(ctypes.c_float)),
-                ("mode", ctypes.c_int32), ("host_io", ctypes.c_int32)]
+                ("mode", ctypes.c_int32), ("host_io", ctypes.c_int32), ("io_ring_layers", ctypes.c_int32)]
 
 
 # Every exported symbol of include/pcr.h with its prototype (restype, argtypes).
@@ -278,7 +278,7 @@ class Context:
 
     def run_prefill_ex(self, req_id, q_all, k_all, v_all, out_all, compute_stream, load_stream=None,
                        offload_stream=None, comm_stream=None, gathered_all=None, mode=MODE_OVERLAP,
-                       layer_times=False, host_io=False):
+                       layer_times=False, host_io=False, io_ring_layers=0):
         """Full pipeline (P:480 three streams): returns [L][3] ms (gather, append+attn, offload) if
         layer_times, else None.  host_io: q/k/v/out are page-locked HOST tensors; the library
         stages them per layer on its own copy streams (the e2e path)."""
@@ -286,7 +286,7 @@ class Context:
         o = PcrRunOpts(_stream(compute_stream), _stream(load_stream), _stream(offload_stream),
                        _stream(comm_stream), _ptr(gathered_all),
                        ctypes.cast(times, _P(ctypes.c_float)) if times is not None else None, mode,
-                       1 if host_io else 0)
+                       1 if host_io else 0, int(io_ring_layers))
         self._check(self.lib.pcr_run_prefill_ex(self.h, req_id, _ptr(q_all), _ptr(k_all), _ptr(v_all),
                                                 _ptr(out_all), ctypes.byref(o)), "pcr_run_prefill_ex")
         if layer_times:

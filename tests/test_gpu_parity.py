@@ -139,13 +139,15 @@ def test_overlap_sync_and_per_layer_api_are_bitwise_identical():
     assert np.array_equal(to_host(o), out)
 
 
-@pytest.mark.parametrize("mode", [0, 1])
-def test_host_io_matches_device_buffers(mode):
+@pytest.mark.parametrize("mode,load_mode,ring", [(0, 0, 2), (1, 0, 0), (0, 5, 2), (0, 5, 0), (1, 5, 2)])
+def test_host_io_matches_device_buffers(mode, load_mode, ring):
     """pcr_run_prefill_ex with host_io: page-locked HOST q/k/v/out, staged per layer by the library
-    on its own copy streams, gives the device-buffer result bit for bit (OVERLAP and SYNC); 5 layers
-    so the double-buffered staging wraps; pageable host memory is refused."""
+    (in OVERLAP mode the inputs ride in the layer's load: before the gather kernel, or inside the
+    copy-engine batch with load_mode auto), gives the device-buffer result bit for bit (OVERLAP and
+    SYNC); 5 layers with a 2-deep staging ring so it wraps, and the default (whole-request) ring;
+    pageable host memory is refused."""
     L, n1, n2 = 5, 1024, 130
-    rig, plan, q, k, v, out = _single_request("iid", L, 32, 8, 128, 256, 64, n1, n2, seed=9)
+    rig, plan, q, k, v, out = _single_request("iid", L, 32, 8, 128, 256, 64, n1, n2, seed=9, load_mode=load_mode)
     rig.ctx.release(1, True)
     rng = make_rng(9)
     doc = rng.integers(0, 1000, n1, dtype=np.uint32)
@@ -156,7 +158,7 @@ def test_host_io_matches_device_buffers(mode):
     for rid in (2, 3):
         rig.ctx.submit(rid, toks, n_cacheable=n1)
         assert rig.ctx.match_prefix(rid, [])["n1"] == n1
-        rig.ctx.run_prefill_ex(rid, qh, kh, vh, oh, rig.cs, rig.ls, mode=mode, host_io=True)
+        rig.ctx.run_prefill_ex(rid, qh, kh, vh, oh, rig.cs, rig.ls, mode=mode, host_io=True, io_ring_layers=ring)
         rig.cs.synchronize()
         assert np.array_equal(oh.numpy().view(np.uint16), out), rid
         rig.ctx.release(rid, True)

@@ -181,10 +181,10 @@ def test_invalid_configs():
 
 
 def test_pcr_run_opts_layout_matches_header():
-    """The binding's ctypes structs mirror include/pcr.h (ABI v4): field order and offsets that the
-    C side reads (host_io in pcr_run_opts, load_ce_fraction in pcr_config)."""
+    """The binding's ctypes structs mirror include/pcr.h (ABI v5): field order and offsets that the
+    C side reads (host_io / io_ring_layers in pcr_run_opts, load_ce_fraction in pcr_config)."""
     import ctypes
-    assert [f for f, _ in pcr.PcrRunOpts._fields_][-2:] == ["mode", "host_io"]
+    assert [f for f, _ in pcr.PcrRunOpts._fields_][-3:] == ["mode", "host_io", "io_ring_layers"]
     assert pcr.PcrConfig.load_ce_fraction.offset == pcr.PcrConfig.load_mode.offset + 4
     assert pcr.PcrConfig.ssd_path.offset % ctypes.alignment(ctypes.c_void_p) == 0
 
