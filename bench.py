@@ -50,7 +50,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="L8", choices=list(WORKLOADS))
     ap.add_argument("--ratio", type=float, default=1.0, help="prefix hit ratio of the doc tokens (M7 sweep)")
-    ap.add_argument("--mode", default="overlap", choices=["overlap", "sync"])
+    ap.add_argument("--mode", default="overlap", choices=["overlap", "sync", "only-up", "only-down"],
+                    help="layer-wise overlap of loading (up) and, with --offload, offloading (down), P:703")
+    ap.add_argument("--offload", action="store_true",
+                    help="f1: offload the request's new cacheable chunks layer by layer on a third stream "
+                         "(dropped at release so every step sees the same hit ratio)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -397,7 +401,9 @@ def run_ours(args):
     # the load stream gets the highest priority: its few gather CTAs are scheduled ahead of the
     # attention grid's CTAs whenever an SM slot frees up
     cs, ls = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
-    mode = MODE_OVERLAP if args.mode == "overlap" else MODE_SYNC
+    mode = {"overlap": 0, "sync": MODE_SYNC, "only-up": 2, "only-down": 3}[args.mode]
+    os_ = torch.cuda.Stream() if args.offload else None
+    assert not (args.offload and (world > 1 or args.layer_body)), "--offload: single GPU, no layer body"
     req_counter = [0]
     match_us = []
 
@@ -450,6 +456,9 @@ def run_ours(args):
             t = run_with_layer_body(rid, out)
         elif world > 1 and lib_comm:
             t = ctx.run_prefill_sharded(rid, q, k, v, out, gathered, cs, ls, xs, mode=mode, layer_times=times)
+        elif os_ is not None:
+            t = ctx.run_prefill_ex(rid, q, k, v, out, cs, ls, offload_stream=os_,
+                                   mode=mode if step_mode is None else step_mode, layer_times=times)
         else:
             t = ctx.run_prefill(rid, q, k, v, out, cs, ls, mode=mode if step_mode is None else step_mode,
                                 layer_times=times)
@@ -514,12 +523,14 @@ def run_ours(args):
         lt = np.array([step(q_d, k_d, v_d, out_d, times=True) for _ in range(max(1, args.profile_steps))])
         attn_ms = float(lt[:, :, 1].mean())
         gather_ms_evented = float(lt[:, :, 0].mean())
+        offload_ms = float(lt[:, :, 2].mean()) if lt.shape[2] > 2 else None
         # the same kernels with nothing running beside them (SYNC order: gather, then attention)
         lt_iso = np.array([step(q_d, k_d, v_d, out_d, times=True, step_mode=MODE_SYNC)
                            for _ in range(max(1, args.profile_steps))]) if world == 1 else None
         attn_ms_iso = float(lt_iso[:, :, 1].mean()) if lt_iso is not None else float("nan")
     else:   # per-layer events are not recorded on the layer-body path
         attn_ms = gather_ms_evented = attn_ms_iso = float("nan")
+        offload_ms = None
 
     # When the copy engines carried the timed loads (auto on long runs), time the SM gather
     # kernel on the same steps too (same events, load stream busy time per layer).
@@ -672,7 +683,9 @@ def run_ours(args):
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) bf16 KV/Q, random token ids)",
         "config": workload_config(args, geo, N1, N2, world=world, shard=shard),
-        "pipeline": {"mode": args.mode, "load_mode": args.load_mode},
+        "pipeline": {"mode": args.mode, "load_mode": args.load_mode, "offload": bool(args.offload)},
+        "offload_ms_per_layer": offload_ms,
+        "offload_bytes_per_layer": (2 * (n_doc - N1) * hkv * d * 2) if args.offload else None,
         "ttft_ms": statistics.median(step_ms), "ttft_ms_p90": float(np.percentile(step_ms, 90)),
         "ttft_pred_ms": ttft_pred, "sync_bound_ms": L * (gather_ms + attn_ms) if attn_tflops else None,
         "gather_ms_per_layer": gather_ms,

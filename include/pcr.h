@@ -278,12 +278,17 @@ pcr_status pcr_offload_layer_kv(pcr_ctx* ctx, int64_t req_id, int32_t layer, voi
 /* Options of pcr_run_prefill_ex: the paper's three streams + the optional all-gather. */
 typedef struct pcr_run_opts {
   void* compute_stream;    /* required; joined with every other stream at the end */
-  void* load_stream;       /* required in OVERLAP mode (distinct from compute_stream) */
+  void* load_stream;       /* required in OVERLAP / ONLY_UP mode (distinct from compute_stream) */
   void* offload_stream;    /* nullable: offload reserved chunks layer by layer on this stream */
   void* comm_stream;       /* required iff gathered_all != NULL */
   void* gathered_all;      /* nullable: per-layer NCCL all-gather target (pcr_run_prefill_sharded) */
   float* layer_times_ms;   /* nullable: [3L] per-layer gather, append+attention, offload (ms); blocks */
-  int32_t mode;            /* 0 OVERLAP, 1 SYNC (everything in order on compute_stream) */
+  int32_t mode;            /* 0 OVERLAP (layer-wise loading and offloading both overlapped: the
+                            * paper's Up-Down), 1 SYNC (everything in order on compute_stream),
+                            * 2 ONLY_UP (loads overlapped, offload in order after each layer's
+                            * attention on compute_stream), 3 ONLY_DOWN (loads in order on
+                            * compute_stream, offload overlapped) — P:703, fig:breakdown.
+                            * Without an offload stream 2 == 0 and 3 == 1. */
   int32_t host_io;         /* 1: q_all/k_all/v_all/out_all are PAGE-LOCKED HOST buffers (cudaHostAlloc /
                             * cudaHostRegister; PCR_E_INVAL otherwise).  Layer l's q/k/v are copied
                             * into a library-owned ring of device staging buffers (as many layers

@@ -395,9 +395,13 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
   Request* r = planned_request(c, req_id, &st);
   if (!r) return st;
   if (!q_all || !k_all || !v_all || !out_all) return fail(c, PCR_E_INVAL, "null q/k/v/out");
-  if (o.mode != 0 && o.mode != 1) return fail(c, PCR_E_INVAL, "mode must be 0 (OVERLAP) or 1 (SYNC)");
+  if (o.mode < 0 || o.mode > 3)
+    return fail(c, PCR_E_INVAL, "mode must be 0 (OVERLAP), 1 (SYNC), 2 (ONLY_UP) or 3 (ONLY_DOWN)");
+  // layer-wise loading (up) and offloading (down) overlapped or in order on the compute stream
+  // (Only-Up, Only-Down, Up-Down)
+  const bool up = o.mode == 0 || o.mode == 2, down = o.mode == 0 || o.mode == 3;
   if (!o.compute_stream) return fail(c, PCR_E_INVAL, "null compute stream");
-  if (o.mode == 0 && (!o.load_stream || o.load_stream == o.compute_stream))
+  if (up && (!o.load_stream || o.load_stream == o.compute_stream))
     return fail(c, PCR_E_INVAL, "OVERLAP mode needs a load stream distinct from the compute stream");
   if (o.gathered_all && (!o.comm_stream || !c->nccl_comm))
     return fail(c, o.comm_stream ? PCR_E_STATE : PCR_E_INVAL, "all-gather needs pcr_comm_init and a comm stream");
@@ -406,8 +410,8 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
   if (o.host_io && !(is_pinned_host(q_all) && is_pinned_host(k_all) && is_pinned_host(v_all) && is_pinned_host(out_all)))
     return fail(c, PCR_E_INVAL, "host_io needs page-locked host q/k/v/out buffers");
   cudaStream_t cs = static_cast<cudaStream_t>(o.compute_stream);
-  cudaStream_t ls = o.mode == 0 ? static_cast<cudaStream_t>(o.load_stream) : cs;
-  cudaStream_t os = o.offload_stream ? (o.mode == 0 ? static_cast<cudaStream_t>(o.offload_stream) : cs) : nullptr;
+  cudaStream_t ls = up ? static_cast<cudaStream_t>(o.load_stream) : cs;
+  cudaStream_t os = o.offload_stream ? (down ? static_cast<cudaStream_t>(o.offload_stream) : cs) : nullptr;
   cudaStream_t xs = static_cast<cudaStream_t>(o.comm_stream);
   const int64_t n2 = r->plan.n2;
   const int64_t q_layer = n2 * c->hq * c->cfg.head_dim, kv_layer = n2 * c->hkv * c->cfg.head_dim;
@@ -415,7 +419,7 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
   const pcr::NcclApi* api = o.gathered_all ? pcr::nccl_api() : nullptr;
   if (o.gathered_all && !api) return fail(c, PCR_E_UNSUPPORTED, "libnccl.so.2 not loadable");
   if ((st = ensure_tables(c, r, ls)) != PCR_OK) return st;
-  if (o.mode == 0) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->region_ev[r->plan.region], 0));
+  if (up) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->region_ev[r->plan.region], 0));
   // host_io: layer l's inputs/outputs go through staging buffer l % R (q | k | v | out).  In
   // OVERLAP mode the inputs are copied on the LOAD stream, in the same copy batch as layer l's KV
   // load (or just ahead of the gather kernel): one FIFO of host->device traffic in the order the
@@ -427,7 +431,7 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
   cudaStream_t ds = cs;
   if (o.host_io) {
     if ((st = ensure_host_io(c, io_layer, o.io_ring_layers, &ring)) != PCR_OK) return st;
-    if (o.mode == 0) {
+    if (up) {
       ds = c->io_d2h;
       CUDA_TRY(c, cudaEventRecord(c->ev_io_join, cs));    // staging may still be read by earlier work
       CUDA_TRY(c, cudaStreamWaitEvent(ls, c->ev_io_join, 0));
@@ -448,7 +452,7 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
   for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
     cudaEvent_t* et = &c->ev_t[6 * l];
     H2dCopies in;
-    if (o.host_io && o.mode == 0) {   // layer l's inputs join its KV load batch
+    if (o.host_io && up) {   // layer l's inputs join its KV load batch
       uint16_t* b = buf_of(l);
       if (l >= ring) CUDA_TRY(c, cudaStreamWaitEvent(ls, c->ev_attn[l - ring], 0));  // buffer free
       in.n = 3;
@@ -465,7 +469,7 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
     if (times) CUDA_TRY(c, cudaEventRecord(et[0], ls));
     if ((st = enqueue_gather(c, r, l, ls, &in)) != PCR_OK) return st;
     if (times) CUDA_TRY(c, cudaEventRecord(et[1], ls));
-    if (o.mode == 0) {
+    if (up) {
       CUDA_TRY(c, cudaEventRecord(c->ev_load[l], ls));
       CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_load[l], 0));
     }
@@ -475,8 +479,8 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
     uint16_t* out_l = static_cast<uint16_t*>(out_all) + l * q_layer;
     if (o.host_io) {
       uint16_t* b = buf_of(l);
-      if (o.mode == 1 && (st = stage(l)) != PCR_OK) return st;
-      if (o.mode == 0) {   // (the inputs precede the load on ls, whose event cs already waits for)
+      if (!up && (st = stage(l)) != PCR_OK) return st;
+      if (up) {   // (the inputs precede the load on ls, whose event cs already waits for)
         if (l >= ring) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_outdone[l - ring], 0));  // out buffer drained
       }
       q_l = b;
@@ -494,7 +498,7 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
       if (ds != cs) CUDA_TRY(c, cudaStreamWaitEvent(ds, c->ev_attn[l], 0));
       CUDA_TRY(c, cudaMemcpyAsync(static_cast<uint16_t*>(out_all) + l * q_layer, out_l, q_layer * 2,
                                   cudaMemcpyDeviceToHost, ds));
-      if (o.mode == 0) CUDA_TRY(c, cudaEventRecord(c->ev_outdone[l], ds));
+      if (up) CUDA_TRY(c, cudaEventRecord(c->ev_outdone[l], ds));
     }
     if (os) {
       // layer-wise offload of the new chunks right after this layer's KV exists
@@ -512,7 +516,7 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
       if (rr != 0) return fail(c, PCR_E_CUDA, "ncclAllGather failed");
     }
   }
-  if (o.mode == 0) {
+  if (up) {
     CUDA_TRY(c, cudaEventRecord(c->ev_join, ls));
     CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_join, 0));
   }
@@ -524,7 +528,7 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
     CUDA_TRY(c, cudaEventRecord(c->ev_comm, xs));
     CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_comm, 0));
   }
-  if (o.host_io && o.mode == 0) {   // the last outputs have reached the host buffer
+  if (o.host_io && up) {   // the last outputs have reached the host buffer
     CUDA_TRY(c, cudaEventRecord(c->ev_io_join, ds));
     CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_io_join, 0));
   }

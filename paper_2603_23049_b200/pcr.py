@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libpcr.so")
 
 STATUS = {0: "OK", -1: "INVAL", -2: "NOMEM", -3: "CUDA", -4: "STATE", -5: "NOREQ", -6: "INTERNAL",
           -7: "UNSUPPORTED"}
-MODE_OVERLAP, MODE_SYNC = 0, 1
+MODE_OVERLAP, MODE_SYNC, MODE_ONLY_UP, MODE_ONLY_DOWN = 0, 1, 2, 3   # P:703 Up-Down, base, Only-Up, Only-Down
 LOAD_SM_GATHER, LOAD_CE_BATCH, LOAD_CE_BLOCKS, LOAD_TMA, LOAD_HYBRID, LOAD_AUTO = 0, 1, 2, 3, 4, 5
 
 

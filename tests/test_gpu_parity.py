@@ -363,10 +363,12 @@ def test_auto_load_mode_picks_the_gather_for_short_runs():
         assert np.array_equal(p[layer][plan["pages"]], exp[layer][plan["pages"]])
 
 
-def test_offload_third_stream_commits_real_kv():
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+def test_offload_third_stream_commits_real_kv(mode):
     """f1: the Appendix C trace where new chunks reach the store ONLY through the library's
     layer-wise offload on a third stream (pcr_run_prefill_ex); every committed slot must hold
-    exactly the K/V the request computed (bitwise), and later hits must attend correctly."""
+    exactly the K/V the request computed (bitwise), and later hits must attend correctly -- in
+    each of the paper's overlap settings: Up-Down, none, Only-Up, Only-Down."""
     docs, order, reqs = appendix_c_trace(0)
     model = TinyModel(L=2, Hq=4, Hkv=2, d=64, d_model=96, d_ff=128, vocab=1 << 17, seed=0)
     W = 2
@@ -384,7 +386,8 @@ def test_offload_third_stream_commits_real_kv():
         v = np.stack([f32_to_bf16_bits(kv[l][1].astype(np.float32)) for l in range(2)])
         qd, kd, vd = to_dev(q), to_dev(k[:, N1:]), to_dev(v[:, N1:])
         od = torch.empty_like(qd)
-        t3 = rig.ctx.run_prefill_ex(i, qd, kd, vd, od, rig.cs, rig.ls, offload_stream=os_, layer_times=True)
+        t3 = rig.ctx.run_prefill_ex(i, qd, kd, vd, od, rig.cs, rig.ls, offload_stream=os_, layer_times=True,
+                                    mode=mode)
         rig.cs.synchronize()
         assert t3.shape == (2, 3)
         out = to_host(od)
