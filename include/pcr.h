@@ -98,7 +98,9 @@ typedef struct pcr_config {
                             runs of >= 128 KiB on average (consecutive pool pages of a chunk are
                             one run), else mode 0 — the copy engines reach ~98% of the host
                             link on long runs, the SM gather ~90% at any run length
-                            (profiles/r01_ce_probe.txt) */
+                            (profiles/r01_ce_probe.txt); the f1 offload of the
+                            reserved chunks makes the same choice (copy-engine D2H batch or
+                            the SM scatter kernel).  Modes 0-4 offload with the SM kernel. */
   float load_ce_fraction;  /* load_mode 4 only: share of the chunks for the copy engines, [0, 1] */
   /* SSD tier (§8 f2): a file of ssd_chunks chunk records behind the DRAM store.
    * Committed chunks are written back asynchronously; chunks of requests in the
@@ -201,6 +203,7 @@ typedef struct pcr_stats {
   int64_t ce_copies;        /* copy-engine copies enqueued for a2 loads (load_mode 1/2/4/5) */
   int64_t ce_layer_loads;   /* layer loads done by the copy engines (load_mode 1/2/5) */
   int64_t sm_layer_loads;   /* layer loads done by the SM gather kernel (load_mode 0/3/4/5) */
+  int64_t ce_offload_layers; /* layer offloads done by the copy engines (load_mode 5, long runs) */
 } pcr_stats;
 pcr_status pcr_get_stats(const pcr_ctx* ctx, pcr_stats* out);
 

@@ -74,7 +74,8 @@ struct Request {
   std::vector<int32_t> matched, reserved;  // node indices
   Plan plan;
   bool tables_uploaded = false;
-  int8_t load_auto = -1;   // load_mode 5: -1 undecided, 0 SM gather, 1 copy engines (runtime-owned)
+  int8_t load_auto = -1;      // load_mode 5: -1 undecided, 0 SM gather, 1 copy engines (runtime-owned)
+  int8_t offload_auto = -1;   // the same choice for the offload of the reserved chunks
   std::vector<int32_t> loads;      // LOADING nodes this request's match started (drained at release)
 };
 

@@ -48,6 +48,7 @@ struct pcr_ctx {
   std::string err;
   int64_t launches = 0;
   int64_t ce_copies = 0, ce_layer_loads = 0, sm_layer_loads = 0;   // a2 load-path counters (pcr_stats)
+  int64_t ce_offload_layers = 0;
   pcr::KvGeom geom{};
   int32_t gather_ctas = 16;
   // split-KV workspace: ws_floats partial-O floats followed by ws_floats/d LSE floats
@@ -175,7 +176,8 @@ pcr_status device_ready(pcr_ctx* c) {
 // images whose pool pages are also adjacent are merged into one run, so a chunk whose pages are
 // consecutive is one Hkv*2*C*d*2-byte copy (1 MiB for L8).  batch: one cudaMemcpyBatchAsync over
 // the runs; otherwise one cudaMemcpyAsync per page image (the paper's block-by-block baseline).
-int64_t build_ce_runs(pcr_ctx* c, const Request* r, int32_t layer, int32_t ch0, int32_t ch1, bool merge) {
+int64_t build_ce_runs(pcr_ctx* c, const Request* r, int32_t layer, int32_t ch0, int32_t ch1, bool merge,
+                      bool d2h = false) {
   const pcr_config& k = c->cfg;
   const int32_t ppc = k.chunk_tokens / k.page_tokens;
   const size_t page_img = static_cast<size_t>(c->hkv) * 2 * k.page_tokens * k.head_dim * 2;
@@ -188,6 +190,7 @@ int64_t build_ce_runs(pcr_ctx* c, const Request* r, int32_t layer, int32_t ch0, 
     for (int32_t pp = 0; pp < ppc; ++pp) {
       uint8_t* src = store + r->plan.slots[ch] * c->slot_bytes + (int64_t(layer) * ppc + pp) * page_img;
       uint8_t* dst = pool + (int64_t(layer) * c->n_pool_pages + r->plan.pages[ch * ppc + pp]) * page_img;
+      if (d2h) std::swap(src, dst);   // offload: pool page image -> store
       if (merge && !c->ce_src.empty() && static_cast<uint8_t*>(c->ce_src.back()) + c->ce_size.back() == src &&
           static_cast<uint8_t*>(c->ce_dst.back()) + c->ce_size.back() == dst) {
         c->ce_size.back() += page_img;
@@ -210,8 +213,8 @@ struct H2dCopies {
 };
 
 pcr_status enqueue_ce_copy(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s, int32_t ch0, int32_t ch1,
-                           bool batch, const H2dCopies* extra = nullptr) {
-  build_ce_runs(c, r, layer, ch0, ch1, batch);
+                           bool batch, const H2dCopies* extra = nullptr, bool d2h = false) {
+  build_ce_runs(c, r, layer, ch0, ch1, batch, d2h);
   for (int32_t i = 0; extra && i < extra->n; ++i) {
     c->ce_dst.push_back(extra->dst[i]);
     c->ce_src.push_back(const_cast<void*>(extra->src[i]));
@@ -228,9 +231,10 @@ pcr_status enqueue_ce_copy(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s
                                      &fail_idx, s));
   } else {
     for (int64_t j = 0; j < n; ++j)
-      CUDA_TRY(c, cudaMemcpyAsync(c->ce_dst[j], c->ce_src[j], c->ce_size[j], cudaMemcpyHostToDevice, s));
+      CUDA_TRY(c, cudaMemcpyAsync(c->ce_dst[j], c->ce_src[j], c->ce_size[j],
+                                  d2h ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, s));
   }
-  c->ce_copies += n;
+  if (!d2h) c->ce_copies += n;   // (a2 loads only)
   return PCR_OK;
 }
 
@@ -245,15 +249,27 @@ pcr_status enqueue_ce_copy(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s
 // and tail weigh on a 2 MiB load), profiles/r01_rankslice.jsonl.
 constexpr int64_t kCeMinRun = 128 << 10;
 
+bool long_runs(pcr_ctx* c, const Request* r, int32_t ch0, int32_t ch1) {
+  const int64_t n = build_ce_runs(c, r, 0, ch0, ch1, true);
+  const int64_t bytes = int64_t(ch1 - ch0) * c->slot_bytes / c->cfg.n_layers;
+  return n > 0 && bytes / n >= kCeMinRun;
+}
+
 bool use_copy_engines(pcr_ctx* c, const Request* r) {
   if (c->cfg.load_mode == 1 || c->cfg.load_mode == 2) return true;
   if (c->cfg.load_mode != 5) return false;
-  if (r->load_auto < 0) {
-    const int64_t n = build_ce_runs(c, r, 0, 0, r->plan.n_matched, true);
-    const int64_t bytes = int64_t(r->plan.n_matched) * c->slot_bytes / c->cfg.n_layers;
-    const_cast<Request*>(r)->load_auto = (n > 0 && bytes / n >= kCeMinRun) ? 1 : 0;
-  }
+  if (r->load_auto < 0) const_cast<Request*>(r)->load_auto = long_runs(c, r, 0, r->plan.n_matched) ? 1 : 0;
   return r->load_auto == 1;
+}
+
+// f1 offload mover: load_mode 5 applies the same rule to the reserved chunks' runs (D2H); the
+// other modes keep the SM scatter kernel.
+bool offload_with_copy_engines(pcr_ctx* c, const Request* r) {
+  if (c->cfg.load_mode != 5) return false;
+  if (r->offload_auto < 0)
+    const_cast<Request*>(r)->offload_auto =
+        long_runs(c, r, r->plan.n_matched, r->plan.n_matched + r->plan.n_reserved) ? 1 : 0;
+  return r->offload_auto == 1;
 }
 
 pcr_status enqueue_gather(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s, const H2dCopies* extra = nullptr) {
@@ -342,6 +358,11 @@ pcr_status enqueue_attn(pcr_ctx* c, Request* r, int32_t layer, const void* q, co
 
 pcr_status enqueue_offload(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s) {
   if (r->plan.n_reserved == 0) return PCR_OK;
+  if (offload_with_copy_engines(c, r)) {
+    c->ce_offload_layers += 1;
+    return enqueue_ce_copy(c, r, layer, s, r->plan.n_matched, r->plan.n_matched + r->plan.n_reserved, true,
+                           nullptr, true);
+  }
   CUDA_TRY(c, pcr::launch_kv_scatter(c->cfg.pool, c->store_dev, d_slots_of(c, r), d_pages_of(c, r),
                                      r->plan.n_matched, r->plan.n_reserved, layer, c->geom, c->gather_ctas, s));
   c->launches += 1;
@@ -803,6 +824,7 @@ pcr_status pcr_get_stats(const pcr_ctx* c, pcr_stats* out) {
   out->ce_copies = c->ce_copies;
   out->ce_layer_loads = c->ce_layer_loads;
   out->sm_layer_loads = c->sm_layer_loads;
+  out->ce_offload_layers = c->ce_offload_layers;
   return PCR_OK;
 }
 

@@ -53,7 +53,8 @@ class PcrStats(ctypes.Structure):
                 ("writebacks", ctypes.c_int64), ("ssd_evictions", ctypes.c_int64),
                 ("dram_evictions", ctypes.c_int64), ("ssd_bytes_read", ctypes.c_int64),
                 ("ssd_bytes_written", ctypes.c_int64), ("ce_copies", ctypes.c_int64),
-                ("ce_layer_loads", ctypes.c_int64), ("sm_layer_loads", ctypes.c_int64)]
+                ("ce_layer_loads", ctypes.c_int64), ("sm_layer_loads", ctypes.c_int64),
+                ("ce_offload_layers", ctypes.c_int64)]
 
 
 class PcrRunOpts(ctypes.Structure):

@@ -363,8 +363,48 @@ def test_auto_load_mode_picks_the_gather_for_short_runs():
         assert np.array_equal(p[layer][plan["pages"]], exp[layer][plan["pages"]])
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2, 3])
-def test_offload_third_stream_commits_real_kv(mode):
+@pytest.mark.parametrize("fragment", [False, True])
+@pytest.mark.parametrize("load_mode", [0, 5])
+def test_offload_long_runs_store_records(load_mode, fragment):
+    """f1 offload at the L8 geometry (1 MiB chunk-layers): with load_mode auto the reserved
+    chunks go back to the store in one copy-engine D2H batch per layer (runs split where the
+    pool pages are not consecutive), otherwise through the SM scatter kernel; either way every
+    reserved slot then holds exactly the request's K/V record (bitwise, O3 in reverse)."""
+    L, Hq, Hkv, d, C, S, n_doc, n2q = 2, 32, 8, 128, 256, 64, 768, 90
+    rng = make_rng(77)
+    rig = Rig(L, Hq, Hkv, d, C, S, store_chunks=6, n_pool_pages=40, load_mode=load_mode)
+    if fragment:
+        for hid in (2000, 2001):
+            rig.ctx.submit(hid, rng.integers(5000, 6000, S, dtype=np.uint32), n_cacheable=0)
+            rig.ctx.match_prefix(hid, [])
+        rig.ctx.release(2000, False)
+    N = n_doc + n2q
+    toks = rng.integers(0, 1000, N, dtype=np.uint32)
+    rig.ctx.submit(1, toks, n_cacheable=n_doc)
+    plan = rig.ctx.match_prefix(1, [])
+    assert plan["n_matched"] == 0 and plan["n_reserved"] == 3
+    q, k, v = [], [], []
+    for l in range(L):
+        ql, kl, vl = stress_values("iid", 500 + l, 0, N, Hq, Hkv, d)
+        q.append(ql)
+        k.append(kl)
+        v.append(vl)
+    q, k, v = np.stack(q), np.stack(k), np.stack(v)
+    os_ = torch.cuda.Stream()
+    qd, kd, vd = to_dev(q), to_dev(k), to_dev(v)
+    od = torch.empty_like(qd)
+    rig.ctx.run_prefill_ex(1, qd, kd, vd, od, rig.cs, rig.ls, offload_stream=os_)
+    rig.cs.synchronize()
+    recs = pack_store_slots(k, v, 3, C)
+    for c in range(3):
+        got = rig.ctx.store_read(plan["slots"][c]).reshape(recs[c].shape)
+        assert np.array_equal(got, recs[c]), c
+    assert rig.ctx.stats["ce_offload_layers"] == (L if load_mode == 5 else 0)
+    rig.ctx.release(1, True)
+
+
+@pytest.mark.parametrize("mode,load_mode", [(0, 0), (1, 0), (2, 0), (3, 0), (0, 5), (3, 5)])
+def test_offload_third_stream_commits_real_kv(mode, load_mode):
     """f1: the Appendix C trace where new chunks reach the store ONLY through the library's
     layer-wise offload on a third stream (pcr_run_prefill_ex); every committed slot must hold
     exactly the K/V the request computed (bitwise), and later hits must attend correctly -- in
@@ -372,7 +412,7 @@ def test_offload_third_stream_commits_real_kv(mode):
     docs, order, reqs = appendix_c_trace(0)
     model = TinyModel(L=2, Hq=4, Hkv=2, d=64, d_model=96, d_ff=128, vocab=1 << 17, seed=0)
     W = 2
-    rig = Rig(2, 4, 2, 64, 64, 16, store_chunks=10, n_pool_pages=64, window=W)
+    rig = Rig(2, 4, 2, 64, 64, 16, store_chunks=10, n_pool_pages=64, window=W, load_mode=load_mode)
     os_ = torch.cuda.Stream()
     for i, t in enumerate(reqs):
         rig.ctx.submit(i, t)
