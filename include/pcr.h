@@ -110,6 +110,17 @@ typedef struct pcr_config {
    * records are meaningless without the context's in-memory index. */
   const char* ssd_path;
   int64_t ssd_chunks;
+  /* How `world` ranks share a request.  0 = KV-head sharding: rank r owns KV
+   * heads [r*Hkv/world, (r+1)*Hkv/world) and their query heads, of every chunk.
+   * 1 = context split (the §8(e) variant for world > Hkv, or to spread the prefix load): every
+   * rank holds all heads; a chunk at chain depth c belongs to rank c % world (its store holds
+   * and loads only those; the planner stays replicated, so the store is still sized
+   * store_chunks slots per rank), and the suffix keys to rank (n_matched % world).  Each rank
+   * attends all suffix rows to its own keys and returns a partial (O normalised by its own row
+   * sum, log2-domain LSE: pcr_run_opts.partial_all); the partials of all ranks merge into the
+   * output (pcr_merge_partials, or the per-layer NCCL all-gather + merge of
+   * pcr_run_prefill_sharded).  Every rank receives all heads' q/k_new/v_new. */
+  int32_t shard_mode;
 } pcr_config;
 
 /* Create a context.  Allocates the pinned store (mmap + NUMA-local mbind to the GPU's
@@ -262,6 +273,9 @@ pcr_status pcr_comm_init(pcr_ctx* ctx, const uint8_t* id);
  * ncclAllGather(out_l -> gathered_l), so the gather of layer l overlaps the work of layer l+1.
  * gathered_all = [L][world][N2][Hq_loc][d] (rank-major; rank r's block holds query heads
  * [r*Hq/world, (r+1)*Hq/world)).  compute_stream is joined after the last all-gather.
+ * shard_mode 1: `out_all` receives the merged bf16 output [L][N2][Hq][d] and gathered_all is a
+ * device fp32 scratch [L][world][N2*Hq*(d+1)]: after attn(l) the comm stream all-gathers this
+ * rank's partial of layer l (library-owned) and merges the world partials into out_all[l].
  * PCR_E_STATE if pcr_comm_init has not been called. */
 pcr_status pcr_run_prefill_sharded(pcr_ctx* ctx, int64_t req_id, const void* q_all, const void* k_all,
                                    const void* v_all, void* out_all, void* gathered_all,
@@ -301,6 +315,11 @@ typedef struct pcr_run_opts {
                             * combinable with gathered_all. */
   int32_t io_ring_layers;  /* host_io staging ring depth in layers: 0 = as many as fit 512 MiB
                             * (clamped to [2, L]); otherwise clamped to [2, L]. */
+  float* partial_all;      /* shard_mode 1 (required there, NULL otherwise): device fp32
+                            * [L][N2*Hq*(d+1)]; layer l's block holds this rank's partial O
+                            * ([N2][Hq][d], normalised by its own row sums) followed by its
+                            * log2-domain LSE ([N2][Hq]; -inf for rows that see no key here).
+                            * out_all is not written (may be NULL) unless gathered_all is set. */
 } pcr_run_opts;
 
 /* The full per-request pipeline: pcr_run_prefill + (optional) offload on a third stream, the
@@ -311,6 +330,12 @@ pcr_status pcr_run_prefill_ex(pcr_ctx* ctx, int64_t req_id, const void* q_all, c
 
 /* Count of kernels launched by this ctx since creation (bench `gpu_launches`). */
 int64_t pcr_kernel_launches(const pcr_ctx* ctx);
+
+/* shard_mode 1: merge n_parts partial blocks (gathered [n_parts][N2*Hq*(d+1)], device, each
+ * laid out as pcr_run_opts.partial_all's per-layer block) into bf16 out [N2][Hq][d] on stream:
+ * out = sum_p 2^(lse_p - M) O_p / sum_p 2^(lse_p - M), M = max_p lse_p (the split-KV combine). */
+pcr_status pcr_merge_partials(pcr_ctx* ctx, const float* gathered, int32_t n_parts, int64_t n2, void* out,
+                              void* stream);
 
 /* Switch the a2 load path (pcr_config.load_mode / load_ce_fraction, same ranges) for layer loads
  * enqueued after this call; call it between requests (a load_mode 5 request keeps the choice it

@@ -4,5 +4,6 @@ The product is libpcr.so (include/pcr.h): C++ host control (prefix tree + look-a
 and hand-written sm_100a kernels (16-byte host->HBM gather, suffix append, tcgen05/TMEM/TMA
 suffix attention), driven per layer on two CUDA streams.  `pcr` is the ctypes binding.
 """
-from .pcr import (MODE_ONLY_DOWN, MODE_ONLY_UP, MODE_OVERLAP, MODE_SYNC, Context, PcrError, blake2b, comm_unique_id,  # noqa: F401
+from .pcr import (MODE_ONLY_DOWN, MODE_ONLY_UP, MODE_OVERLAP, MODE_SYNC, SHARD_CONTEXT, SHARD_HEADS, Context,  # noqa: F401
+                  PcrError, blake2b, comm_unique_id,
                   load_library)

@@ -54,7 +54,20 @@ struct AttnParams {
   float* ws_o;            // split-KV workspace [splits][N2*hq][d] fp32 (nullable: no split-KV)
   float* ws_lse;          // [splits][N2*hq] log2-domain LSE
   int64_t ws_bytes;       // bytes available in ws_o
+  // Context-split sharding: keys available on this rank = [0, kv_len) of the virtual
+  // context (its own prefix chunks, then -- on the rank that holds it -- the suffix); 0 = n1 + n2;
+  // < 0 = no key on this rank.
+  int32_t kv_len;
+  // Non-null: write this rank's partial -- O normalised by its own row sum (fp32, [N2*hq][d]) and
+  // the log2-domain LSE ([N2*hq]) -- instead of the bf16 output (merged across ranks later).
+  float* part_o;
+  float* part_lse;
 };
+
+// Merge n_parts partials (O normalised per part, log2-domain LSE; part s at o + s*o_stride and
+// lse + s*lse_stride, rows x d and rows floats) into bf16 out [rows][d] (the split-KV combine).
+cudaError_t launch_merge_partials(const float* o, int64_t o_stride, const float* lse, int64_t lse_stride,
+                                  int32_t n_parts, int64_t rows, int32_t d, uint16_t* out, cudaStream_t stream);
 
 // a4: suffix-query causal attention over the request's pool pages (tcgen05 + TMEM + TMA).
 // `tmap_pool` is a 2D tensor map over the pool viewed as [rows][d] (rows = L*pages*Hkv*2*S),

@@ -182,7 +182,8 @@ __global__ void __maxnreg__(136)
   const int mblock = n_mblocks - 1 - blockIdx.x / p.hkv;
   const int i0 = mblock * kNQ * tok_per_tile;
   const int i_end = min(i0 + kNQ * tok_per_tile, p.n2);
-  const int n_tiles_all = (p.n1 + i_end + kBlockN - 1) / kBlockN;
+  const int kv_len = p.kv_len > 0 ? p.kv_len : (p.kv_len < 0 ? 0 : p.n1 + p.n2);   // keys present here
+  const int n_tiles_all = (min(p.n1 + i_end, kv_len) + kBlockN - 1) / kBlockN;
   const int per_split = (n_tiles_all + p.n_splits - 1) / p.n_splits;
   const int j_begin = blockIdx.z * per_split;
   const int j_end = min(j_begin + per_split, n_tiles_all);
@@ -382,8 +383,9 @@ __global__ void __maxnreg__(136)
     const int qh = g * G + (r % G);              // local query head
     const uint32_t lane_base = tmem + (uint32_t((warp & 3) * 32) << 16);
     const uint32_t o_col = lane_base + Lay::kColO + t * D;
-    const int limit = p.n1 + i;  // last visible key of this row
-    const int tile_first_key_limit = p.n1 + i0 + t * tok_per_tile;
+    const int kv_len_s = p.kv_len > 0 ? p.kv_len : (p.kv_len < 0 ? 0 : p.n1 + p.n2);
+    const int limit = min(p.n1 + i, kv_len_s - 1);  // last visible key of this row
+    const int tile_first_key_limit = min(p.n1 + i0 + t * tok_per_tile, kv_len_s - 1);
     // Per tile of 64 keys: (1) row max of S (two 32-column TMEM loads, four FMNMX3 chains);
     // (2) P = bf16(2^(s*scale - m)) via FFMA2 + ex2 (MUFU, or a polynomial on the FMA pipe for
     // kPolyPairs of every 16 pairs), written over the S columns it came from, and the row sum
@@ -563,7 +565,7 @@ __global__ void __maxnreg__(136)
       tc_fence_after();
     }
     const float inv_l = (n_iter > 0 && l > 0.f) ? 1.f / l : 0.f;
-    if (p.n_splits == 1) {
+    if (p.n_splits == 1 && p.part_o == nullptr) {
       uint4* dst = reinterpret_cast<uint4*>(p.out + row_id * D);
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
@@ -616,26 +618,39 @@ __global__ void __maxnreg__(136)
 }
 
 // Merge split-KV partials: out = sum_s 2^(lse_s - M) O_s / sum_s 2^(lse_s - M), M = max_s lse_s.
+// Part s lives at ws_o + s*o_stride (rows x D) and ws_lse + s*lse_stride.  part_o != null: write
+// the merged fp32 O and log2-domain LSE (this rank's partial, context split) instead of bf16.
 template <int D>
-__global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
-                                                      uint16_t* __restrict__ out, int64_t rows_total, int n_splits) {
+__global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ ws_o, int64_t o_stride,
+                                                      const float* __restrict__ ws_lse, int64_t lse_stride,
+                                                      uint16_t* __restrict__ out, float* __restrict__ part_o,
+                                                      float* __restrict__ part_lse, int64_t rows_total, int n_splits) {
   constexpr int kVec = D / 8;  // 8 outputs (one 16-byte store) per thread
   const int64_t n = rows_total * kVec;
   for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < n; u += int64_t(gridDim.x) * blockDim.x) {
     const int64_t row = u / kVec;
     const int c8 = int(u % kVec) * 8;
     float mx = -INFINITY;
-    for (int s = 0; s < n_splits; ++s) mx = fmaxf(mx, ws_lse[s * rows_total + row]);
+    for (int s = 0; s < n_splits; ++s) mx = fmaxf(mx, ws_lse[s * lse_stride + row]);
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, wsum = 0.f;
-    for (int s = 0; s < n_splits; ++s) {
-      const float w = ex2(ws_lse[s * rows_total + row] - mx);
-      wsum += w;
-      const float4* src = reinterpret_cast<const float4*>(ws_o + (s * rows_total + row) * D + c8);
-      const float4 a = src[0], b = src[1];
-      acc[0] += w * a.x; acc[1] += w * a.y; acc[2] += w * a.z; acc[3] += w * a.w;
-      acc[4] += w * b.x; acc[5] += w * b.y; acc[6] += w * b.z; acc[7] += w * b.w;
+    if (mx != -INFINITY) {
+      for (int s = 0; s < n_splits; ++s) {
+        const float w = ex2(ws_lse[s * lse_stride + row] - mx);
+        wsum += w;
+        const float4* src = reinterpret_cast<const float4*>(ws_o + s * o_stride + row * D + c8);
+        const float4 a = src[0], b = src[1];
+        acc[0] += w * a.x; acc[1] += w * a.y; acc[2] += w * a.z; acc[3] += w * a.w;
+        acc[4] += w * b.x; acc[5] += w * b.y; acc[6] += w * b.z; acc[7] += w * b.w;
+      }
     }
-    const float inv = 1.f / wsum;
+    const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+    if (part_o) {
+      float4* dst = reinterpret_cast<float4*>(part_o + row * D + c8);
+      dst[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+      dst[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+      if (c8 == 0) part_lse[row] = wsum > 0.f ? mx + __log2f(wsum) : -INFINITY;
+      continue;
+    }
     uint32_t wv[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -691,13 +706,17 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
   const int ctas = n_mblocks * p.hkv;
   const int max_tiles = (p.n1 + p.n2 + kBlockN - 1) / kBlockN;
   int splits = 1;
-  if (p.ws_o && ctas < 148) {
+  if (p.ws_o && ctas < 148) {   // (kv_len < n1 + n2 only shortens the key range: fewer tiles)
     splits = std::max(1, 148 / ctas);
     splits = std::min(splits, std::max(1, max_tiles / PCR_SPLIT_MIN_TILES));
     const int64_t per_split_bytes = int64_t(p.n2) * p.hq * (D + 1) * 4;
     splits = int(std::min<int64_t>(splits, std::max<int64_t>(1, p.ws_bytes / per_split_bytes)));
   }
   p.n_splits = splits;
+  if (p.part_o && splits == 1) {   // one split: the kernel writes the partial itself
+    p.ws_o = p.part_o;
+    p.ws_lse = p.part_lse;
+  }
   dim3 grid(n_mblocks * p.hkv, 1, splits);
   kern<<<grid, kThreads, Layout<D>::kAlloc, stream>>>(*tmap_pool, tmap_q, p);
   cudaError_t e = cudaGetLastError();
@@ -707,7 +726,8 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
     const int64_t rows_total = int64_t(p.n2) * p.hq;
     int64_t blocks = (rows_total * (D / 8) + 255) / 256;
     blocks = std::min<int64_t>(blocks, 148 * 8);
-    combine_kernel<D><<<int(blocks), 256, 0, stream>>>(p.ws_o, p.ws_lse, p.out, rows_total, splits);
+    combine_kernel<D><<<int(blocks), 256, 0, stream>>>(p.ws_o, rows_total * D, p.ws_lse, rows_total, p.out,
+                                                        p.part_o, p.part_lse, rows_total, splits);
     e = cudaGetLastError();
     *launches += 1;
   }
@@ -717,6 +737,21 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
 }  // namespace
 
 int32_t attn_pool_box_rows(int32_t S) { return std::min(S, kBlockN); }
+
+cudaError_t launch_merge_partials(const float* o, int64_t o_stride, const float* lse, int64_t lse_stride,
+                                  int32_t n_parts, int64_t rows, int32_t d, uint16_t* out, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  int64_t blocks = std::min<int64_t>((rows * (d / 8) + 255) / 256, 148 * 8);
+  if (d == 128)
+    combine_kernel<128><<<int(blocks), 256, 0, stream>>>(o, o_stride, lse, lse_stride, out, nullptr, nullptr, rows,
+                                                         n_parts);
+  else if (d == 64)
+    combine_kernel<64><<<int(blocks), 256, 0, stream>>>(o, o_stride, lse, lse_stride, out, nullptr, nullptr, rows,
+                                                        n_parts);
+  else
+    return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_suffix_attn(const CUtensorMap* tmap_pool, const AttnParams& p, int32_t d, cudaStream_t stream,
                                int* launches) {

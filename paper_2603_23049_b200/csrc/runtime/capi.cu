@@ -27,6 +27,10 @@ using pcr::Request;
 struct pcr_ctx {
   pcr_config cfg{};
   int32_t hkv = 0, hq = 0, G = 0;
+  bool ctx_split = false;          // shard_mode 1
+  int64_t chunk_cap = 0;           // chunk entries per plan region
+  float* part_scratch = nullptr;   // shard_mode 1 + all-gather: [L][block] partials (grown on demand)
+  int64_t part_scratch_floats = 0;
   int64_t slot_elems = 0, slot_bytes = 0, page_elems_all_layers = 0, n_pool_pages = 0;
   std::unique_ptr<Planner> planner;
   bool device = false;
@@ -148,6 +152,12 @@ Request* planned_request(pcr_ctx* c, int64_t id, pcr_status* st) {
 
 int32_t* d_pages_of(pcr_ctx* c, const Request* r) { return c->d_arena + r->plan.region * c->region_words; }
 int32_t* d_slots_of(pcr_ctx* c, const Request* r) { return d_pages_of(c, r) + c->region_page_cap; }
+// shard_mode 1 region tail: [own_slots | vpages | own_res_slots | own_res_pages]
+int32_t* d_own_slots_of(pcr_ctx* c, const Request* r) { return d_slots_of(c, r) + c->chunk_cap; }
+int32_t* d_vpages_of(pcr_ctx* c, const Request* r) { return d_own_slots_of(c, r) + c->chunk_cap; }
+int32_t* d_own_res_slots_of(pcr_ctx* c, const Request* r) { return d_vpages_of(c, r) + c->region_page_cap; }
+int32_t* d_own_res_pages_of(pcr_ctx* c, const Request* r) { return d_own_res_slots_of(c, r) + c->chunk_cap; }
+bool owns_chunk(const pcr_ctx* c, int32_t depth) { return !c->ctx_split || depth % c->cfg.world == c->cfg.rank; }
 
 // First device call of a request uploads its page/slot tables; later calls (on any stream)
 // are ordered after that upload by an event.
@@ -187,7 +197,7 @@ int64_t build_ce_runs(pcr_ctx* c, const Request* r, int32_t layer, int32_t ch0, 
   uint8_t* pool = static_cast<uint8_t*>(k.pool);
   uint8_t* store = static_cast<uint8_t*>(c->store);
   for (int32_t ch = ch0; ch < ch1; ++ch)
-    for (int32_t pp = 0; pp < ppc; ++pp) {
+    for (int32_t pp = 0; pp < ppc && owns_chunk(c, ch); ++pp) {
       uint8_t* src = store + r->plan.slots[ch] * c->slot_bytes + (int64_t(layer) * ppc + pp) * page_img;
       uint8_t* dst = pool + (int64_t(layer) * c->n_pool_pages + r->plan.pages[ch * ppc + pp]) * page_img;
       if (d2h) std::swap(src, dst);   // offload: pool page image -> store
@@ -251,7 +261,8 @@ constexpr int64_t kCeMinRun = 128 << 10;
 
 bool long_runs(pcr_ctx* c, const Request* r, int32_t ch0, int32_t ch1) {
   const int64_t n = build_ce_runs(c, r, 0, ch0, ch1, true);
-  const int64_t bytes = int64_t(ch1 - ch0) * c->slot_bytes / c->cfg.n_layers;
+  int64_t bytes = 0;
+  for (size_t b : c->ce_size) bytes += static_cast<int64_t>(b);
   return n > 0 && bytes / n >= kCeMinRun;
 }
 
@@ -285,6 +296,22 @@ pcr_status enqueue_gather(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s,
                                      const_cast<size_t*>(extra->bytes), extra->n, &attr, &idx, 1, &fail_idx, s));
   }
   if (r->plan.n_matched == 0) return PCR_OK;
+  if (c->ctx_split) {   // this rank's chunks only (compacted tables), gather kernel or copy engines
+    if (use_copy_engines(c, r)) {
+      c->ce_layer_loads += 1;
+      return enqueue_ce_copy(c, r, layer, s, 0, r->plan.n_matched, c->cfg.load_mode != 2);
+    }
+    if (r->ctx_n_own == 0) return PCR_OK;
+    c->sm_layer_loads += 1;
+    if (c->cfg.load_mode == 3)
+      CUDA_TRY(c, pcr::launch_kv_gather_tma(c->store_dev, c->cfg.pool, d_own_slots_of(c, r), d_vpages_of(c, r),
+                                            r->ctx_n_own, layer, c->geom, 4 * c->gather_ctas, s));
+    else
+      CUDA_TRY(c, pcr::launch_kv_gather(c->store_dev, c->cfg.pool, d_own_slots_of(c, r), d_vpages_of(c, r),
+                                        r->ctx_n_own, layer, c->geom, c->gather_ctas, s));
+    c->launches += 1;
+    return PCR_OK;
+  }
   if (c->cfg.load_mode == 3) {
     CUDA_TRY(c, pcr::launch_kv_gather_tma(c->store_dev, c->cfg.pool, d_slots_of(c, r), d_pages_of(c, r),
                                           r->plan.n_matched, layer, c->geom, 4 * c->gather_ctas, s));
@@ -328,14 +355,23 @@ pcr_status enqueue_gather(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s,
 }
 
 pcr_status enqueue_attn(pcr_ctx* c, Request* r, int32_t layer, const void* q, const void* k, const void* v,
-                        void* out, cudaStream_t s) {
-  const int64_t n1 = r->plan.n1, n2 = r->plan.n2;
-  const int32_t n_pages = static_cast<int32_t>(r->plan.pages.size());
-  CUDA_TRY(c, pcr::launch_kv_append(k, v, c->cfg.pool, d_pages_of(c, r), n1, n2, n_pages, layer, c->geom, s));
+                        void* out, cudaStream_t s, float* part = nullptr) {
+  // shard_mode 1: the virtual context of this rank = its own prefix chunks, then the suffix
+  // (every rank appends the suffix: its reserved chunks are offloaded from there)
+  const int64_t n1 = c->ctx_split ? int64_t(r->ctx_n_own) * c->cfg.chunk_tokens : r->plan.n1, n2 = r->plan.n2;
+  const int32_t n_pages = c->ctx_split ? r->ctx_n_vpages : static_cast<int32_t>(r->plan.pages.size());
+  const int32_t* pages = c->ctx_split ? d_vpages_of(c, r) : d_pages_of(c, r);
+  CUDA_TRY(c, pcr::launch_kv_append(k, v, c->cfg.pool, pages, n1, n2, n_pages, layer, c->geom, s));
   pcr::AttnParams p{};
   p.q = static_cast<const uint16_t*>(q);
   p.out = static_cast<uint16_t*>(out);
-  p.pages = d_pages_of(c, r);
+  p.pages = pages;
+  if (c->ctx_split) {
+    const int64_t len = n1 + (r->ctx_suffix ? n2 : 0);
+    p.kv_len = len > 0 ? static_cast<int32_t>(len) : -1;   // -1: no key here (O = 0, LSE = -inf)
+    p.part_o = part;
+    p.part_lse = part + n2 * c->hq * c->cfg.head_dim;
+  }
   p.n1 = static_cast<int32_t>(n1);
   p.n2 = static_cast<int32_t>(n2);
   p.hq = c->hq;
@@ -362,6 +398,13 @@ pcr_status enqueue_offload(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s
     c->ce_offload_layers += 1;
     return enqueue_ce_copy(c, r, layer, s, r->plan.n_matched, r->plan.n_matched + r->plan.n_reserved, true,
                            nullptr, true);
+  }
+  if (c->ctx_split) {
+    if (r->ctx_n_res_own == 0) return PCR_OK;
+    CUDA_TRY(c, pcr::launch_kv_scatter(c->cfg.pool, c->store_dev, d_own_res_slots_of(c, r), d_own_res_pages_of(c, r),
+                                       0, r->ctx_n_res_own, layer, c->geom, c->gather_ctas, s));
+    c->launches += 1;
+    return PCR_OK;
   }
   CUDA_TRY(c, pcr::launch_kv_scatter(c->cfg.pool, c->store_dev, d_slots_of(c, r), d_pages_of(c, r),
                                      r->plan.n_matched, r->plan.n_reserved, layer, c->geom, c->gather_ctas, s));
@@ -415,7 +458,12 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
   if (st != PCR_OK) return st;
   Request* r = planned_request(c, req_id, &st);
   if (!r) return st;
-  if (!q_all || !k_all || !v_all || !out_all) return fail(c, PCR_E_INVAL, "null q/k/v/out");
+  if (!q_all || !k_all || !v_all || (!out_all && !(c->ctx_split && !o.gathered_all)))
+    return fail(c, PCR_E_INVAL, "null q/k/v/out");
+  if (c->ctx_split && !o.gathered_all && !o.partial_all)
+    return fail(c, PCR_E_INVAL, "shard_mode 1 needs partial_all (or gathered_all with pcr_run_prefill_sharded)");
+  if (!c->ctx_split && o.partial_all) return fail(c, PCR_E_INVAL, "partial_all is for shard_mode 1");
+  if (c->ctx_split && o.host_io) return fail(c, PCR_E_INVAL, "host_io is implemented for shard_mode 0 only");
   if (o.mode < 0 || o.mode > 3)
     return fail(c, PCR_E_INVAL, "mode must be 0 (OVERLAP), 1 (SYNC), 2 (ONLY_UP) or 3 (ONLY_DOWN)");
   // layer-wise loading (up) and offloading (down) overlapped or in order on the compute stream
@@ -460,6 +508,17 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
     }
   }
   auto buf_of = [&](int32_t l) { return c->io_buf + (l % ring) * io_layer; };
+  // shard_mode 1: per-layer partial block = O [N2*Hq][d] + LSE [N2*Hq] floats
+  const int64_t part_block = n2 * c->hq * (c->cfg.head_dim + 1);
+  if (c->ctx_split && !o.partial_all && part_block * c->cfg.n_layers > c->part_scratch_floats) {
+    if (c->part_scratch) {
+      CUDA_TRY(c, cudaDeviceSynchronize());   // rare: grows to the largest N2 seen
+      CUDA_TRY(c, cudaFree(c->part_scratch));
+      c->part_scratch = nullptr;
+    }
+    CUDA_TRY(c, cudaMalloc(reinterpret_cast<void**>(&c->part_scratch), part_block * c->cfg.n_layers * sizeof(float)));
+    c->part_scratch_floats = part_block * c->cfg.n_layers;
+  }
   auto stage = [&](int32_t l) -> pcr_status {   // SYNC mode: H2D of layer l's q/k/v into buffer l % R
     uint16_t* b = buf_of(l);
     CUDA_TRY(c, cudaMemcpyAsync(b, static_cast<const uint16_t*>(q_all) + l * q_layer, q_layer * 2,
@@ -497,7 +556,7 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
     const uint16_t *q_l = static_cast<const uint16_t*>(q_all) + l * q_layer,
                    *k_l = static_cast<const uint16_t*>(k_all) + l * kv_layer,
                    *v_l = static_cast<const uint16_t*>(v_all) + l * kv_layer;
-    uint16_t* out_l = static_cast<uint16_t*>(out_all) + l * q_layer;
+    uint16_t* out_l = out_all ? static_cast<uint16_t*>(out_all) + l * q_layer : nullptr;
     if (o.host_io) {
       uint16_t* b = buf_of(l);
       if (!up && (st = stage(l)) != PCR_OK) return st;
@@ -509,8 +568,10 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
       v_l = b + q_layer + kv_layer;
       out_l = b + q_layer + 2 * kv_layer;
     }
+    float* part_l = nullptr;   // shard_mode 1: this rank's partial of layer l
+    if (c->ctx_split) part_l = (o.partial_all ? o.partial_all : c->part_scratch) + l * part_block;
     if (times) CUDA_TRY(c, cudaEventRecord(et[2], cs));
-    st = enqueue_attn(c, r, l, q_l, k_l, v_l, out_l, cs);
+    st = enqueue_attn(c, r, l, q_l, k_l, v_l, out_l, cs, part_l);
     if (st != PCR_OK) return st;
     if (times) CUDA_TRY(c, cudaEventRecord(et[3], cs));
     if (os || o.gathered_all || o.host_io) CUDA_TRY(c, cudaEventRecord(c->ev_attn[l], cs));
@@ -528,7 +589,17 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
       if ((st = enqueue_offload(c, r, l, os)) != PCR_OK) return st;
       if (times) CUDA_TRY(c, cudaEventRecord(et[5], os));
     }
-    if (o.gathered_all) {
+    if (o.gathered_all && c->ctx_split) {
+      // context split: all-gather the ranks' partials of layer l, merge them into out_all[l]
+      CUDA_TRY(c, cudaStreamWaitEvent(xs, c->ev_attn[l], 0));
+      float* g = static_cast<float*>(o.gathered_all) + l * c->cfg.world * part_block;
+      int rr = api->all_gather(part_l, g, static_cast<size_t>(part_block) * 4, /*ncclInt8*/ 0, c->nccl_comm, xs);
+      if (rr != 0) return fail(c, PCR_E_CUDA, "ncclAllGather failed");
+      const int64_t rows = n2 * c->hq;
+      CUDA_TRY(c, pcr::launch_merge_partials(g, part_block, g + rows * c->cfg.head_dim, part_block, c->cfg.world, rows,
+                                             c->cfg.head_dim, static_cast<uint16_t*>(out_all) + l * q_layer, xs));
+      c->launches += 1;
+    } else if (o.gathered_all) {
       // re-assemble this layer's head-sharded output on the comm stream while layer l+1 runs
       CUDA_TRY(c, cudaStreamWaitEvent(xs, c->ev_attn[l], 0));
       const size_t bytes = static_cast<size_t>(q_layer) * 2;
@@ -580,6 +651,19 @@ int64_t pcr_pool_pages(const pcr_ctx* ctx) { return ctx ? ctx->n_pool_pages : -1
 int64_t pcr_slot_bytes(const pcr_ctx* ctx) { return ctx ? ctx->slot_bytes : -1; }
 int64_t pcr_kernel_launches(const pcr_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
+pcr_status pcr_merge_partials(pcr_ctx* c, const float* gathered, int32_t n_parts, int64_t n2, void* out,
+                              void* stream) {
+  if (!c) return PCR_E_INVAL;
+  pcr_status st = device_ready(c);
+  if (st != PCR_OK) return st;
+  if (!gathered || !out || n_parts < 1 || n2 < 0) return fail(c, PCR_E_INVAL, "pcr_merge_partials: bad argument");
+  const int64_t rows = n2 * c->hq, block = rows * (c->cfg.head_dim + 1);
+  CUDA_TRY(c, pcr::launch_merge_partials(gathered, block, gathered + rows * c->cfg.head_dim, block, n_parts, rows,
+                                         c->cfg.head_dim, static_cast<uint16_t*>(out), static_cast<cudaStream_t>(stream)));
+  c->launches += 1;
+  return PCR_OK;
+}
+
 pcr_status pcr_set_load_mode(pcr_ctx* c, int32_t load_mode, float load_ce_fraction) {
   if (!c) return PCR_E_INVAL;
   if (load_mode < 0 || load_mode > 5 || !(load_ce_fraction >= 0.f && load_ce_fraction <= 1.f))
@@ -595,7 +679,8 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
   const pcr_config& k = *cfg;
   if (k.n_layers < 1 || k.n_q_heads < 1 || k.n_kv_heads < 1 || k.n_q_heads % k.n_kv_heads ||
       k.head_dim < 8 || k.head_dim % 8 || k.world < 1 || k.rank < 0 || k.rank >= k.world ||
-      k.n_kv_heads % k.world || k.chunk_tokens < 1 || k.page_tokens < 1 || k.chunk_tokens % k.page_tokens ||
+      (k.shard_mode == 0 && k.n_kv_heads % k.world) || k.shard_mode < 0 || k.shard_mode > 1 ||
+      k.chunk_tokens < 1 || k.page_tokens < 1 || k.chunk_tokens % k.page_tokens ||
       k.store_chunks < 1 || k.window < 0 || k.pool_bytes < 0 || k.max_inflight < 0 || k.max_tokens < 0 ||
       k.gather_ctas < 0 || k.load_mode < 0 || k.load_mode > 5 || k.ssd_chunks < 0 ||
       !(k.load_ce_fraction >= 0.f && k.load_ce_fraction <= 1.f) ||
@@ -604,8 +689,9 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
   auto c = std::make_unique<pcr_ctx>();
   c->cfg = k;
   c->device = k.device >= 0;
-  c->hkv = k.n_kv_heads / k.world;
-  c->hq = k.n_q_heads / k.world;
+  c->ctx_split = k.shard_mode == 1;
+  c->hkv = c->ctx_split ? k.n_kv_heads : k.n_kv_heads / k.world;   // context split: all heads per rank
+  c->hq = c->ctx_split ? k.n_q_heads : k.n_q_heads / k.world;
   c->G = c->hq / c->hkv;
   c->slot_elems = int64_t(k.n_layers) * c->hkv * 2 * k.chunk_tokens * k.head_dim;
   c->slot_bytes = c->slot_elems * 2;
@@ -621,7 +707,8 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
   const int64_t max_tokens = k.max_tokens > 0 ? k.max_tokens : std::max<int64_t>(1, c->n_pool_pages * k.page_tokens);
   c->max_regions = k.max_inflight > 0 ? k.max_inflight : 4;
   c->region_page_cap = (max_tokens + k.page_tokens - 1) / k.page_tokens;
-  c->region_words = c->region_page_cap + (max_tokens + k.chunk_tokens - 1) / k.chunk_tokens;
+  c->chunk_cap = (max_tokens + k.chunk_tokens - 1) / k.chunk_tokens;
+  c->region_words = (c->ctx_split ? 2 : 1) * (c->region_page_cap + c->chunk_cap);   // + context-split tables
   c->region_words = (c->region_words + 63) / 64 * 64;
   c->planner = std::make_unique<Planner>(k.chunk_tokens, k.page_tokens, k.store_chunks, c->n_pool_pages, k.window,
                                          c->max_regions, k.ssd_chunks);
@@ -716,6 +803,7 @@ void pcr_destroy(pcr_ctx* c) {
     for (auto e : c->ev_outdone) cudaEventDestroy(e);
     if (c->ev_io_join) cudaEventDestroy(c->ev_io_join);
     if (c->io_d2h) cudaStreamDestroy(c->io_d2h);
+    if (c->part_scratch) cudaFree(c->part_scratch);
     if (c->io_buf) cudaFree(c->io_buf);
     if (c->ev_ce_fork) cudaEventDestroy(c->ev_ce_fork);
     if (c->ev_ce_join) cudaEventDestroy(c->ev_ce_join);
@@ -789,6 +877,31 @@ pcr_status pcr_match_prefix(pcr_ctx* c, int64_t req_id, const int64_t* pending, 
   int32_t* h = c->h_arena + pl.region * c->region_words;
   std::copy(pl.pages.begin(), pl.pages.end(), h);
   std::copy(pl.slots.begin(), pl.slots.end(), h + c->region_page_cap);
+  if (c->ctx_split) {
+    // [own_slots | vpages | own_res_slots | own_res_pages]: chunks at depth c % world == rank;
+    // vpages = their pages, then the pages of the suffix tokens [n1, N)
+    const int32_t ppc = c->cfg.chunk_tokens / c->cfg.page_tokens;
+    int32_t* own_slots = h + c->region_page_cap + c->chunk_cap;
+    int32_t* vpages = own_slots + c->chunk_cap;
+    int32_t* res_slots = vpages + c->region_page_cap;
+    int32_t* res_pages = res_slots + c->chunk_cap;
+    int32_t n_own = 0, n_res = 0, nv = 0;
+    for (int32_t ch = 0; ch < pl.n_matched; ++ch)
+      if (owns_chunk(c, ch)) {
+        own_slots[n_own++] = pl.slots[ch];
+        for (int32_t pp = 0; pp < ppc; ++pp) vpages[nv++] = pl.pages[ch * ppc + pp];
+      }
+    for (size_t pg = static_cast<size_t>(pl.n_matched) * ppc; pg < pl.pages.size(); ++pg) vpages[nv++] = pl.pages[pg];
+    for (int32_t ch = pl.n_matched; ch < pl.n_matched + pl.n_reserved; ++ch)
+      if (owns_chunk(c, ch)) {
+        for (int32_t pp = 0; pp < ppc; ++pp) res_pages[n_res * ppc + pp] = pl.pages[ch * ppc + pp];
+        res_slots[n_res++] = pl.slots[ch];
+      }
+    r->ctx_n_own = n_own;
+    r->ctx_n_res_own = n_res;
+    r->ctx_n_vpages = nv;
+    r->ctx_suffix = pl.n_matched % c->cfg.world == c->cfg.rank;
+  }
   return PCR_OK;
 }
 

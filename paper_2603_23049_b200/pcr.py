@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libpcr.so")
 
 STATUS = {0: "OK", -1: "INVAL", -2: "NOMEM", -3: "CUDA", -4: "STATE", -5: "NOREQ", -6: "INTERNAL",
           -7: "UNSUPPORTED"}
+SHARD_HEADS, SHARD_CONTEXT = 0, 1   # pcr_config.shard_mode (SURVEY §8(e) and its context-split variant)
 MODE_OVERLAP, MODE_SYNC, MODE_ONLY_UP, MODE_ONLY_DOWN = 0, 1, 2, 3   # P:703 Up-Down, base, Only-Up, Only-Down
 LOAD_SM_GATHER, LOAD_CE_BATCH, LOAD_CE_BLOCKS, LOAD_TMA, LOAD_HYBRID, LOAD_AUTO = 0, 1, 2, 3, 4, 5
 
@@ -36,7 +37,8 @@ class PcrConfig(ctypes.Structure):
                 ("store_chunks", ctypes.c_int64), ("window", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("pool", ctypes.c_void_p), ("pool_bytes", ctypes.c_int64), ("max_inflight", ctypes.c_int32),
                 ("max_tokens", ctypes.c_int32), ("gather_ctas", ctypes.c_int32), ("load_mode", ctypes.c_int32),
-                ("load_ce_fraction", ctypes.c_float), ("ssd_path", ctypes.c_char_p), ("ssd_chunks", ctypes.c_int64)]
+                ("load_ce_fraction", ctypes.c_float), ("ssd_path", ctypes.c_char_p), ("ssd_chunks", ctypes.c_int64),
+                ("shard_mode", ctypes.c_int32)]
 
 
 class PcrPlan(ctypes.Structure):
@@ -61,7 +63,8 @@ class PcrRunOpts(ctypes.Structure):
     _fields_ = [("compute_stream", ctypes.c_void_p), ("load_stream", ctypes.c_void_p),
                 ("offload_stream", ctypes.c_void_p), ("comm_stream", ctypes.c_void_p),
                 ("gathered_all", ctypes.c_void_p), ("layer_times_ms", ctypes.POINTER(ctypes.c_float)),
-                ("mode", ctypes.c_int32), ("host_io", ctypes.c_int32), ("io_ring_layers", ctypes.c_int32)]
+                ("mode", ctypes.c_int32), ("host_io", ctypes.c_int32), ("io_ring_layers", ctypes.c_int32),
+                ("partial_all", ctypes.POINTER(ctypes.c_float))]
 
 
 # Every exported symbol of include/pcr.h with its prototype (restype, argtypes).
@@ -85,6 +88,7 @@ PROTOTYPES = {
     "pcr_run_prefill": (_I32, [_VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _I32, _P(ctypes.c_float)]),
     "pcr_kernel_launches": (_I64, [_VP]),
     "pcr_set_load_mode": (_I32, [_VP, _I32, ctypes.c_float]),
+    "pcr_merge_partials": (_I32, [_VP, _VP, _I32, _I64, _VP, _VP]),
     "pcr_comm_unique_id": (_I32, [_P(ctypes.c_uint8)]),
     "pcr_comm_init": (_I32, [_VP, _P(ctypes.c_uint8)]),
     "pcr_run_prefill_sharded": (_I32, [_VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32,
@@ -151,7 +155,8 @@ class Context:
 
     def __init__(self, n_layers, n_q_heads, n_kv_heads, head_dim, chunk_tokens, page_tokens, store_chunks,
                  window, device=-1, pool=None, pool_bytes=None, rank=0, world=1, max_inflight=0, max_tokens=0,
-                 gather_ctas=0, load_mode=LOAD_SM_GATHER, ssd_path=None, ssd_chunks=0, load_ce_fraction=0.0):
+                 gather_ctas=0, load_mode=LOAD_SM_GATHER, ssd_path=None, ssd_chunks=0, load_ce_fraction=0.0,
+                 shard_mode=SHARD_HEADS):
         self.lib = load_library()
         if pool_bytes is None:
             pool_bytes = pool.numel() * pool.element_size() if hasattr(pool, "numel") else 0
@@ -159,7 +164,7 @@ class Context:
         self._ssd_path = ssd_path.encode() if isinstance(ssd_path, str) else ssd_path
         cfg = PcrConfig(n_layers, n_q_heads, n_kv_heads, head_dim, rank, world, chunk_tokens, page_tokens,
                         store_chunks, window, device, _ptr(pool), int(pool_bytes), max_inflight, max_tokens,
-                        gather_ctas, load_mode, float(load_ce_fraction), self._ssd_path, ssd_chunks)
+                        gather_ctas, load_mode, float(load_ce_fraction), self._ssd_path, ssd_chunks, shard_mode)
         h = ctypes.c_void_p()
         st = self.lib.pcr_create(ctypes.byref(cfg), ctypes.byref(h))
         if st != 0:
@@ -279,7 +284,7 @@ class Context:
 
     def run_prefill_ex(self, req_id, q_all, k_all, v_all, out_all, compute_stream, load_stream=None,
                        offload_stream=None, comm_stream=None, gathered_all=None, mode=MODE_OVERLAP,
-                       layer_times=False, host_io=False, io_ring_layers=0):
+                       layer_times=False, host_io=False, io_ring_layers=0, partial_all=None):
         """Full pipeline (P:480 three streams): returns [L][3] ms (gather, append+attn, offload) if
         layer_times, else None.  host_io: q/k/v/out are page-locked HOST tensors; the library
         stages them per layer on its own copy streams (the e2e path)."""
@@ -287,12 +292,18 @@ class Context:
         o = PcrRunOpts(_stream(compute_stream), _stream(load_stream), _stream(offload_stream),
                        _stream(comm_stream), _ptr(gathered_all),
                        ctypes.cast(times, _P(ctypes.c_float)) if times is not None else None, mode,
-                       1 if host_io else 0, int(io_ring_layers))
+                       1 if host_io else 0, int(io_ring_layers),
+                       ctypes.cast(_ptr(partial_all), _P(ctypes.c_float)) if partial_all is not None else None)
         self._check(self.lib.pcr_run_prefill_ex(self.h, req_id, _ptr(q_all), _ptr(k_all), _ptr(v_all),
                                                 _ptr(out_all), ctypes.byref(o)), "pcr_run_prefill_ex")
         if layer_times:
             return np.array(times[:], dtype=np.float64).reshape(self.n_layers, 3)
         return None
+
+    def merge_partials(self, gathered, n_parts, n2, out, stream):
+        """shard_mode 1: merge n_parts partial blocks (fp32 device tensor) into bf16 `out`."""
+        self._check(self.lib.pcr_merge_partials(self.h, _ptr(gathered), int(n_parts), int(n2), _ptr(out),
+                                                _stream(stream)), "pcr_merge_partials")
 
     def comm_init(self, uid: bytes):
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)

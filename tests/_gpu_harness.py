@@ -30,7 +30,8 @@ class Rig:
     def __init__(self, L, Hq, Hkv, d, C, S, store_chunks, n_pool_pages, window=0, rank=0, world=1, **kw):
         import torch
         from paper_2603_23049_b200 import Context
-        self.L, self.Hq, self.Hkv, self.d, self.C, self.S = L, Hq // world, Hkv // world, d, C, S
+        split = 1 if kw.get("shard_mode", 0) == 1 else world   # context split: all heads on every rank
+        self.L, self.Hq, self.Hkv, self.d, self.C, self.S = L, Hq // split, Hkv // split, d, C, S
         page_elems = L * self.Hkv * 2 * S * d
         self.pool = torch.zeros(n_pool_pages * page_elems, dtype=torch.int16, device="cuda")
         self.ctx = Context(L, Hq, Hkv, d, C, S, store_chunks, window, device=torch.cuda.current_device(),

@@ -454,3 +454,78 @@ def test_split_kv_edge_sweep(n1, n2):
     kc, vc = rig.expected_context(plan, k[:, n1:], v[:, n1:], 0)
     r, m = check_attention(out[0], q[0], kc, vc, n1, blocked=True)
     assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (r, m)
+
+
+@pytest.mark.parametrize("P,load_mode,kind", [(2, 0, "iid"), (3, 5, "advfuture"), (4, 5, "kout"), (8, 0, "q4")])
+def test_context_split_partials_merge_to_oracle(P, load_mode, kind):
+    """shard_mode 1 (SURVEY §8(e) variant): P ranks (emulated on one GPU, one context each) split a
+    request by chunk depth (chunk c -> rank c % P, the suffix keys -> rank n_matched % P).  Every
+    rank's store holds NaN garbage in the slots it does not own, so a rank that touched another
+    rank's chunk would poison the result.  The merged partials equal the fp64 oracle over the
+    whole context; each rank's pool holds its own chunks bit for bit; its share of the new chunks
+    reaches its store through the layer-wise offload."""
+    L, Hq, Hkv, d, C, S = 2, 32, 8, 128, 256, 64
+    n_doc, n_new, n_q = 5 * C, 2 * C, 150           # 5 cached chunks, 2 new cacheable chunks, query
+    N1, N = n_doc, n_doc + n_new + n_q
+    N2 = N - N1
+    q, k, v = [], [], []
+    for l in range(L):
+        ql, kl, vl = stress_values(kind, 900 + l, N1, N2, Hq, Hkv, d)
+        q.append(ql)
+        k.append(kl)
+        v.append(vl)
+    q, k, v = np.stack(q), np.stack(k), np.stack(v)
+    rng = make_rng(31)
+    doc = rng.integers(0, 1000, n_doc, dtype=np.uint32)
+    toks = np.concatenate([doc, rng.integers(0, 1000, N - n_doc, dtype=np.uint32)])
+    recs = pack_store_slots(k, v, (n_doc + n_new) // C, C)
+    garbage = np.full(recs[0].shape, 0x7FC0, np.uint16)   # bf16 NaN
+    block = N2 * Hq * (d + 1)
+    parts, rigs = [], []
+    for r in range(P):
+        rig = Rig(L, Hq, Hkv, d, C, S, store_chunks=12, n_pool_pages=N // S + 24, rank=r, world=P,
+                  shard_mode=1, load_mode=load_mode)
+        rig.ctx.submit(1000, np.concatenate([doc, [7]]).astype(np.uint32))
+        warm = rig.ctx.match_prefix(1000, [])
+        for c, slot in enumerate(warm["slots"]):
+            rig.write_slot(slot, recs[c] if c % P == r else garbage)
+        rig.ctx.release(1000, True)
+        rig.ctx.submit(1, toks, n_cacheable=n_doc + n_new)
+        plan = rig.ctx.match_prefix(1, [])
+        assert plan["n_matched"] == 5 and plan["n_reserved"] == 2 and plan["n1"] == N1
+        for c in range(5, 7):                            # reserved slots: garbage until offloaded
+            rig.ctx.store_write(plan["slots"][c], garbage)
+        part = torch.full((L, block), float("nan"), dtype=torch.float32, device="cuda")
+        qd, kd, vd = to_dev(q), to_dev(k[:, N1:]), to_dev(v[:, N1:])
+        os_ = torch.cuda.Stream()
+        rig.ctx.run_prefill_ex(1, qd, kd, vd, None, rig.cs, rig.ls, offload_stream=os_, partial_all=part)
+        rig.cs.synchronize()
+        parts.append(part)
+        rigs.append((rig, plan))
+        # own prefix chunks in this rank's pool (bitwise), via the oracle's load on the own subset
+        pool = rig.pool_np()
+        ppc = C // S
+        for l in range(L):
+            for c in range(5):
+                if c % P != r:
+                    continue
+                for pp in range(ppc):
+                    page = plan["pages"][c * ppc + pp]
+                    exp = recs[c][l][:, :, pp * S:(pp + 1) * S]            # [Hkv][2][S][d]
+                    assert np.array_equal(pool[l, page], exp), (r, l, c, pp)
+        # this rank's new chunks reached its store through the offload
+        for c in range(5, 7):
+            got = rig.ctx.store_read(plan["slots"][c]).reshape(recs[c].shape)
+            assert np.array_equal(got, recs[c] if c % P == r else garbage), (r, c)
+    rig0 = rigs[0][0]
+    gathered = torch.stack(parts, dim=1).contiguous()    # [L][P][block]
+    out = torch.empty((L, N2, Hq, d), dtype=torch.int16, device="cuda")
+    for l in range(L):
+        rig0.ctx.merge_partials(gathered[l], P, N2, out[l], rig0.cs)
+    rig0.cs.synchronize()
+    out = to_host(out)
+    for l in range(L):
+        r_l2, m = check_attention(out[l], q[l], k[l], v[l], N1)
+        assert r_l2 <= TOL_REL_L2 and m <= TOL_MAX_ABS, (l, r_l2, m)
+    for rig, _ in rigs:
+        rig.ctx.release(1, False)

@@ -178,13 +178,19 @@ def test_invalid_configs():
     with pytest.raises(pcr.PcrError):
         pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=4, load_ce_fraction=1.5)
     pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=4, load_ce_fraction=0.5).close()
+    with pytest.raises(pcr.PcrError):
+        pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, shard_mode=2)         # no such sharding
+    # context split: world need not divide Hkv, and every rank keeps all heads
+    c = pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, rank=3, world=4, shard_mode=1)
+    assert c.slot_bytes == 2 * 2 * 2 * 64 * 64 * 2
+    c.close()
 
 
 def test_pcr_run_opts_layout_matches_header():
     """The binding's ctypes structs mirror include/pcr.h (ABI v5): field order and offsets that the
     C side reads (host_io / io_ring_layers in pcr_run_opts, load_ce_fraction in pcr_config)."""
     import ctypes
-    assert [f for f, _ in pcr.PcrRunOpts._fields_][-3:] == ["mode", "host_io", "io_ring_layers"]
+    assert [f for f, _ in pcr.PcrRunOpts._fields_][-4:] == ["mode", "host_io", "io_ring_layers", "partial_all"]
     assert pcr.PcrConfig.load_ce_fraction.offset == pcr.PcrConfig.load_mode.offset + 4
     assert pcr.PcrConfig.ssd_path.offset % ctypes.alignment(ctypes.c_void_p) == 0
 
