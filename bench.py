@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--ssd-frac", type=float, default=0.0, help="Z: SSD tier size / distinct chunks (0 = none)")
     ap.add_argument("--ssd-path", default="/tmp/pcr_ssd_tier.bin", help="Z: SSD tier file")
     ap.add_argument("--ce-frac", type=float, default=0.5, help="--load-mode hybrid: copy-engine share of the chunks")
+    ap.add_argument("--shard", default="heads", choices=["heads", "context"],
+                    help="how P GPUs (or --rank-slice P) split a request: KV heads (north_star) or the "
+                         "context-split variant (chunk c -> rank c % P, partials merged)")
     ap.add_argument("--rank-slice", type=int, default=1,
                     help="single process doing the per-GPU work of rank 0 of a P-GPU KV-head-sharded run "
                          "(its head slice of the load and attention, no all-gather): a one-GPU estimate of "
@@ -226,10 +229,19 @@ def metric_name(workload):
     return f"reuse-prefill tokens/s ({workload}: context tokens N1+N2 per second; TTFT in ttft_ms)"
 
 
-def workload_config(args, geo, N1, N2, world=1, shard=1):
+def workload_config(args, geo, N1, N2, world=1, shard=1, ctx_split=False):
     """The `config` object both arms print (the workload, not the implementation)."""
     L, Hq, Hkv, d, C, S = geo["L"], geo["Hq"], geo["Hkv"], geo["d"], geo["C"], geo["S_pg"]
     load_bytes = 2 * N1 * (Hkv // shard) * d * 2
+    if ctx_split:
+        kind = "context split"
+        return {"workload": f"{args.workload}: {L}L {Hq}/{Hkv} heads d={d}, N1={N1} cached (host DRAM) + "
+                            f"N2={N2} computed, B=1, C={C}, S_pg={S}",
+                "N1": N1, "N2": N2,
+                "parallelism": f"{kind} x{world} (chunk c -> rank c % P, partials all-gathered and merged)"
+                if world > 1 else f"rank 0 of a {kind} x{shard}, emulated on one GPU (its chunks' load, "
+                                  f"attention of all rows to its keys, partial out; no all-gather/merge)",
+                "l2": f"inputs > L2: {L * load_bytes / 2**20:.0f} MiB of prefix KV streamed from host per step"}
     return {"workload": f"{args.workload}: {L}L {Hq}/{Hkv} heads d={d}, N1={N1} cached (host DRAM) + "
                         f"N2={N2} computed, B=1, C={C}, S_pg={S}"
                         + (", +layer body (f3)" if getattr(args, "layer_body", False) else ""),
@@ -335,16 +347,20 @@ def run_ours(args):
     wl_geo, n_doc, n_query = WORKLOADS[args.workload]
     geo = geometry(wl_geo)
     L, Hq, Hkv, d, C, S = geo["L"], geo["Hq"], geo["Hkv"], geo["d"], geo["C"], geo["S_pg"]
-    assert Hkv % world == 0, "KV-head sharding needs world | Hkv"
+    ctx_split = args.shard == "context"
+    assert ctx_split or Hkv % world == 0, "KV-head sharding needs world | Hkv"
     shard = world
     if args.rank_slice > 1:
-        assert world == 1 and Hkv % args.rank_slice == 0, "--rank-slice P: one process, P | Hkv"
+        assert world == 1 and (ctx_split or Hkv % args.rank_slice == 0), "--rank-slice P: one process, P | Hkv"
         shard = args.rank_slice
-    hkv, hq = Hkv // shard, Hq // shard
+    hkv, hq = (Hkv, Hq) if ctx_split else (Hkv // shard, Hq // shard)
     N1 = int(round(args.ratio * (n_doc // C))) * C
     N = n_doc + n_query
     N2 = N - N1
     n_chunks = N1 // C
+    # context split: this rank's chunks (depth c -> rank c % P) and whether it holds the suffix keys
+    n_own = sum(1 for c in range(n_chunks) if c % shard == rank) if ctx_split else n_chunks
+    suffix_here = (n_chunks % shard == rank) if ctx_split else True
     rng = make_rng(1000 + rank)
 
     # pool: room for 2 requests; store: the doc chunks (+ slack)
@@ -355,7 +371,8 @@ def run_ours(args):
     store_chunks = n_doc // C + 4
     load_mode = {"sm": 0, "ce_batch": 1, "ce_blocks": 2, "tma": 3, "hybrid": 4, "auto": 5}[args.load_mode]
     ctx = Context(L, Hq, Hkv, d, C, S, store_chunks, 4, device=local, pool=pool, rank=rank, world=shard,
-                  gather_ctas=args.gather_ctas, load_mode=load_mode, load_ce_fraction=args.ce_frac)
+                  gather_ctas=args.gather_ctas, load_mode=load_mode, load_ce_fraction=args.ce_frac,
+                  shard_mode=1 if ctx_split else 0)
 
     # warm the DRAM store: commit a request whose first n_chunks chunks are the cached docs
     doc = make_rng(7).integers(0, 128256, n_doc, dtype=np.uint32)       # same tokens on every rank
@@ -384,8 +401,12 @@ def run_ours(args):
     # N > 1: the library re-assembles each layer's head-sharded output with an NCCL all-gather on
     # a comm stream, overlapped with the next layer (pcr_run_prefill_sharded)
     gathered, xs, lib_comm = None, None, False
+    part_d = None     # context split on one process: this rank's partials (the merge needs every rank)
+    if ctx_split and world == 1:
+        part_d = torch.empty((L, N2 * hq * (d + 1)), dtype=torch.float32, device="cuda")
     if world > 1:
-        gathered = torch.empty((L, world) + tuple(out_d.shape[1:]), dtype=out_d.dtype, device="cuda")
+        gathered = (torch.empty((L, world, N2 * hq * (d + 1)), dtype=torch.float32, device="cuda") if ctx_split else
+                    torch.empty((L, world) + tuple(out_d.shape[1:]), dtype=out_d.dtype, device="cuda"))
         xs = torch.cuda.Stream()
         try:
             uid = [comm_unique_id() if rank == 0 else None]
@@ -404,6 +425,8 @@ def run_ours(args):
     mode = {"overlap": 0, "sync": MODE_SYNC, "only-up": 2, "only-down": 3}[args.mode]
     os_ = torch.cuda.Stream() if args.offload else None
     assert not (args.offload and (world > 1 or args.layer_body)), "--offload: single GPU, no layer body"
+    assert not (ctx_split and (args.layer_body or (world > 1 and not lib_comm))), \
+        "--shard context: no layer body; N > 1 needs the library's NCCL communicator"
     req_counter = [0]
     match_us = []
 
@@ -456,6 +479,9 @@ def run_ours(args):
             t = run_with_layer_body(rid, out)
         elif world > 1 and lib_comm:
             t = ctx.run_prefill_sharded(rid, q, k, v, out, gathered, cs, ls, xs, mode=mode, layer_times=times)
+        elif part_d is not None:
+            t = ctx.run_prefill_ex(rid, q, k, v, None, cs, ls, offload_stream=os_, partial_all=part_d,
+                                   mode=mode if step_mode is None else step_mode, layer_times=times)
         elif os_ is not None:
             t = ctx.run_prefill_ex(rid, q, k, v, out, cs, ls, offload_stream=os_,
                                    mode=mode if step_mode is None else step_mode, layer_times=times)
@@ -558,7 +584,7 @@ def run_ours(args):
     # tensors handed to pcr_run_prefill_ex(host_io=1); the library stages each layer's inputs
     # (H2D) and returns its output (D2H) on its own copy streams, overlapped with the pipeline.
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and part_d is None:   # (one rank of a context split has no whole output)
         q_p = torch.from_numpy(q_h.view(np.int16)).pin_memory()
         k_p = torch.from_numpy(k_h.view(np.int16)).pin_memory()
         v_p = torch.from_numpy(v_h.view(np.int16)).pin_memory()
@@ -606,8 +632,9 @@ def run_ours(args):
                "path": "pcr_run_prefill_ex(host_io=1): per-layer H2D/D2H staged by the library" if host_io
                        else "pinned-host copies around pcr_run_prefill (device buffers)"}
 
-    load_bytes = 2 * N1 * hkv * d * 2               # algorithmic bytes per gather launch (one layer)
-    attn_flops = 4 * hq * d * (N2 * N1 + N2 * (N2 + 1) // 2)
+    n1_here = n_own * C                             # keys this rank loads (context split: its chunks)
+    load_bytes = 2 * n1_here * hkv * d * 2          # algorithmic bytes per gather launch (one layer)
+    attn_flops = 4 * hq * d * (N2 * n1_here + (N2 * (N2 + 1) // 2 if suffix_here else 0))
     peak_h2d_after = h2d_peak_gbs(torch)
     peak_h2d = max(peak_h2d_before, peak_h2d_after)
     peaks = {}
@@ -625,7 +652,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        t_layer, n_l = oracle_sample(geo, N1, N2, hkv, hq, budget_s=15.0)
+        t_layer, n_l = oracle_sample(geo, n1_here, N2, hkv, hq, budget_s=15.0)
         cpu = {"value": N / (t_layer * L), "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
                "sample": f"{n_l} of {L} layers (pool load + append + fp64 suffix attention over all heads), "
                          f"extrapolated x{L}/{n_l}"}
@@ -682,7 +709,7 @@ def run_ours(args):
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) bf16 KV/Q, random token ids)",
-        "config": workload_config(args, geo, N1, N2, world=world, shard=shard),
+        "config": workload_config(args, geo, N1, N2, world=world, shard=shard, ctx_split=ctx_split),
         "pipeline": {"mode": args.mode, "load_mode": args.load_mode, "offload": bool(args.offload)},
         "offload_ms_per_layer": offload_ms,
         "offload_bytes_per_layer": (2 * (n_doc - N1) * hkv * d * 2) if args.offload else None,
