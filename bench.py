@@ -551,11 +551,22 @@ def run_ours(args):
         gather_ms_evented = float(lt[:, :, 0].mean())
         offload_ms = float(lt[:, :, 2].mean()) if lt.shape[2] > 2 else None
         # the same kernels with nothing running beside them (SYNC order: gather, then attention)
-        lt_iso = np.array([step(q_d, k_d, v_d, out_d, times=True, step_mode=MODE_SYNC)
-                           for _ in range(max(1, args.profile_steps))]) if world == 1 else None
+        lt_iso, sync_ms = None, []
+        if world == 1:
+            lt_iso = []
+            for _ in range(max(1, args.profile_steps)):
+                e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e_a.record(cs)
+                lt_iso.append(step(q_d, k_d, v_d, out_d, times=True, step_mode=MODE_SYNC))
+                e_b.record(cs)
+                e_b.synchronize()
+                sync_ms.append(e_a.elapsed_time(e_b))   # (includes the per-layer event reads)
+            lt_iso = np.array(lt_iso)
         attn_ms_iso = float(lt_iso[:, :, 1].mean()) if lt_iso is not None else float("nan")
+        gather_ms_iso = float(lt_iso[:, :, 0].mean()) if lt_iso is not None else float("nan")
     else:   # per-layer events are not recorded on the layer-body path
-        attn_ms = gather_ms_evented = attn_ms_iso = float("nan")
+        attn_ms = gather_ms_evented = attn_ms_iso = gather_ms_iso = float("nan")
+        sync_ms = []
         offload_ms = None
 
     # When the copy engines carried the timed loads (auto on long runs), time the SM gather
@@ -713,6 +724,16 @@ def run_ours(args):
         "pipeline": {"mode": args.mode, "load_mode": args.load_mode, "offload": bool(args.offload)},
         "offload_ms_per_layer": offload_ms,
         "offload_bytes_per_layer": (2 * (n_doc - N1) * hkv * d * 2) if args.offload else None,
+        "suffix_tokens_per_s": N2 / (statistics.median(step_ms) * 1e-3),
+        # SURVEY §8(d) derived overlap metrics (SYNC = every op in order on one stream)
+        "overlap": None if not sync_ms else {
+            "sync_ttft_ms": statistics.median(sync_ms),
+            "hidden_load_pct": 100 * (statistics.median(sync_ms) - statistics.median(step_ms)) / (L * gather_ms_iso)
+            if N1 else None,
+            "exposed_load_ms": statistics.median(step_ms) - L * attn_ms_iso,
+            "contention_attn": attn_ms / attn_ms_iso,
+            "note": "hidden load % = (SYNC - OVERLAP) / sum of isolated loads; exposed = OVERLAP - sum of isolated "
+                    "append+attention; contention = append+attention time beside the loads / alone"},
         "ttft_ms": statistics.median(step_ms), "ttft_ms_p90": float(np.percentile(step_ms, 90)),
         "ttft_pred_ms": ttft_pred, "sync_bound_ms": L * (gather_ms + attn_ms) if attn_tflops else None,
         "gather_ms_per_layer": gather_ms,
