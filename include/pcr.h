@@ -231,15 +231,16 @@ pcr_status pcr_blake2b(const void* data, int64_t n, const void* key, int32_t key
  * pinned host store into the request's pool pages:
  *   pool[layer][pages[t/S_pg]][h][kv][t%S_pg][:] = store[slots[t/C]][layer][h][kv][t%C][:]
  * for t < n1.  An sm_100a kernel reads the mapped host memory over PCIe with 16-byte
- * loads and writes 16-byte stores into the pool pages (no copy engine).  The first
- * device call of a request also uploads its page/slot tables on its stream. */
+ * loads and writes 16-byte stores into the pool pages, or (load_mode 1/2/5) the copy engines.
+ * The first device call of a request also uploads its page/slot tables on its stream. */
 pcr_status pcr_load_layer_kv(pcr_ctx* ctx, int64_t req_id, int32_t layer, void* load_stream);
 
 /* a3 + a4 — enqueue on compute_stream: append k_new/v_new ([N2][Hkv_loc][d]) at tokens
  * n1..n1+N2-1 of the pool, then suffix-query causal attention:
  *   out[i][h] = softmax_j( q[i][h] . K[j][h/G] / sqrt(d) ) V[j][h/G],  j <= n1 + i,
  * bf16 inputs, fp32 accumulation (tcgen05/TMEM), bf16 output.  The caller orders this
- * after pcr_load_layer_kv(layer) (pcr_run_prefill does so with events). */
+ * after pcr_load_layer_kv(layer) (pcr_run_prefill does so with events).  PCR_E_INVAL under
+ * shard_mode 1 (a rank's result there is a partial: pcr_run_prefill_ex with partial_all). */
 pcr_status pcr_prefill_attn_layer(pcr_ctx* ctx, int64_t req_id, int32_t layer, const void* q,
                                   const void* k_new, const void* v_new, void* out,
                                   void* compute_stream);

@@ -1012,6 +1012,8 @@ pcr_status pcr_prefill_attn_layer(pcr_ctx* c, int64_t req_id, int32_t layer, con
   if (!r) return st;
   if (layer < 0 || layer >= c->cfg.n_layers) return fail(c, PCR_E_INVAL, "layer out of range");
   if (!q || !k_new || !v_new || !out) return fail(c, PCR_E_INVAL, "null q/k/v/out");
+  if (c->ctx_split)   // a rank's attention is a partial there: pcr_run_prefill_ex(partial_all)
+    return fail(c, PCR_E_INVAL, "pcr_prefill_attn_layer: shard_mode 1 returns partials (pcr_run_prefill_ex)");
   cudaStream_t s = static_cast<cudaStream_t>(compute_stream);
   if ((st = ensure_tables(c, r, s)) != PCR_OK) return st;
   return enqueue_attn(c, r, layer, q, k_new, v_new, out, s);
