@@ -250,12 +250,16 @@ def test_appendix_c_trace_tiny_model():
         orc.release(i, True)
 
 
-def test_l8_full_size_sampled():
-    """configs[1] at full size in the bench's launch configuration (OVERLAP, 32 layers,
+@pytest.mark.parametrize("load_mode", [0, 5])
+def test_l8_full_size_sampled(load_mode):
+    """configs[1] at full size in the bench's launch configuration (OVERLAP, 32 layers, load_mode
+    auto = the copy-engine batch bench.py times, and the SM gather kernel;
     4096 cached + 128 query): sampled rows vs the oracle on layers 0, 15, 31; pool bit-exact
     on those layers."""
     L, Hq, Hkv, d, C, S, N1, N2 = 32, 32, 8, 128, 256, 64, 4096, 128
-    rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, N1, N2, seed=1)
+    rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, N1, N2, seed=1, load_mode=load_mode)
+    st = rig.ctx.stats
+    assert st["ce_layer_loads" if load_mode == 5 else "sm_layer_loads"] == L   # the mover bench.py times
     rows = sample_rows(N2, N1, C, S, k=64, seed=1)
     pool = rig.pool_np()
     for l in (0, 15, 31):
@@ -282,7 +286,7 @@ def test_m7_half_hit_full_size_sampled():
     OVERLAP: 32 layers, N1 = 4096 cached + N2 = 4224 computed (multi-wave attention grid, no KV
     split); sampled rows vs the oracle and the pool bit-exact on layers 0, 17, 31."""
     L, Hq, Hkv, d, C, S, N1, N2 = 32, 32, 8, 128, 256, 64, 4096, 4224
-    rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, N1, N2, seed=4)
+    rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, N1, N2, seed=4, load_mode=5)
     _check_sampled(rig, plan, q, k, v, out, N1, N2, C, S, (0, 17, 31), seed=4)
 
 
@@ -292,7 +296,7 @@ def test_l70_rank_slice_full_size_sampled():
     cached + N2 = 8320 computed; sampled rows and pool on layers 0, 41, 79."""
     L, Hq, Hkv, d, C, S, N1, N2 = 80, 64, 8, 128, 256, 64, 8192, 8320
     rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, N1, N2, seed=6, world=8, rank=5,
-                                              local_only=True)
+                                              local_only=True, load_mode=5)
     _check_sampled(rig, plan, q, k, v, out, N1, N2, C, S, (0, 41, 79), seed=6)
 
 
