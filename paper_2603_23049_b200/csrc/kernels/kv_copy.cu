@@ -10,6 +10,7 @@
 #include <algorithm>
 
 #include "kernels.h"
+#include "sm100_ptx.cuh"
 
 namespace pcr {
 namespace {
@@ -82,6 +83,7 @@ __global__ void kv_append_kernel(const uint4* __restrict__ k_new, const uint4* _
                                  uint4* __restrict__ pool, const int32_t* __restrict__ pages, int64_t n1,
                                  int64_t n2, int32_t n_req_pages, int32_t layer, KvGeom g, int32_t row16_log2,
                                  int32_t S_log2) {
+  ptx::grid_dep_launch();   // PDL: the attention after this append may start its prologue now
   const int64_t row16 = int64_t(1) << row16_log2;
   const int64_t page16 = int64_t(g.Hkv) * 2 * g.S * row16;
   uint4* dst_layer = pool + int64_t(layer) * g.n_pool_pages * page16;

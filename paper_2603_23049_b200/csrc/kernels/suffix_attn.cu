@@ -32,6 +32,8 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <utility>
 
 #include "kernels.h"
 #include "sm100_ptx.cuh"
@@ -214,6 +216,10 @@ __global__ void __maxnreg__(136)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  // Everything above (barrier init, descriptor prefetch, TMEM alloc) overlaps the tail of the
+  // append kernel before it under PDL; q and the pool are read only after it has completed.
+  grid_dep_wait();
+  grid_dep_launch();
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
@@ -627,6 +633,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
                                                       float* __restrict__ part_lse, int64_t rows_total, int n_splits) {
   constexpr int kVec = D / 8;  // 8 outputs (one 16-byte store) per thread
   const int64_t n = rows_total * kVec;
+  grid_dep_wait();   // PDL: the partials are complete and visible past this point
   for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < n; u += int64_t(gridDim.x) * blockDim.x) {
     const int64_t row = u / kVec;
     const int c8 = int(u % kVec) * 8;
@@ -677,6 +684,32 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// Programmatic dependent launch (PCR_PDL=0 disables): the grid may be scheduled while the kernel
+// before it in the stream drains; its griddepcontrol.wait then orders every dependent read.
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PCR_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 template <int D>
 cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStream_t stream, int* launches) {
   static bool configured = false;
@@ -718,17 +751,18 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
     p.ws_lse = p.part_lse;
   }
   dim3 grid(n_mblocks * p.hkv, 1, splits);
-  kern<<<grid, kThreads, Layout<D>::kAlloc, stream>>>(*tmap_pool, tmap_q, p);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(kern, grid, dim3(kThreads), Layout<D>::kAlloc, stream, *tmap_pool, tmap_q, p);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   *launches += 1;
   if (splits > 1) {
     const int64_t rows_total = int64_t(p.n2) * p.hq;
     int64_t blocks = (rows_total * (D / 8) + 255) / 256;
     blocks = std::min<int64_t>(blocks, 148 * 8);
-    combine_kernel<D><<<int(blocks), 256, 0, stream>>>(p.ws_o, rows_total * D, p.ws_lse, rows_total, p.out,
-                                                        p.part_o, p.part_lse, rows_total, splits);
-    e = cudaGetLastError();
+    e = launch_pdl(combine_kernel<D>, dim3(int(blocks)), dim3(256), 0, stream, (const float*)p.ws_o,
+                   rows_total * D, (const float*)p.ws_lse, rows_total, p.out, p.part_o, p.part_lse, rows_total,
+                   splits);
+    if (e == cudaSuccess) e = cudaGetLastError();
     *launches += 1;
   }
   return e;
