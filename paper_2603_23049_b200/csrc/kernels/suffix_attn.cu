@@ -122,6 +122,25 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// Experiment knob: K/V TMA loads carry an L2 evict_last policy (the pool's layer stays in L2
+// while the next layer's load streams in beside the attention).
+#ifndef PCR_KV_L2HINT
+#define PCR_KV_L2HINT 0
+#endif
+__device__ __forceinline__ void tma_load_2d_kv(void* smem_dst, const CUtensorMap* m, int32_t c0, int32_t c1,
+                                               uint64_t* bar, uint64_t policy) {
+#if PCR_KV_L2HINT
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+#else
+  (void)policy;
+  tma_load_2d(smem_dst, m, c0, c1, bar);
+#endif
+}
+
 // D[tmem] (+)= A[tmem] * B[smem]  (kind::f16; A is M x K bf16 packed two per 32-bit column).
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {
@@ -239,6 +258,10 @@ __global__ void __maxnreg__(136)
       const int box = min(p.S, kBlockN);  // rows per TMA box (the pool tensor map's box height)
       const int n_box = kBlockN / box;    // 1, 2 or 4 (S_pg >= 16)
       int pg_base = -64, pg_val = 0;
+      uint64_t kv_policy = 0;
+#if PCR_KV_L2HINT
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(kv_policy));
+#endif
       // K(j) and V(j) go into stage j % kStages once their previous occupants are consumed: K after
       // the last QK^T that read it (k_empty), V after the last PV (v_empty).
       for (int it = 0; it < n_iter; ++it) {
@@ -272,8 +295,8 @@ __global__ void __maxnreg__(136)
 #pragma unroll
               for (int hf = 0; hf < Lay::kHalves; ++hf)
                 if (b < n_box)
-                tma_load_2d(ks + hf * Lay::kKVHalf + b * box * 128, &tmap_pool, hf * 64, int32_t(row_k[b]),
-                            &bars->k_full[st]);
+                tma_load_2d_kv(ks + hf * Lay::kKVHalf + b * box * 128, &tmap_pool, hf * 64, int32_t(row_k[b]),
+                               &bars->k_full[st], kv_policy);
           }
         }
         __syncwarp();
@@ -288,8 +311,8 @@ __global__ void __maxnreg__(136)
 #pragma unroll
               for (int hf = 0; hf < Lay::kHalves; ++hf)
                 if (b < n_box)
-                tma_load_2d(vs + hf * Lay::kKVHalf + b * box * 128, &tmap_pool, hf * 64, int32_t(row_k[b] + p.S),
-                            &bars->v_full[st]);
+                tma_load_2d_kv(vs + hf * Lay::kKVHalf + b * box * 128, &tmap_pool, hf * 64,
+                               int32_t(row_k[b] + p.S), &bars->v_full[st], kv_policy);
           }
         }
         __syncwarp();
