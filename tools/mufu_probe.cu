@@ -16,6 +16,9 @@ __global__ void k(float* out, int iters, long long* clk) {
     for (int i = 0; i < 8; ++i) {
       if (OP == 0) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
       if (OP == 1) asm volatile("fma.rn.f32 %0, %0, 0f3F7FF000, 0fBA800000;" : "+f"(a[i]));
+      // packed forms: one instruction, two results (reported per instruction)
+      if (OP == 2) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(*reinterpret_cast<uint32_t*>(&a[i])));
+      if (OP == 3) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(*reinterpret_cast<uint32_t*>(&a[i])));
     }
   }
   __syncthreads();
@@ -78,6 +81,8 @@ void run(const char* name, int threads) {
 int main() {
   for (int t : {128, 256, 512}) run<0>("MUFU.EX2", t);
   for (int t : {128, 256, 512}) run<1>("FFMA", t);
+  for (int t : {128, 256, 512}) run<2>("MUFU.EX2 bf16x2 (instructions)", t);
+  for (int t : {128, 256, 512}) run<3>("MUFU.EX2 f16x2 (instructions)", t);
   run_lat<0>("FMNMX (max.f32, 2 inputs)");
   run_lat<1>("FMNMX3 (max.f32, 3 inputs)");
   run_lat<2>("FFMA2 (fma.rn.f32x2)");
