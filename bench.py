@@ -66,6 +66,8 @@ def parse():
                          "cuBLAS) around the attention, driven through the per-layer C-ABI calls")
     ap.add_argument("--store-frac", type=float, default=0.10, help="Z: DRAM store size / distinct chunks")
     ap.add_argument("--requests", type=int, default=1000, help="Z: requests in the trace")
+    ap.add_argument("--rho", default="", help="Z: comma list of loads (e.g. 0.5,0.8,0.95): extra passes with "
+                                              "Poisson arrivals at rho x the measured service rate")
     ap.add_argument("--ssd-frac", type=float, default=0.0, help="Z: SSD tier size / distinct chunks (0 = none)")
     ap.add_argument("--ssd-path", default="/tmp/pcr_ssd_tier.bin", help="Z: SSD tier file")
     ap.add_argument("--ce-frac", type=float, default=0.5, help="--load-mode hybrid: copy-engine share of the chunks")
@@ -755,13 +757,105 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def poisson_arrivals(n, rho, service_ms, seed=5):
+    """Arrival times (ms) of a Poisson process at rho x the measured service rate
+    (SURVEY 8(d) preset Z: rho in {0.5, 0.8, 0.95})."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return np.cumsum(rng.exponential(service_ms / rho, n))
+
+
+class VirtualQueue:
+    """FIFO single server in virtual time over measured service times: request i starts at
+    max(arrival_i, finish_{i-1}); its look-ahead window (Alg. 1, pending[:W]) holds the
+    next W requests that have ARRIVED by then, so the window only helps when a queue forms."""
+
+    def __init__(self, arrivals, window):
+        self.a = np.asarray(arrivals, dtype=np.float64)
+        self.w = window
+        self.t = 0.0
+
+    def start(self, i):
+        self.t = max(self.t, float(self.a[i]))
+        j = i + 1
+        while j < min(len(self.a), i + 1 + self.w) and self.a[j] <= self.t:
+            j += 1
+        return list(range(i + 1, j))
+
+    def finish(self, i, service_ms):
+        self.t += service_ms
+        return self.t - float(self.a[i])   # queueing + service
+
+
+def _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=None):
+    """One pass of the Z trace on a fresh Context (cold store).  queue=None: every request is
+    waiting from the start (saturated queue, pending = next W); else a VirtualQueue."""
+    from paper_2603_23049_b200 import MODE_OVERLAP, Context
+    geo = geometry("L8")
+    L, Hq, Hkv, d, C, S = geo["L"], geo["Hq"], geo["Hkv"], geo["d"], geo["C"], geo["S_pg"]
+    max_n = max(len(r) for r in reqs)
+    t0 = time.perf_counter()
+    ctx = Context(L, Hq, Hkv, d, C, S, cap, args.window, device=0, pool=pool, max_tokens=max_n,
+                  gather_ctas=args.gather_ctas, ssd_path=args.ssd_path if ssd_chunks else None,
+                  ssd_chunks=ssd_chunks,
+                  load_mode={"sm": 0, "ce_batch": 1, "ce_blocks": 2, "tma": 3, "hybrid": 4, "auto": 5}[args.load_mode],
+                  load_ce_fraction=args.ce_frac)
+    t_pin = time.perf_counter() - t0
+    q_d, k_d, v_d, o_d = bufs
+    cs, ls, os_ = torch.cuda.Stream(), torch.cuda.Stream(priority=-1), torch.cuda.Stream()
+    for i, (t, n) in enumerate(zip(reqs, ndoc)):
+        ctx.submit(i, t, n)
+    r = {"ttft": [], "wall": [], "ttft_q": [], "pending": [], "hits": 0, "chunks": 0, "toks": 0, "n1s": [],
+         "plan_us": [], "t_pin": t_pin}
+    launches0 = ctx.kernel_launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(cs)
+    for i in range(len(reqs)):
+        pend = queue.start(i) if queue else list(range(i + 1, min(len(reqs), i + 1 + args.window)))
+        r["pending"].append(len(pend))
+        tp = time.perf_counter()
+        plan = ctx.match_prefix(i, pend)
+        r["plan_us"].append((time.perf_counter() - tp) * 1e6)
+        n2 = plan["n2"]
+        # contiguous [L][N2][H][d] views over the front of the max-size buffers
+        q = q_d.view(-1)[: L * n2 * Hq * d].view(L, n2, Hq, d)
+        k = k_d.view(-1)[: L * n2 * Hkv * d].view(L, n2, Hkv, d)
+        v = v_d.view(-1)[: L * n2 * Hkv * d].view(L, n2, Hkv, d)
+        o = o_d.view(-1)[: L * n2 * Hq * d].view(L, n2, Hq, d)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cs)
+        ls.wait_event(a)
+        os_.wait_event(a)
+        ctx.run_prefill_ex(i, q, k, v, o, cs, ls, offload_stream=os_, mode=MODE_OVERLAP)
+        b.record(cs)
+        b.synchronize()
+        r["ttft"].append(a.elapsed_time(b))
+        r["wall"].append((time.perf_counter() - tp) * 1e3)   # host plan (+ on-demand SSD loads) + GPU
+        ctx.release(i, True)
+        if queue:
+            r["ttft_q"].append(queue.finish(i, r["wall"][-1]))
+        r["hits"] += plan["n_matched"]
+        r["chunks"] += ndoc[i] // C
+        r["toks"] += len(reqs[i])
+        r["n1s"].append(plan["n1"])
+    ev1.record(cs)
+    torch.cuda.synchronize()
+    r["total_ms"] = ev0.elapsed_time(ev1)
+    r["launches"] = ctx.kernel_launches - launches0
+    r["stats"] = ctx.stats
+    ctx.close()
+    return r
+
+
 def run_trace_z(args):
     """configs[4]: the Zipf RAG trace end to end on one GPU (look-ahead LRU + layer overlap +
     layer-wise offload of new chunks on a third stream, committed at release).  One step = one
-    request; value = trace context tokens / device time; TTFT per request from CUDA events."""
+    request; value = trace context tokens / device time; TTFT per request from CUDA events.
+    --rho r1,r2,...: after the saturated pass (which measures the mean service time), one more
+    pass per rho with Poisson arrivals at rho x that service rate (virtual-time FIFO queue; TTFT
+    then includes queueing)."""
     import torch
 
-    from paper_2603_23049_b200 import MODE_OVERLAP, Context
     from pcrgen import make_rng, randn_bf16, zipf_trace
     torch.cuda.set_device(0)
     geo = geometry("L8")
@@ -776,7 +870,6 @@ def run_trace_z(args):
     pages_req = -(-max_n // S)
     page_elems = L * Hkv * 2 * S * d
     pool = torch.empty(2 * pages_req * page_elems + page_elems, dtype=torch.int16, device="cuda")
-    t0 = time.perf_counter()
     ssd_chunks = int(args.ssd_frac * len(distinct))
     if ssd_chunks:
         # the tier file is pre-sized: refuse (loudly) rather than fill the disk
@@ -785,63 +878,35 @@ def run_trace_z(args):
         if ssd_chunks * rec > 0.8 * free:
             sys.exit(f"bench: SSD tier of {ssd_chunks} x {rec >> 20} MiB = {ssd_chunks * rec / 1e9:.0f} GB does not "
                      f"fit in 80% of the {free / 1e9:.0f} GB free under {args.ssd_path}; lower --ssd-frac or --requests")
-    ctx = Context(L, Hq, Hkv, d, C, S, cap, args.window, device=0, pool=pool, max_tokens=max_n,
-                  gather_ctas=args.gather_ctas, ssd_path=args.ssd_path if ssd_chunks else None,
-                  ssd_chunks=ssd_chunks,
-                  load_mode={"sm": 0, "ce_batch": 1, "ce_blocks": 2, "tma": 3, "hybrid": 4, "auto": 5}[args.load_mode],
-                  load_ce_fraction=args.ce_frac)
-    t_pin = time.perf_counter() - t0
     rng = make_rng(11)
-    max_n2 = max_n
-    q_d = torch.from_numpy(randn_bf16(rng, (L, max_n2, Hq, d)).view(np.int16)).cuda()
-    k_d = torch.from_numpy(randn_bf16(rng, (L, max_n2, Hkv, d)).view(np.int16)).cuda()
-    v_d = torch.from_numpy(randn_bf16(rng, (L, max_n2, Hkv, d)).view(np.int16)).cuda()
-    o_d = torch.empty_like(q_d)
-    cs, ls, os_ = torch.cuda.Stream(), torch.cuda.Stream(priority=-1), torch.cuda.Stream()
-    for i, (t, n) in enumerate(zip(reqs, ndoc)):
-        ctx.submit(i, t, n)
-    ttft, wall, hits, chunks, toks, n1s, plan_us = [], [], 0, 0, 0, [], []
-    launches0 = ctx.kernel_launches
+    bufs = tuple(torch.from_numpy(randn_bf16(rng, (L, max_n, h, d)).view(np.int16)).cuda() for h in (Hq, Hkv, Hkv))
+    bufs = bufs + (torch.empty_like(bufs[0]),)
     clocks = ClockSampler(0, pci_bus_id(torch, 0))
     clocks.start()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
     clocks.begin()
-    ev0.record(cs)
-    for i in range(len(reqs)):
-        pend = list(range(i + 1, min(len(reqs), i + 1 + args.window)))
-        tp = time.perf_counter()
-        plan = ctx.match_prefix(i, pend)
-        plan_us.append((time.perf_counter() - tp) * 1e6)
-        n2 = plan["n2"]
-        # contiguous [L][N2][H][d] views over the front of the max-size buffers
-        q = q_d.view(-1)[: L * n2 * Hq * d].view(L, n2, Hq, d)
-        k = k_d.view(-1)[: L * n2 * Hkv * d].view(L, n2, Hkv, d)
-        v = v_d.view(-1)[: L * n2 * Hkv * d].view(L, n2, Hkv, d)
-        o = o_d.view(-1)[: L * n2 * Hq * d].view(L, n2, Hq, d)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(cs)
-        ls.wait_event(a)
-        os_.wait_event(a)
-        ctx.run_prefill_ex(i, q, k, v, o, cs, ls, offload_stream=os_, mode=MODE_OVERLAP)
-        b.record(cs)
-        b.synchronize()
-        ttft.append(a.elapsed_time(b))
-        wall.append((time.perf_counter() - tp) * 1e3)   # host plan (+ on-demand SSD loads) + GPU
-        ctx.release(i, True)
-        hits += plan["n_matched"]
-        chunks += ndoc[i] // C
-        toks += len(reqs[i])
-        n1s.append(plan["n1"])
-    ev1.record(cs)
-    torch.cuda.synchronize()
-    total_ms = ev0.elapsed_time(ev1)
+    r = _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs)
+    rhos = [float(x) for x in args.rho.split(",")] if args.rho else []
+    service_ms = float(np.mean(r["wall"]))
+    poisson = []
+    for rho in rhos:
+        arr = poisson_arrivals(len(reqs), rho, service_ms)
+        rq = _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=VirtualQueue(arr, args.window))
+        tq = np.array(rq["ttft_q"])
+        poisson.append({
+            "rho": rho, "arrival_rate_per_s": 1e3 * rho / service_ms,
+            "ttft_ms_mean": float(tq.mean()), "ttft_ms_p50": float(np.percentile(tq, 50)),
+            "ttft_ms_p95": float(np.percentile(tq, 95)), "ttft_ms_p99": float(np.percentile(tq, 99)),
+            "service_ms_mean": float(np.mean(rq["wall"])), "device_ttft_ms_mean": float(np.mean(rq["ttft"])),
+            "mean_pending": float(np.mean(rq["pending"])), "chunk_hit_ratio": rq["hits"] / max(1, rq["chunks"]),
+        })
     clk = clocks.stop()
-    tt = np.array(ttft)
+    tt = np.array(r["ttft"])
+    wall = r["wall"]
     line = {
         "metric": "Z trace: context tokens/s over 1000 Zipf RAG requests (TTFT per request in ttft_ms_*)",
-        "value": toks / (total_ms * 1e-3), "unit": "tokens/s", "n_gpus": 1, "steps": len(reqs), "warmup": 0,
-        "ms_per_step": total_ms / len(reqs), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "value": r["toks"] / (r["total_ms"] * 1e-3), "unit": "tokens/s", "n_gpus": 1, "steps": len(reqs),
+        "warmup": 0, "ms_per_step": r["total_ms"] / len(reqs), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded Zipf(1.0) corpus of 1000 docs x 4-16 chunks, 2 docs + "
                                    "128-256 query tokens per request; random bf16 KV)",
         "config": {"workload": f"Z: L8 shape, W={args.window}, store={cap} chunks "
@@ -849,13 +914,18 @@ def run_trace_z(args):
                                f"offload on",
                    "requests": len(reqs), "window": args.window, "store_chunks": cap, "ssd_chunks": ssd_chunks},
         "ttft_wall_ms_mean": float(np.mean(wall)), "ttft_wall_ms_p95": float(np.percentile(wall, 95)),
-        "tier_stats": ctx.stats,
+        "tier_stats": r["stats"],
         "ttft_ms_mean": float(tt.mean()), "ttft_ms_p50": float(np.percentile(tt, 50)),
         "ttft_ms_p95": float(np.percentile(tt, 95)), "ttft_ms_p99": float(np.percentile(tt, 99)),
-        "chunk_hit_ratio": hits / max(1, chunks), "mean_n1_tokens": float(np.mean(n1s)),
-        "match_prefix_us_p50": float(np.percentile(plan_us, 50)), "store_pin_s": t_pin,
-        "gpu_launches": ctx.kernel_launches - launches0, "clocks": clk,
+        "chunk_hit_ratio": r["hits"] / max(1, r["chunks"]), "mean_n1_tokens": float(np.mean(r["n1s"])),
+        "match_prefix_us_p50": float(np.percentile(r["plan_us"], 50)), "store_pin_s": r["t_pin"],
+        "gpu_launches": r["launches"], "clocks": clk,
     }
+    if poisson:
+        line["poisson"] = poisson
+        line["poisson_note"] = ("saturated pass first (every request waiting from t=0; its mean wall service "
+                                "time sets the rate), then one cold-store pass per rho with Poisson arrivals; "
+                                "ttft_ms_* there = queueing + service (virtual-time FIFO over measured service)")
     print(json.dumps(line), flush=True)
 
 

@@ -3,13 +3,18 @@
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
 OUT=gpurun_out/workloads.jsonl; [ -n "$APPEND" ] || : > $OUT
-# SECTIONS (default all): z ssd f3 l70 t
+# SECTIONS (default all but zq): z zq ssd f3 l70 t
 rm -f /tmp/pcr_ssd_tier.bin   # a leftover tier file from an interrupted run
 df -h /tmp | tail -1 > gpurun_out/disk.txt
 S=" ${SECTIONS:-z ssd f3 l70 t} "
 if [[ $S == *" z "* ]]; then
 for W in 0 4; do
   timeout 900 python bench.py --workload Z --window $W >> $OUT 2>> gpurun_out/workloads.err; echo "Z W=$W rc=$?"
+done
+fi
+if [[ $S == *" zq "* ]]; then   # Poisson arrivals at rho x the measured service rate
+for W in 0 4; do
+  timeout 900 python bench.py --workload Z --window $W --rho 0.5,0.8,0.95 >> $OUT 2>> gpurun_out/workloads.err; echo "Z rho W=$W rc=$?"
 done
 fi
 if [[ $S == *" ssd "* ]]; then
@@ -35,5 +40,9 @@ for l in open("gpurun_out/workloads.jsonl"):
     j=json.loads(l)
     keep={k:j.get(k) for k in ("value","ttft_ms","ttft_ms_mean","ttft_ms_p95","ttft_wall_ms_mean","chunk_hit_ratio","gather_ms_per_layer","attn_ms_per_layer","tier_stats")}
     print(j["config"]["workload"][:110], json.dumps(keep))
+    for pz in j.get("poisson", []):
+        print("   rho %.2f: TTFT mean %.2f p95 %.2f p99 %.2f ms (queue+service), service %.2f, pending %.2f, hit %.3f" % (
+            pz["rho"], pz["ttft_ms_mean"], pz["ttft_ms_p95"], pz["ttft_ms_p99"], pz["service_ms_mean"],
+            pz["mean_pending"], pz["chunk_hit_ratio"]))
 PY
 tail -5 gpurun_out/workloads.err
