@@ -66,6 +66,11 @@ def parse():
                          "cuBLAS) around the attention, driven through the per-layer C-ABI calls")
     ap.add_argument("--store-frac", type=float, default=0.10, help="Z: DRAM store size / distinct chunks")
     ap.add_argument("--requests", type=int, default=1000, help="Z: requests in the trace")
+    ap.add_argument("--rho-service-ms", type=float, default=0.0,
+                    help="Z: service time (ms) that rho refers to (0 = this run's saturated-pass mean; set it "
+                         "to compare configurations at the same arrival rate)")
+    ap.add_argument("--no-reuse", action="store_true",
+                    help="Z: nothing cacheable (every request recomputes its context: the no-PCR baseline)")
     ap.add_argument("--rho", default="", help="Z: comma list of loads (e.g. 0.5,0.8,0.95): extra passes with "
                                               "Poisson arrivals at rho x the measured service rate")
     ap.add_argument("--ssd-frac", type=float, default=0.0, help="Z: SSD tier size / distinct chunks (0 = none)")
@@ -786,9 +791,52 @@ class VirtualQueue:
         return self.t - float(self.a[i])   # queueing + service
 
 
-def _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=None):
+def _z_layer_body(torch, geo, max_n):
+    """f3 stand-in layer body for the Z trace (same shapes as run_ours --layer-body)."""
+    dm, dff = 4096, 14336
+    hq, hkv, d = geo["Hq"], geo["Hkv"], geo["d"]
+    g = torch.Generator(device="cuda").manual_seed(5)
+    wgt = lambda i, o: (torch.randn(i, o, device="cuda", generator=g, dtype=torch.bfloat16) / i ** 0.5)  # noqa: E731
+    return dict(wq=wgt(dm, hq * d), wk=wgt(dm, hkv * d), wv=wgt(dm, hkv * d), wo=wgt(hq * d, dm),
+                wg=wgt(dm, dff), wu=wgt(dm, dff), wd=wgt(dff, dm),
+                x=torch.randn(max_n, dm, device="cuda", generator=g, dtype=torch.bfloat16),
+                ev_ld=[torch.cuda.Event() for _ in range(geo["L"])],
+                ev_at=[torch.cuda.Event() for _ in range(geo["L"])])
+
+
+def _z_request_with_body(torch, ctx, rid, n2, geo, body, out, cs, ls, os_):
+    """One request through the per-layer C-ABI calls with the layer body around the attention:
+    load(l) on ls || QKV projection on cs; attention(l); offload(l) on os_ || O projection + MLP.
+    Only the N2 computed tokens go through the GEMMs (the reused prefix needs no hidden states)."""
+    L, hq, hkv, d = geo["L"], geo["Hq"], geo["Hkv"], geo["d"]
+    b = body
+    x = b["x"][:n2]
+    ls.wait_stream(cs)
+    os_.wait_stream(cs)
+    for l in range(L):
+        ctx.load_layer_kv(rid, l, ls)
+        b["ev_ld"][l].record(ls)
+        with torch.cuda.stream(cs):
+            qd = (x @ b["wq"]).view(n2, hq, d)
+            kd = (x @ b["wk"]).view(n2, hkv, d)
+            vd = (x @ b["wv"]).view(n2, hkv, d)
+            cs.wait_event(b["ev_ld"][l])
+            ctx.prefill_attn_layer(rid, l, qd.view(torch.int16), kd.view(torch.int16), vd.view(torch.int16),
+                                   out[l], cs)
+            b["ev_at"][l].record(cs)
+            os_.wait_event(b["ev_at"][l])
+            ctx.offload_layer_kv(rid, l, os_)
+            x = x + out[l].view(torch.bfloat16).view(n2, hq * d) @ b["wo"]
+            x = x + (torch.nn.functional.silu(x @ b["wg"]) * (x @ b["wu"])) @ b["wd"]
+    cs.wait_stream(ls)
+    cs.wait_stream(os_)
+
+
+def _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=None, body=None):
     """One pass of the Z trace on a fresh Context (cold store).  queue=None: every request is
-    waiting from the start (saturated queue, pending = next W); else a VirtualQueue."""
+    waiting from the start (saturated queue, pending = next W); else a VirtualQueue.
+    body: the f3 layer body around the attention (per-layer calls); args.no_reuse: nothing is
+    cacheable (every request recomputes its whole context: the no-PCR baseline)."""
     from paper_2603_23049_b200 import MODE_OVERLAP, Context
     geo = geometry("L8")
     L, Hq, Hkv, d, C, S = geo["L"], geo["Hq"], geo["Hkv"], geo["d"], geo["C"], geo["S_pg"]
@@ -803,7 +851,7 @@ def _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=None):
     q_d, k_d, v_d, o_d = bufs
     cs, ls, os_ = torch.cuda.Stream(), torch.cuda.Stream(priority=-1), torch.cuda.Stream()
     for i, (t, n) in enumerate(zip(reqs, ndoc)):
-        ctx.submit(i, t, n)
+        ctx.submit(i, t, 0 if args.no_reuse else n)
     r = {"ttft": [], "wall": [], "ttft_q": [], "pending": [], "hits": 0, "chunks": 0, "toks": 0, "n1s": [],
          "plan_us": [], "t_pin": t_pin}
     launches0 = ctx.kernel_launches
@@ -826,7 +874,10 @@ def _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=None):
         a.record(cs)
         ls.wait_event(a)
         os_.wait_event(a)
-        ctx.run_prefill_ex(i, q, k, v, o, cs, ls, offload_stream=os_, mode=MODE_OVERLAP)
+        if body is not None:
+            _z_request_with_body(torch, ctx, i, n2, geometry("L8"), body, o, cs, ls, os_)
+        else:
+            ctx.run_prefill_ex(i, q, k, v, o, cs, ls, offload_stream=os_, mode=MODE_OVERLAP)
         b.record(cs)
         b.synchronize()
         r["ttft"].append(a.elapsed_time(b))
@@ -881,19 +932,21 @@ def run_trace_z(args):
     rng = make_rng(11)
     bufs = tuple(torch.from_numpy(randn_bf16(rng, (L, max_n, h, d)).view(np.int16)).cuda() for h in (Hq, Hkv, Hkv))
     bufs = bufs + (torch.empty_like(bufs[0]),)
+    body = _z_layer_body(torch, geo, max_n) if args.layer_body else None
     clocks = ClockSampler(0, pci_bus_id(torch, 0))
     clocks.start()
     clocks.begin()
-    r = _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs)
+    r = _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, body=body)
     rhos = [float(x) for x in args.rho.split(",")] if args.rho else []
-    service_ms = float(np.mean(r["wall"]))
+    service_ms = args.rho_service_ms or float(np.mean(r["wall"]))
     poisson = []
     for rho in rhos:
         arr = poisson_arrivals(len(reqs), rho, service_ms)
-        rq = _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=VirtualQueue(arr, args.window))
+        rq = _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=VirtualQueue(arr, args.window),
+                     body=body)
         tq = np.array(rq["ttft_q"])
         poisson.append({
-            "rho": rho, "arrival_rate_per_s": 1e3 * rho / service_ms,
+            "rho": rho, "rho_service_ms": service_ms, "arrival_rate_per_s": 1e3 * rho / service_ms,
             "ttft_ms_mean": float(tq.mean()), "ttft_ms_p50": float(np.percentile(tq, 50)),
             "ttft_ms_p95": float(np.percentile(tq, 95)), "ttft_ms_p99": float(np.percentile(tq, 99)),
             "service_ms_mean": float(np.mean(rq["wall"])), "device_ttft_ms_mean": float(np.mean(rq["ttft"])),
@@ -911,7 +964,8 @@ def run_trace_z(args):
                                    "128-256 query tokens per request; random bf16 KV)",
         "config": {"workload": f"Z: L8 shape, W={args.window}, store={cap} chunks "
                                f"({args.store_frac:.0%} of {len(distinct)} distinct), ssd={ssd_chunks} chunks, "
-                               f"offload on",
+                               f"offload on" + (", +layer body (f3)" if body is not None else "")
+                               + (", NO REUSE (full recompute baseline)" if args.no_reuse else ""),
                    "requests": len(reqs), "window": args.window, "store_chunks": cap, "ssd_chunks": ssd_chunks},
         "ttft_wall_ms_mean": float(np.mean(wall)), "ttft_wall_ms_p95": float(np.percentile(wall, 95)),
         "tier_stats": r["stats"],

@@ -12,10 +12,15 @@ for W in 0 4; do
   timeout 900 python bench.py --workload Z --window $W >> $OUT 2>> gpurun_out/workloads.err; echo "Z W=$W rc=$?"
 done
 fi
-if [[ $S == *" zq "* ]]; then   # Poisson arrivals at rho x the measured service rate
-for W in 0 4; do
-  timeout 900 python bench.py --workload Z --window $W --rho 0.5,0.8,0.95 >> $OUT 2>> gpurun_out/workloads.err; echo "Z rho W=$W rc=$?"
-done
+if [[ $S == *" zq "* ]]; then
+# Poisson arrivals with the f3 layer body, so a prefix hit saves real recompute:
+# PCR with W=4, with W=0, and the no-reuse baseline, all at the SAME arrival rates (rho x the
+# W=4 run's mean service time).
+ZQ="--workload Z --layer-body --requests ${ZQ_REQ:-300}"
+timeout 900 python bench.py $ZQ --window 4 --rho 0.5,0.8,0.95 >> $OUT 2>> gpurun_out/workloads.err; echo "Zq W=4 rc=$?"
+SVC=$(tail -1 $OUT | python -c "import json,sys; print(json.loads(sys.stdin.read())['ttft_wall_ms_mean'])")
+timeout 900 python bench.py $ZQ --window 0 --rho 0.5,0.8,0.95 --rho-service-ms $SVC >> $OUT 2>> gpurun_out/workloads.err; echo "Zq W=0 rc=$?"
+timeout 900 python bench.py $ZQ --window 0 --no-reuse --rho 0.5,0.8,0.95 --rho-service-ms $SVC >> $OUT 2>> gpurun_out/workloads.err; echo "Zq no-reuse rc=$?"
 fi
 if [[ $S == *" ssd "* ]]; then
 timeout 900 python bench.py --workload Z --window 4 --requests 300 --store-frac 0.03 --ssd-frac 0.25 >> $OUT 2>> gpurun_out/workloads.err; echo "Z ssd rc=$?"
