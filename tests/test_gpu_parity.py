@@ -533,3 +533,28 @@ def test_context_split_partials_merge_to_oracle(P, load_mode, kind):
         assert r_l2 <= TOL_REL_L2 and m <= TOL_MAX_ABS, (l, r_l2, m)
     for rig, _ in rigs:
         rig.ctx.release(1, False)
+
+
+_PDL_SCRIPT = """
+import sys, zlib
+sys.path.insert(0, {root!r})
+from tests.test_gpu_parity import _single_request
+rig, plan, q, k, v, out = _single_request("iid", 3, 32, 8, 128, 256, 64, 1024, 130, seed=5)
+print("CRC", zlib.crc32(out.tobytes()))
+"""
+
+
+def test_programmatic_dependent_launch_off_is_bitwise_identical():
+    """PCR_PDL=0 (plain stream-ordered launches) gives the same bytes as the default PDL chain
+    append -> attention -> split-KV combine (4 splits at this shape)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    _, _, _, _, _, out = _single_request("iid", 3, 32, 8, 128, 256, 64, 1024, 130, seed=5)
+    env = dict(os.environ, PCR_PDL="0")
+    res = subprocess.run([sys.executable, "-c", _PDL_SCRIPT.format(root=root)], env=env, capture_output=True,
+                         text=True, timeout=300, cwd=root)
+    assert res.returncode == 0, res.stderr[-2000:]
+    crc = int([ln for ln in res.stdout.splitlines() if ln.startswith("CRC")][0].split()[1])
+    assert crc == zlib.crc32(out.tobytes())
