@@ -660,17 +660,35 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
   for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < n; u += int64_t(gridDim.x) * blockDim.x) {
     const int64_t row = u / kVec;
     const int c8 = int(u % kVec) * 8;
+    // The loads of a group of 4 splits are issued before any of them is used (the loop is
+    // latency-bound otherwise); the accumulation order over s is unchanged.
     float mx = -INFINITY;
+#pragma unroll 8
     for (int s = 0; s < n_splits; ++s) mx = fmaxf(mx, ws_lse[s * lse_stride + row]);
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, wsum = 0.f;
     if (mx != -INFINITY) {
-      for (int s = 0; s < n_splits; ++s) {
-        const float w = ex2(ws_lse[s * lse_stride + row] - mx);
-        wsum += w;
-        const float4* src = reinterpret_cast<const float4*>(ws_o + s * o_stride + row * D + c8);
-        const float4 a = src[0], b = src[1];
-        acc[0] += w * a.x; acc[1] += w * a.y; acc[2] += w * a.z; acc[3] += w * a.w;
-        acc[4] += w * b.x; acc[5] += w * b.y; acc[6] += w * b.z; acc[7] += w * b.w;
+      for (int s0 = 0; s0 < n_splits; s0 += 4) {
+        float lse[4];
+        float4 a[4], b[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (s0 + k < n_splits) {
+            const int s = s0 + k;
+            lse[k] = ws_lse[s * lse_stride + row];
+            const float4* src = reinterpret_cast<const float4*>(ws_o + s * o_stride + row * D + c8);
+            a[k] = src[0];
+            b[k] = src[1];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (s0 + k < n_splits) {
+            const float w = ex2(lse[k] - mx);
+            wsum += w;
+            acc[0] += w * a[k].x; acc[1] += w * a[k].y; acc[2] += w * a[k].z; acc[3] += w * a[k].w;
+            acc[4] += w * b[k].x; acc[5] += w * b[k].y; acc[6] += w * b[k].z; acc[7] += w * b[k].w;
+          }
+        }
       }
     }
     const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
