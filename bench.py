@@ -43,6 +43,9 @@ WORKLOADS = {
 }
 
 
+LOAD_MODES = {"sm": 0, "ce_runs": 1, "ce_blocks": 2, "tma": 3, "hybrid": 4}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -83,8 +86,10 @@ def parse():
                     help="single process doing the per-GPU work of rank 0 of a P-GPU KV-head-sharded run "
                          "(its head slice of the load and attention, no all-gather): a one-GPU estimate of "
                          "the per-rank critical path at P GPUs")
-    ap.add_argument("--load-mode", default="auto", choices=["sm", "ce_batch", "ce_blocks", "tma", "hybrid", "auto"],
-                    help="a2 implementation: sm_100a gather kernel, or the paper's copy-engine paths")
+    ap.add_argument("--load-mode", default="sm", choices=list(LOAD_MODES),
+                    help="a2 implementation: sm_100a 16-byte gather kernel (default), or the f4 baselines: "
+                         "copy engines with one cudaMemcpyAsync per merged run (ce_runs) or per page image "
+                         "(ce_blocks), TMA bulk copies, or the hybrid")
     return ap.parse_args()
 
 
@@ -376,7 +381,7 @@ def run_ours(args):
     page_elems = L * hkv * 2 * S * d
     pool = torch.empty(n_pool_pages * page_elems, dtype=torch.int16, device="cuda")
     store_chunks = n_doc // C + 4
-    load_mode = {"sm": 0, "ce_batch": 1, "ce_blocks": 2, "tma": 3, "hybrid": 4, "auto": 5}[args.load_mode]
+    load_mode = LOAD_MODES[args.load_mode]
     ctx = Context(L, Hq, Hkv, d, C, S, store_chunks, 4, device=local, pool=pool, rank=rank, world=shard,
                   gather_ctas=args.gather_ctas, load_mode=load_mode, load_ce_fraction=args.ce_frac,
                   shard_mode=1 if ctx_split else 0)
@@ -576,28 +581,7 @@ def run_ours(args):
         sync_ms = []
         offload_ms = None
 
-    # When the copy engines carried the timed loads (auto on long runs), time the SM gather
-    # kernel on the same steps too (same events, load stream busy time per layer).
     sm_leg = None
-    if ce_layers and N1 and body is None:
-        ctx.set_load_mode(0)
-        for _ in range(2):
-            step(q_d, k_d, v_d, out_d)
-        sm_ms, sm_ld = [], []
-        for _ in range(max(5, min(args.steps, 15))):
-            e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            l_a, l_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e_a.record(cs)
-            ls.wait_event(e_a)
-            step(q_d, k_d, v_d, out_d, load_events=(l_a, l_b))
-            e_b.record(cs)
-            e_b.synchronize()
-            sm_ms.append(e_a.elapsed_time(e_b))
-            sm_ld.append(l_a.elapsed_time(l_b))
-        ctx.set_load_mode(load_mode, args.ce_frac)
-        sm_leg = {"ttft_ms": statistics.median(sm_ms), "avg_launch_ms": float(np.mean(sm_ld)) / L,
-                  "steps": len(sm_ms)}
-
     # e2e: the same step through the C-ABI with HOST buffers: q/k/v/out are page-locked host
     # tensors handed to pcr_run_prefill_ex(host_io=1); the library stages each layer's inputs
     # (H2D) and returns its output (D2H) on its own copy streams, overlapped with the pipeline.
@@ -685,9 +669,9 @@ def run_ours(args):
     except Exception:
         ncu_t = {}
     if ce_layers:
-        load_kernel = (f"kv_load on the copy engines: one cudaMemcpyBatchAsync per layer, "
-                       f"{ce_copies_per_layer:.0f} runs of {load_bytes / ce_copies_per_layer / 2**10:.0f} KiB "
-                       f"(load_mode {args.load_mode})")
+        load_kernel = (f"kv_load on the copy engines (f4 baseline, load_mode {args.load_mode}): "
+                       f"{ce_copies_per_layer:.0f} cudaMemcpyAsync per layer of "
+                       f"{load_bytes / ce_copies_per_layer / 2**10:.0f} KiB")
     else:
         load_kernel = {4: f"kv_gather + copy engines ({args.ce_frac:.2f} of the chunks)", 3: "kv_gather_tma"}.get(
             load_mode, "kv_gather")
@@ -845,7 +829,7 @@ def _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=None, bo
     ctx = Context(L, Hq, Hkv, d, C, S, cap, args.window, device=0, pool=pool, max_tokens=max_n,
                   gather_ctas=args.gather_ctas, ssd_path=args.ssd_path if ssd_chunks else None,
                   ssd_chunks=ssd_chunks,
-                  load_mode={"sm": 0, "ce_batch": 1, "ce_blocks": 2, "tma": 3, "hybrid": 4, "auto": 5}[args.load_mode],
+                  load_mode=LOAD_MODES[args.load_mode],
                   load_ce_fraction=args.ce_frac)
     t_pin = time.perf_counter() - t0
     q_d, k_d, v_d, o_d = bufs

@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define PCR_ABI_VERSION 5
+#define PCR_ABI_VERSION 6
 
 typedef struct pcr_ctx pcr_ctx;
 
@@ -86,21 +86,17 @@ typedef struct pcr_config {
   int32_t max_inflight;  /* requests planned but not yet released; 0 -> 4 */
   int32_t max_tokens;    /* max tokens of one request; 0 -> pool capacity in tokens */
   int32_t gather_ctas;   /* CTAs of the host->HBM gather kernel; 0 -> library default */
-  int32_t load_mode;     /* a2 implementation: 0 = sm_100a 16-byte gather kernel (default);
-                            baselines of the paper's copy path (fig:api), no SMs used:
-                            1 = copy engine, one cudaMemcpyBatchAsync per layer over all page
-                            segments; 2 = copy engine, one cudaMemcpyAsync per page segment;
+  int32_t load_mode;     /* a2 implementation: 0 = sm_100a 16-byte gather kernel (default; the
+                            north_star mover: coalesced 16-byte loads from the mapped host store).
+                            f4 baselines of the paper's copy path (fig:api), no SMs used:
+                            1 = copy engines, one cudaMemcpyAsync per run (adjacent page images of
+                            a chunk whose pool pages are also adjacent merge into one run);
+                            2 = copy engines, one cudaMemcpyAsync per page image (block by block);
                             3 = experiment: TMA bulk copies host -> smem -> pool page;
-                            4 = hybrid: the copy engines move the first load_ce_fraction of the
-                            matched chunks (one cudaMemcpyBatchAsync on a library stream) while
-                            the gather kernel moves the rest, both over the same host link;
-                            5 = auto: per request, mode 1 when the chunk-layer copies merge into
-                            runs of >= 128 KiB on average (consecutive pool pages of a chunk are
-                            one run), else mode 0 — the copy engines reach ~98% of the host
-                            link on long runs, the SM gather ~90% at any run length
-                            (profiles/r01_ce_probe.txt); the f1 offload of the
-                            reserved chunks makes the same choice (copy-engine D2H batch or
-                            the SM scatter kernel).  Modes 0-4 offload with the SM kernel. */
+                            4 = hybrid: the copy engines (one cudaMemcpyAsync per run, on a library
+                            stream) move the first load_ce_fraction of the matched chunks while
+                            the gather kernel moves the rest, both over the same host link.
+                            The f1 offload always uses the SM scatter kernel. */
   float load_ce_fraction;  /* load_mode 4 only: share of the chunks for the copy engines, [0, 1] */
   /* SSD tier (§8 f2): a file of ssd_chunks chunk records behind the DRAM store.
    * Committed chunks are written back asynchronously; chunks of requests in the
@@ -211,10 +207,9 @@ typedef struct pcr_stats {
   int64_t ssd_evictions;    /* SSD records overwritten (LRU) */
   int64_t dram_evictions;   /* DRAM leaves evicted */
   int64_t ssd_bytes_read, ssd_bytes_written;
-  int64_t ce_copies;        /* copy-engine copies enqueued for a2 loads (load_mode 1/2/4/5) */
-  int64_t ce_layer_loads;   /* layer loads done by the copy engines (load_mode 1/2/5) */
-  int64_t sm_layer_loads;   /* layer loads done by the SM gather kernel (load_mode 0/3/4/5) */
-  int64_t ce_offload_layers; /* layer offloads done by the copy engines (load_mode 5, long runs) */
+  int64_t ce_copies;        /* copy-engine copies (cudaMemcpyAsync) enqueued for a2 loads (load_mode 1/2/4) */
+  int64_t ce_layer_loads;   /* layer loads done by the copy engines alone (load_mode 1/2) */
+  int64_t sm_layer_loads;   /* layer loads with a kernel moving prefix KV (load_mode 0/3/4) */
 } pcr_stats;
 pcr_status pcr_get_stats(const pcr_ctx* ctx, pcr_stats* out);
 
@@ -231,7 +226,7 @@ pcr_status pcr_blake2b(const void* data, int64_t n, const void* key, int32_t key
  * pinned host store into the request's pool pages:
  *   pool[layer][pages[t/S_pg]][h][kv][t%S_pg][:] = store[slots[t/C]][layer][h][kv][t%C][:]
  * for t < n1.  An sm_100a kernel reads the mapped host memory over PCIe with 16-byte
- * loads and writes 16-byte stores into the pool pages, or (load_mode 1/2/5) the copy engines.
+ * loads and writes 16-byte stores into the pool pages, or (load_mode 1/2) the copy engines.
  * The first device call of a request also uploads its page/slot tables on its stream. */
 pcr_status pcr_load_layer_kv(pcr_ctx* ctx, int64_t req_id, int32_t layer, void* load_stream);
 
@@ -310,10 +305,13 @@ typedef struct pcr_run_opts {
   int32_t host_io;         /* 1: q_all/k_all/v_all/out_all are PAGE-LOCKED HOST buffers (cudaHostAlloc /
                             * cudaHostRegister; PCR_E_INVAL otherwise).  Layer l's q/k/v are copied
                             * into a library-owned ring of device staging buffers (as many layers
-                            * as fit 512 MiB, >= 2) on the load stream just ahead of layer l's KV
-                            * load, and its output is copied back on an internal stream right after
-                            * its attention, so the host I/O overlaps the layer pipeline.  Not
-                            * combinable with gathered_all. */
+                            * as fit 512 MiB, >= 2) on the load stream by layer l's gather launch
+                            * itself when the buffers are device-mapped (else one cudaMemcpyAsync
+                            * each, just ahead of the load), and its output is copied back on an
+                            * internal stream right after its attention, so the host I/O overlaps
+                            * the layer pipeline.  Not combinable with gathered_all.  The staging
+                            * ring is per context: host_io calls of one ctx must not overlap in
+                            * time (synchronise the compute stream between them). */
   int32_t io_ring_layers;  /* host_io staging ring depth in layers: 0 = as many as fit 512 MiB
                             * (clamped to [2, L]); otherwise clamped to [2, L]. */
   float* partial_all;      /* shard_mode 1 (required there, NULL otherwise): device fp32
@@ -339,8 +337,8 @@ pcr_status pcr_merge_partials(pcr_ctx* ctx, const float* gathered, int32_t n_par
                               void* stream);
 
 /* Switch the a2 load path (pcr_config.load_mode / load_ce_fraction, same ranges) for layer loads
- * enqueued after this call; call it between requests (a load_mode 5 request keeps the choice it
- * made at its first load).  PCR_E_INVAL on an out-of-range value (nothing changes). */
+ * enqueued after this call; call it between requests.  PCR_E_INVAL on an out-of-range value
+ * (nothing changes). */
 pcr_status pcr_set_load_mode(pcr_ctx* ctx, int32_t load_mode, float load_ce_fraction);
 
 #ifdef __cplusplus

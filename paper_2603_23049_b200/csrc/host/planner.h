@@ -74,8 +74,6 @@ struct Request {
   std::vector<int32_t> matched, reserved;  // node indices
   Plan plan;
   bool tables_uploaded = false;
-  int8_t load_auto = -1;      // load_mode 5: -1 undecided, 0 SM gather, 1 copy engines (runtime-owned)
-  int8_t offload_auto = -1;   // the same choice for the offload of the reserved chunks
   // shard_mode 1 (context split), runtime-owned: this rank's matched / reserved chunks, virtual
   // page-table length, and whether it holds the suffix keys
   int32_t ctx_n_own = 0, ctx_n_res_own = 0, ctx_n_vpages = 0;

@@ -17,11 +17,22 @@ struct KvGeom {
 // pages the chunk fills), so a chunk-layer with consecutive pool pages is one contiguous run.
 // pcr_store_write/read convert from/to the API layout [L][Hkv][2][C][d].
 
+// Up to kMax linear copies of n16[i] 16-byte units, src[i] -> dst[i] (16-byte aligned), that ride
+// in the same gather launch (host_io: the layer's q/k/v from mapped page-locked host memory).
+struct LinearCopies {
+  static constexpr int kMax = 3;
+  int32_t n;
+  const uint4* src[kMax];
+  uint4* dst[kMax];
+  int64_t n16[kMax];
+};
+
 // a2: pool[layer][pages[t/S]][h][kv][t%S] = store[slots[t/C]][layer][(t%C)/S][h][kv][t%S], t < n_matched*C.
 // `store` is the device (UVA) view of the mapped pinned host store; 16-byte loads/stores.
+// `lin` (nullable): extra linear copies done by the same launch.
 cudaError_t launch_kv_gather(const void* store, void* pool, const int32_t* d_slots, const int32_t* d_pages,
                              int32_t n_matched, int32_t layer, const KvGeom& g, int32_t target_ctas,
-                             cudaStream_t stream);
+                             cudaStream_t stream, const LinearCopies* lin = nullptr);
 
 // a2 variant (load_mode 3, experiment): same copy with TMA bulk copies (host -> smem -> pool).
 cudaError_t launch_kv_gather_tma(const void* store, void* pool, const int32_t* d_slots, const int32_t* d_pages,

@@ -1,10 +1,11 @@
 // a2 kv_gather (host store -> HBM pool) and a3 kv_append (suffix K/V -> pool).
 //
-// "To efficiently copy KV cache from a CPU chunk to multiple non-consecutive GPU memory
-// blocks, we leverage ... cudaMemcpyBatchAsync()".  On B200 the copy is an SM kernel instead:
+// the paper copies a CPU chunk into many non-consecutive GPU blocks with a batched
+// copy-engine API.  On B200 the copy is an SM kernel instead:
 // every thread streams 16-byte vectors straight out of the mapped pinned host store over PCIe
 // Gen5 (zero-copy, ld.global.cs) and writes them, 16 bytes at a time, into the pool pages of
-// the request.  Measured on this pool's B200 (tools/h2d_probe.cu): 8+ CTAs x 256 threads with
+// the request.  The same launch can also carry a few linear host->device copies (the layer's
+// q/k/v inputs on the host_io path), so one kernel per layer moves everything the layer needs.  Measured on this pool's B200 (tools/h2d_probe.cu): 8+ CTAs x 256 threads with
 // 4 loads in flight per thread reach 51.2 GB/s = 92% of the copy engine's 55.6 GB/s, so the
 // gather needs only a handful of SMs and leaves the rest to the concurrent attention.
 #include <algorithm>
@@ -51,29 +52,51 @@ __device__ __forceinline__ void segment_addrs(int64_t seg, int32_t chunk0, int32
   pool16 = (int64_t(layer) * g.n_pool_pages + page) * page16 + hk * seg16;
 }
 
+// Segments [0, n_lin_seg) are pieces of the linear copies (each copy cut into seg16-unit pieces,
+// the last one ragged), the rest are page segments.  The linear copies come first: the layer's
+// inputs are needed by the attention as soon as its KV has landed.
 __global__ void __launch_bounds__(kThreads, 6) kv_gather_kernel(const uint4* __restrict__ store,
                                                              uint4* __restrict__ pool,
                                                              const int32_t* __restrict__ slots,
                                                              const int32_t* __restrict__ pages, int32_t n_chunks,
                                                              int32_t layer, KvGeom g, int32_t row16_log2,
-                                                             int32_t ppc_log2) {
+                                                             int32_t ppc_log2, LinearCopies lin) {
   const int lane = threadIdx.x & 31;
-  const int64_t n_seg = (int64_t(n_chunks) * g.Hkv * 2) << ppc_log2;
   const int32_t seg16 = g.S << row16_log2;
+  int64_t lin_seg[LinearCopies::kMax + 1];
+  lin_seg[0] = 0;
+#pragma unroll
+  for (int i = 0; i < LinearCopies::kMax; ++i)
+    lin_seg[i + 1] = lin_seg[i] + (i < lin.n ? (lin.n16[i] + seg16 - 1) / seg16 : 0);
+  const int64_t n_lin = lin_seg[LinearCopies::kMax];
+  const int64_t n_seg = n_lin + ((int64_t(n_chunks) * g.Hkv * 2) << ppc_log2);
   const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
   for (int64_t seg = int64_t(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5); seg < n_seg; seg += warps) {
-    int64_t s16, p16;
-    segment_addrs(seg, 0, layer, g, ppc_log2, row16_log2, slots, pages, s16, p16);
-    const uint4* src = store + s16;
-    uint4* dst = pool + p16;
-    for (int32_t base = lane; base < seg16; base += 32 * kUnroll) {
+    const uint4* src;
+    uint4* dst;
+    int64_t len16 = seg16;
+    if (seg < n_lin) {
+      int i = 0;
+#pragma unroll
+      for (int j = 1; j < LinearCopies::kMax; ++j) i += seg >= lin_seg[j];
+      const int64_t off = (seg - lin_seg[i]) * seg16;
+      src = lin.src[i] + off;
+      dst = lin.dst[i] + off;
+      len16 = min(int64_t(seg16), lin.n16[i] - off);
+    } else {
+      int64_t s16, p16;
+      segment_addrs(seg - n_lin, 0, layer, g, ppc_log2, row16_log2, slots, pages, s16, p16);
+      src = store + s16;
+      dst = pool + p16;
+    }
+    for (int64_t base = lane; base < len16; base += 32 * kUnroll) {
       uint4 v[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u)
-        if (base + 32 * u < seg16) v[u] = ld_host_stream(src + base + 32 * u);
+        if (base + 32 * u < len16) v[u] = ld_host_stream(src + base + 32 * u);
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u)
-        if (base + 32 * u < seg16) dst[base + 32 * u] = v[u];
+        if (base + 32 * u < len16) dst[base + 32 * u] = v[u];
     }
   }
 }
@@ -204,13 +227,21 @@ int ilog2(int64_t x) {
 
 cudaError_t launch_kv_gather(const void* store, void* pool, const int32_t* d_slots, const int32_t* d_pages,
                              int32_t n_matched, int32_t layer, const KvGeom& g, int32_t target_ctas,
-                             cudaStream_t stream) {
-  if (n_matched <= 0) return cudaSuccess;
-  const int64_t n_seg = int64_t(n_matched) * g.Hkv * 2 * (g.C / g.S);
+                             cudaStream_t stream, const LinearCopies* lin) {
+  LinearCopies l{};
+  if (lin) l = *lin;
+  if (l.n < 0 || l.n > LinearCopies::kMax) return cudaErrorInvalidValue;
+  const int64_t seg16 = int64_t(g.S) * (g.d / 8);
+  int64_t n_seg = int64_t(std::max(n_matched, 0)) * g.Hkv * 2 * (g.C / g.S);
+  for (int i = 0; i < l.n; ++i) {
+    if (l.n16[i] < 0) return cudaErrorInvalidValue;
+    n_seg += (l.n16[i] + seg16 - 1) / seg16;
+  }
+  if (n_seg <= 0) return cudaSuccess;
   const int64_t ctas = std::min<int64_t>(target_ctas, (n_seg + kThreads / 32 - 1) / (kThreads / 32));
   kv_gather_kernel<<<int(ctas), kThreads, 0, stream>>>(static_cast<const uint4*>(store), static_cast<uint4*>(pool),
-                                                       d_slots, d_pages, n_matched, layer, g, ilog2(g.d / 8),
-                                                       ilog2(g.C / g.S));
+                                                       d_slots, d_pages, std::max(n_matched, 0), layer, g,
+                                                       ilog2(g.d / 8), ilog2(g.C / g.S), l);
   return cudaGetLastError();
 }
 

@@ -52,18 +52,19 @@ struct pcr_ctx {
   std::string err;
   int64_t launches = 0;
   int64_t ce_copies = 0, ce_layer_loads = 0, sm_layer_loads = 0;   // a2 load-path counters (pcr_stats)
-  int64_t ce_offload_layers = 0;
   pcr::KvGeom geom{};
   int32_t gather_ctas = 16;
-  // split-KV workspace: ws_floats partial-O floats followed by ws_floats/d LSE floats
+  // split-KV workspace, one slice of ws_region_floats per plan region: ws_floats partial-O
+  // floats followed by the LSE floats
   float* ws = nullptr;
-  int64_t ws_floats = 0;
+  int64_t ws_floats = 0, ws_region_floats = 0;
   // multi-GPU output re-assembly (§8(e))
   void* nccl_comm = nullptr;
   std::unique_ptr<pcr::SsdIo> ssd;    // SSD tier I/O thread (f2)
   std::vector<int64_t> slot_write_seq; // per DRAM slot: last write-back task reading it
+  std::vector<int64_t> slot_read_seq;  // per DRAM slot: last SSD read task filling it
   std::unordered_map<int64_t, int64_t> req_load_seq;  // request -> last SSD load it started
-  std::vector<void*> ce_dst, ce_src;  // copy-engine baseline batch (load_mode 1/2)
+  std::vector<void*> ce_dst, ce_src;  // copy-engine baseline runs (load_mode 1/2/4)
   std::vector<size_t> ce_size;
   std::vector<cudaEvent_t> ev_attn;
   cudaEvent_t ev_comm = nullptr;
@@ -181,13 +182,13 @@ pcr_status device_ready(pcr_ctx* c) {
   return PCR_OK;
 }
 
-// Copy-engine path of a2 (the paper's API).  Each matched chunk's layer-l image is C/S
-// pool-page images in the page-major store slot; a page image maps to one pool page.  Adjacent
-// images whose pool pages are also adjacent are merged into one run, so a chunk whose pages are
-// consecutive is one Hkv*2*C*d*2-byte copy (1 MiB for L8).  batch: one cudaMemcpyBatchAsync over
-// the runs; otherwise one cudaMemcpyAsync per page image (the paper's block-by-block baseline).
-int64_t build_ce_runs(pcr_ctx* c, const Request* r, int32_t layer, int32_t ch0, int32_t ch1, bool merge,
-                      bool d2h = false) {
+// Copy-engine baselines of a2 (f4; the paper's copy path, fig:api).  Each matched chunk's
+// layer-l image is C/S pool-page images in the page-major store slot; a page image maps to one pool
+// page.  load_mode 1 merges adjacent images whose pool pages are also adjacent into one run (a chunk
+// whose pages are consecutive is one Hkv*2*C*d*2-byte copy, 1 MiB for L8) and issues one
+// cudaMemcpyAsync per run; load_mode 2 issues one cudaMemcpyAsync per page image (the paper's
+// block-by-block baseline).
+int64_t build_ce_runs(pcr_ctx* c, const Request* r, int32_t layer, int32_t ch0, int32_t ch1, bool merge) {
   const pcr_config& k = c->cfg;
   const int32_t ppc = k.chunk_tokens / k.page_tokens;
   const size_t page_img = static_cast<size_t>(c->hkv) * 2 * k.page_tokens * k.head_dim * 2;
@@ -200,7 +201,6 @@ int64_t build_ce_runs(pcr_ctx* c, const Request* r, int32_t layer, int32_t ch0, 
     for (int32_t pp = 0; pp < ppc && owns_chunk(c, ch); ++pp) {
       uint8_t* src = store + r->plan.slots[ch] * c->slot_bytes + (int64_t(layer) * ppc + pp) * page_img;
       uint8_t* dst = pool + (int64_t(layer) * c->n_pool_pages + r->plan.pages[ch * ppc + pp]) * page_img;
-      if (d2h) std::swap(src, dst);   // offload: pool page image -> store
       if (merge && !c->ce_src.empty() && static_cast<uint8_t*>(c->ce_src.back()) + c->ce_size.back() == src &&
           static_cast<uint8_t*>(c->ce_dst.back()) + c->ce_size.back() == dst) {
         c->ce_size.back() += page_img;
@@ -213,120 +213,79 @@ int64_t build_ce_runs(pcr_ctx* c, const Request* r, int32_t layer, int32_t ch0, 
   return static_cast<int64_t>(c->ce_src.size());
 }
 
-// Extra host->device copies that ride in the same copy-engine batch as a layer's KV load
-// (host_io: the layer's q/k/v inputs).
-struct H2dCopies {
-  int32_t n = 0;
-  void* dst[3];
-  const void* src[3];
-  size_t bytes[3];
-};
-
 pcr_status enqueue_ce_copy(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s, int32_t ch0, int32_t ch1,
-                           bool batch, const H2dCopies* extra = nullptr, bool d2h = false) {
-  build_ce_runs(c, r, layer, ch0, ch1, batch, d2h);
-  for (int32_t i = 0; extra && i < extra->n; ++i) {
-    c->ce_dst.push_back(extra->dst[i]);
-    c->ce_src.push_back(const_cast<void*>(extra->src[i]));
-    c->ce_size.push_back(extra->bytes[i]);
-  }
-  const int64_t n = static_cast<int64_t>(c->ce_src.size());
-  if (n == 0) return PCR_OK;
-  if (batch) {
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    size_t idx = 0, fail_idx = 0;
-    CUDA_TRY(c, cudaMemcpyBatchAsync(c->ce_dst.data(), c->ce_src.data(), c->ce_size.data(), n, &attr, &idx, 1,
-                                     &fail_idx, s));
-  } else {
-    for (int64_t j = 0; j < n; ++j)
-      CUDA_TRY(c, cudaMemcpyAsync(c->ce_dst[j], c->ce_src[j], c->ce_size[j],
-                                  d2h ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, s));
-  }
-  if (!d2h) c->ce_copies += n;   // (a2 loads only)
+                           bool merge) {
+  const int64_t n = build_ce_runs(c, r, layer, ch0, ch1, merge);
+  for (int64_t j = 0; j < n; ++j)
+    CUDA_TRY(c, cudaMemcpyAsync(c->ce_dst[j], c->ce_src[j], c->ce_size[j], cudaMemcpyHostToDevice, s));
+  c->ce_copies += n;
   return PCR_OK;
 }
 
-// load_mode 5 (auto): the copy engines when the request's runs average >= kCeMinRun bytes, else
-// the SM gather.  tools/ce_probe.cu on this pool's B200 (profiles/r01_ce_probe.txt), one 16 MiB
-// layer in runs of 16 KiB / 64 KiB / 256 KiB / 1 MiB: copy engine 25.9 / 43.4 / 51.5 / 53.9 GB/s
-// (54.7 GB/s over 32 back-to-back layers of 256 KiB runs) against 50.1 GB/s for the SM gather at
-// any run size: PCIe reads issued by SMs complete in 128-byte payloads, the copy engines' in
-// larger ones, so only the copy engines reach the link's ~55.6 GB/s, and only for long runs.  In
-// the pipeline at the per-rank geometry of an 8-GPU L8 run (one KV head: 2 MiB per layer in
-// 128 KiB runs) the copy engines still win: 43 us vs 52 us per layer (the gather kernel's ramp-up
-// and tail weigh on a 2 MiB load), profiles/r01_rankslice.jsonl.
-constexpr int64_t kCeMinRun = 128 << 10;
+bool use_copy_engines(const pcr_ctx* c) { return c->cfg.load_mode == 1 || c->cfg.load_mode == 2; }
 
-bool long_runs(pcr_ctx* c, const Request* r, int32_t ch0, int32_t ch1) {
-  const int64_t n = build_ce_runs(c, r, 0, ch0, ch1, true);
-  int64_t bytes = 0;
-  for (size_t b : c->ce_size) bytes += static_cast<int64_t>(b);
-  return n > 0 && bytes / n >= kCeMinRun;
-}
-
-bool use_copy_engines(pcr_ctx* c, const Request* r) {
-  if (c->cfg.load_mode == 1 || c->cfg.load_mode == 2) return true;
-  if (c->cfg.load_mode != 5) return false;
-  if (r->load_auto < 0) const_cast<Request*>(r)->load_auto = long_runs(c, r, 0, r->plan.n_matched) ? 1 : 0;
-  return r->load_auto == 1;
-}
-
-// f1 offload mover: load_mode 5 applies the same rule to the reserved chunks' runs (D2H); the
-// other modes keep the SM scatter kernel.
-bool offload_with_copy_engines(pcr_ctx* c, const Request* r) {
-  if (c->cfg.load_mode != 5) return false;
-  if (r->offload_auto < 0)
-    const_cast<Request*>(r)->offload_auto =
-        long_runs(c, r, r->plan.n_matched, r->plan.n_matched + r->plan.n_reserved) ? 1 : 0;
-  return r->offload_auto == 1;
-}
+// Linear host->device copies that ride along with a layer's KV load (host_io: the layer's q/k/v
+// inputs).  With device-mapped sources and the SM gather they are folded into the gather launch
+// (one kernel per layer, one FIFO over the host link); otherwise one cudaMemcpyAsync each.
+struct H2dCopies {
+  int32_t n = 0;
+  void* dst[3];
+  const void* src[3];        // host pointers
+  const void* src_dev[3];    // their device-mapped views (nullptr: not mapped)
+  size_t bytes[3];
+};
 
 pcr_status enqueue_gather(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s, const H2dCopies* extra = nullptr) {
+  pcr::LinearCopies lin{};
+  const bool gather_kernel = !use_copy_engines(c) && c->cfg.load_mode != 3;
   if (extra && extra->n > 0) {
-    if (r->plan.n_matched > 0 && use_copy_engines(c, r)) {   // one batch: inputs + KV runs
-      c->ce_layer_loads += 1;
-      return enqueue_ce_copy(c, r, layer, s, 0, r->plan.n_matched, c->cfg.load_mode != 2, extra);
+    bool fold = gather_kernel;
+    for (int32_t i = 0; i < extra->n; ++i)
+      fold = fold && extra->src_dev[i] && extra->bytes[i] % 16 == 0 &&
+             (reinterpret_cast<uintptr_t>(extra->src_dev[i]) & 15) == 0 &&
+             (reinterpret_cast<uintptr_t>(extra->dst[i]) & 15) == 0;
+    if (fold) {
+      lin.n = extra->n;
+      for (int32_t i = 0; i < extra->n; ++i) {
+        lin.src[i] = static_cast<const uint4*>(extra->src_dev[i]);
+        lin.dst[i] = static_cast<uint4*>(extra->dst[i]);
+        lin.n16[i] = static_cast<int64_t>(extra->bytes[i] / 16);
+      }
+    } else {
+      for (int32_t i = 0; i < extra->n; ++i)
+        CUDA_TRY(c, cudaMemcpyAsync(extra->dst[i], extra->src[i], extra->bytes[i], cudaMemcpyHostToDevice, s));
     }
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t idx = 0, fail_idx = 0;
-    CUDA_TRY(c, cudaMemcpyBatchAsync(const_cast<void**>(extra->dst), const_cast<void**>(extra->src),
-                                     const_cast<size_t*>(extra->bytes), extra->n, &attr, &idx, 1, &fail_idx, s));
   }
-  if (r->plan.n_matched == 0) return PCR_OK;
-  if (c->ctx_split) {   // this rank's chunks only (compacted tables), gather kernel or copy engines
-    if (use_copy_engines(c, r)) {
-      c->ce_layer_loads += 1;
-      return enqueue_ce_copy(c, r, layer, s, 0, r->plan.n_matched, c->cfg.load_mode != 2);
-    }
-    if (r->ctx_n_own == 0) return PCR_OK;
-    c->sm_layer_loads += 1;
+  if (r->plan.n_matched == 0 && lin.n == 0) return PCR_OK;
+  if (use_copy_engines(c)) {
+    c->ce_layer_loads += 1;
+    return enqueue_ce_copy(c, r, layer, s, 0, r->plan.n_matched, c->cfg.load_mode == 1);
+  }
+  if (c->ctx_split) {   // this rank's chunks only (compacted tables)
+    if (r->ctx_n_own == 0 && lin.n == 0) return PCR_OK;
+    c->sm_layer_loads += r->ctx_n_own > 0;
     if (c->cfg.load_mode == 3)
       CUDA_TRY(c, pcr::launch_kv_gather_tma(c->store_dev, c->cfg.pool, d_own_slots_of(c, r), d_vpages_of(c, r),
                                             r->ctx_n_own, layer, c->geom, 4 * c->gather_ctas, s));
     else
       CUDA_TRY(c, pcr::launch_kv_gather(c->store_dev, c->cfg.pool, d_own_slots_of(c, r), d_vpages_of(c, r),
-                                        r->ctx_n_own, layer, c->geom, c->gather_ctas, s));
+                                        r->ctx_n_own, layer, c->geom, c->gather_ctas, s, &lin));
     c->launches += 1;
     return PCR_OK;
   }
   if (c->cfg.load_mode == 3) {
+    if (r->plan.n_matched == 0) return PCR_OK;
     CUDA_TRY(c, pcr::launch_kv_gather_tma(c->store_dev, c->cfg.pool, d_slots_of(c, r), d_pages_of(c, r),
                                           r->plan.n_matched, layer, c->geom, 4 * c->gather_ctas, s));
     c->launches += 1;
     c->sm_layer_loads += 1;
     return PCR_OK;
   }
-  if (use_copy_engines(c, r)) {
-    c->ce_layer_loads += 1;
-    return enqueue_ce_copy(c, r, layer, s, 0, r->plan.n_matched, c->cfg.load_mode != 2);
-  }
-  c->sm_layer_loads += 1;
+  c->sm_layer_loads += r->plan.n_matched > 0;
   int32_t n_ce = 0;
-  if (c->cfg.load_mode == 4) {
-    // hybrid: chunks [0, n_ce) by the copy engines on ce_stream, the rest by the gather kernel on s
+  if (c->cfg.load_mode == 4 && r->plan.n_matched > 0) {
+    // hybrid: chunks [0, n_ce) by the copy engines (one cudaMemcpyAsync per merged run) on
+    // ce_stream, the rest by the gather kernel on s
     n_ce = std::min(r->plan.n_matched, std::max(0, static_cast<int32_t>(std::lround(
                                                        c->cfg.load_ce_fraction * r->plan.n_matched))));
     if (n_ce > 0) {
@@ -341,10 +300,10 @@ pcr_status enqueue_gather(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s,
       if (st != PCR_OK) return st;
     }
   }
-  if (n_ce < r->plan.n_matched) {
+  if (n_ce < r->plan.n_matched || lin.n > 0) {
     const int32_t ppc = c->cfg.chunk_tokens / c->cfg.page_tokens;
     CUDA_TRY(c, pcr::launch_kv_gather(c->store_dev, c->cfg.pool, d_slots_of(c, r) + n_ce, d_pages_of(c, r) + n_ce * ppc,
-                                      r->plan.n_matched - n_ce, layer, c->geom, c->gather_ctas, s));
+                                      r->plan.n_matched - n_ce, layer, c->geom, c->gather_ctas, s, &lin));
     c->launches += 1;
   }
   if (n_ce > 0) {
@@ -381,8 +340,11 @@ pcr_status enqueue_attn(pcr_ctx* c, Request* r, int32_t layer, const void* q, co
   p.n_req_pages = n_pages;
   p.n_pool_pages = c->n_pool_pages;
   p.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(c->cfg.head_dim));
-  p.ws_o = c->ws;
-  p.ws_lse = c->ws ? c->ws + c->ws_floats : nullptr;
+  // each plan region has its own split-KV workspace slice, so requests in flight on different
+  // streams never share partials
+  float* ws = c->ws ? c->ws + r->plan.region * c->ws_region_floats : nullptr;
+  p.ws_o = ws;
+  p.ws_lse = ws ? ws + c->ws_floats : nullptr;
   p.ws_bytes = c->ws_floats * 4;
   int n = 0;
   cudaError_t e = pcr::launch_suffix_attn(&c->tmap, p, c->cfg.head_dim, s, &n);
@@ -394,11 +356,6 @@ pcr_status enqueue_attn(pcr_ctx* c, Request* r, int32_t layer, const void* q, co
 
 pcr_status enqueue_offload(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s) {
   if (r->plan.n_reserved == 0) return PCR_OK;
-  if (offload_with_copy_engines(c, r)) {
-    c->ce_offload_layers += 1;
-    return enqueue_ce_copy(c, r, layer, s, r->plan.n_matched, r->plan.n_matched + r->plan.n_reserved, true,
-                           nullptr, true);
-  }
   if (c->ctx_split) {
     if (r->ctx_n_res_own == 0) return PCR_OK;
     CUDA_TRY(c, pcr::launch_kv_scatter(c->cfg.pool, c->store_dev, d_own_res_slots_of(c, r), d_own_res_pages_of(c, r),
@@ -412,13 +369,18 @@ pcr_status enqueue_offload(pcr_ctx* c, Request* r, int32_t layer, cudaStream_t s
   return PCR_OK;
 }
 
-bool is_pinned_host(const void* p) {
+// Page-locked host memory: true, with its device-mapped view in *dev (nullptr when the allocation
+// is not mapped into the device address space).
+bool pinned_host(const void* p, const void** dev) {
   cudaPointerAttributes a{};
+  *dev = nullptr;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();   // clear the sticky-free error of an unknown pointer
     return false;
   }
-  return a.type == cudaMemoryTypeHost;
+  if (a.type != cudaMemoryTypeHost) return false;
+  *dev = a.devicePointer;
+  return true;
 }
 
 // host_io: the D2H stream, per-layer events and a ring of R staging buffers [q | k | v | out] of one
@@ -476,7 +438,9 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
     return fail(c, o.comm_stream ? PCR_E_STATE : PCR_E_INVAL, "all-gather needs pcr_comm_init and a comm stream");
   if (o.host_io != 0 && o.host_io != 1) return fail(c, PCR_E_INVAL, "host_io must be 0 or 1");
   if (o.host_io && o.gathered_all) return fail(c, PCR_E_INVAL, "host_io cannot be combined with gathered_all");
-  if (o.host_io && !(is_pinned_host(q_all) && is_pinned_host(k_all) && is_pinned_host(v_all) && is_pinned_host(out_all)))
+  const void *q_dev = nullptr, *k_dev = nullptr, *v_dev = nullptr, *o_dev = nullptr;
+  if (o.host_io && !(pinned_host(q_all, &q_dev) && pinned_host(k_all, &k_dev) && pinned_host(v_all, &v_dev) &&
+                     pinned_host(out_all, &o_dev)))
     return fail(c, PCR_E_INVAL, "host_io needs page-locked host q/k/v/out buffers");
   cudaStream_t cs = static_cast<cudaStream_t>(o.compute_stream);
   cudaStream_t ls = up ? static_cast<cudaStream_t>(o.load_stream) : cs;
@@ -490,11 +454,11 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
   if ((st = ensure_tables(c, r, ls)) != PCR_OK) return st;
   if (up) CUDA_TRY(c, cudaStreamWaitEvent(cs, c->region_ev[r->plan.region], 0));
   // host_io: layer l's inputs/outputs go through staging buffer l % R (q | k | v | out).  In
-  // OVERLAP mode the inputs are copied on the LOAD stream, in the same copy batch as layer l's KV
-  // load (or just ahead of the gather kernel): one FIFO of host->device traffic in the order the
-  // layers need it, so the link never splits between streams and small input copies do not pay
-  // per-copy overhead (tools/bidir_probe.cu, tools/ce_probe.cu); layer l+R's inputs wait for
-  // attention(l) to release the buffer.  Outputs return on the D2H stream (the other direction).
+  // OVERLAP mode the inputs are copied on the LOAD stream by layer l's gather launch itself (16-byte
+  // loads from the mapped host buffers, like the KV) -- one FIFO of host->device traffic in the
+  // order the layers need it, so the link never splits between streams (tools/bidir_probe.cu);
+  // layer l+R's inputs wait for attention(l) to release the buffer.  Outputs return on the D2H
+  // stream (the other direction of the link) with one cudaMemcpyAsync per layer.
   const int64_t io_layer = 2 * q_layer + 2 * kv_layer;
   int32_t ring = 2;
   cudaStream_t ds = cs;
@@ -535,15 +499,21 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
     if (o.host_io && up) {   // layer l's inputs join its KV load batch
       uint16_t* b = buf_of(l);
       if (l >= ring) CUDA_TRY(c, cudaStreamWaitEvent(ls, c->ev_attn[l - ring], 0));  // buffer free
+      auto at = [](const void* base, int64_t elems) -> const void* {
+        return base ? static_cast<const uint16_t*>(base) + elems : nullptr;
+      };
       in.n = 3;
       in.dst[0] = b;
-      in.src[0] = static_cast<const uint16_t*>(q_all) + l * q_layer;
+      in.src[0] = at(q_all, l * q_layer);
+      in.src_dev[0] = at(q_dev, l * q_layer);
       in.bytes[0] = q_layer * 2;
       in.dst[1] = b + q_layer;
-      in.src[1] = static_cast<const uint16_t*>(k_all) + l * kv_layer;
+      in.src[1] = at(k_all, l * kv_layer);
+      in.src_dev[1] = at(k_dev, l * kv_layer);
       in.bytes[1] = kv_layer * 2;
       in.dst[2] = b + q_layer + kv_layer;
-      in.src[2] = static_cast<const uint16_t*>(v_all) + l * kv_layer;
+      in.src[2] = at(v_all, l * kv_layer);
+      in.src_dev[2] = at(v_dev, l * kv_layer);
       in.bytes[2] = kv_layer * 2;
     }
     if (times) CUDA_TRY(c, cudaEventRecord(et[0], ls));
@@ -666,8 +636,8 @@ pcr_status pcr_merge_partials(pcr_ctx* c, const float* gathered, int32_t n_parts
 
 pcr_status pcr_set_load_mode(pcr_ctx* c, int32_t load_mode, float load_ce_fraction) {
   if (!c) return PCR_E_INVAL;
-  if (load_mode < 0 || load_mode > 5 || !(load_ce_fraction >= 0.f && load_ce_fraction <= 1.f))
-    return fail(c, PCR_E_INVAL, "pcr_set_load_mode: load_mode in [0, 5], load_ce_fraction in [0, 1]");
+  if (load_mode < 0 || load_mode > 4 || !(load_ce_fraction >= 0.f && load_ce_fraction <= 1.f))
+    return fail(c, PCR_E_INVAL, "pcr_set_load_mode: load_mode in [0, 4], load_ce_fraction in [0, 1]");
   c->cfg.load_mode = load_mode;
   c->cfg.load_ce_fraction = load_ce_fraction;
   return PCR_OK;
@@ -682,7 +652,7 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
       (k.shard_mode == 0 && k.n_kv_heads % k.world) || k.shard_mode < 0 || k.shard_mode > 1 ||
       k.chunk_tokens < 1 || k.page_tokens < 1 || k.chunk_tokens % k.page_tokens ||
       k.store_chunks < 1 || k.window < 0 || k.pool_bytes < 0 || k.max_inflight < 0 || k.max_tokens < 0 ||
-      k.gather_ctas < 0 || k.load_mode < 0 || k.load_mode > 5 || k.ssd_chunks < 0 ||
+      k.gather_ctas < 0 || k.load_mode < 0 || k.load_mode > 4 || k.ssd_chunks < 0 ||
       !(k.load_ce_fraction >= 0.f && k.load_ce_fraction <= 1.f) ||
       (k.ssd_chunks > 0 && !k.ssd_path))
     return PCR_E_INVAL;
@@ -708,7 +678,9 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
   c->max_regions = k.max_inflight > 0 ? k.max_inflight : 4;
   c->region_page_cap = (max_tokens + k.page_tokens - 1) / k.page_tokens;
   c->chunk_cap = (max_tokens + k.chunk_tokens - 1) / k.chunk_tokens;
-  c->region_words = (c->ctx_split ? 2 : 1) * (c->region_page_cap + c->chunk_cap);   // + context-split tables
+  // [pages | slots], + context split: [own_slots | vpages | own_res_slots | own_res_pages]
+  // (own_res_pages holds <= region_page_cap entries): 3 * (page_cap + chunk_cap) words in all
+  c->region_words = (c->ctx_split ? 3 : 1) * (c->region_page_cap + c->chunk_cap);
   c->region_words = (c->region_words + 63) / 64 * 64;
   c->planner = std::make_unique<Planner>(k.chunk_tokens, k.page_tokens, k.store_chunks, c->n_pool_pages, k.window,
                                          c->max_regions, k.ssd_chunks);
@@ -731,6 +703,7 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
       return PCR_E_NOMEM;
     }
     c->slot_write_seq.assign(k.store_chunks, 0);
+    c->slot_read_seq.assign(k.store_chunks, 0);
   }
   if (c->device) {
     pcr_ctx* cp = c.get();
@@ -762,8 +735,9 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
       if (e == cudaSuccess) cp->ev_attn.push_back(ev);
     }
     if (e == cudaSuccess) {
-      cp->ws_floats = (int64_t(32) << 20) / 4;  // 32 MiB of partial O (+ LSE)
-      e = cudaMalloc(reinterpret_cast<void**>(&cp->ws), (cp->ws_floats + cp->ws_floats / 64 + 64) * 4);
+      cp->ws_floats = (int64_t(32) << 20) / 4;  // 32 MiB of partial O (+ LSE) per region
+      cp->ws_region_floats = cp->ws_floats + cp->ws_floats / 64 + 64;
+      e = cudaMalloc(reinterpret_cast<void**>(&cp->ws), cp->ws_region_floats * c->max_regions * 4);
     }
     for (int l = 0; e == cudaSuccess && l < 6 * k.n_layers; ++l) {
       cudaEvent_t ev;
@@ -854,9 +828,13 @@ pcr_status pcr_match_prefix(pcr_ctx* c, int64_t req_id, const int64_t* pending, 
     uint8_t* store = static_cast<uint8_t*>(c->store);
     for (const pcr::IoOp& op : pl.loads) {
       last = c->ssd->read(op.ssd_slot, store + static_cast<size_t>(op.dram_slot) * c->slot_bytes);
+      c->slot_read_seq[op.dram_slot] = last;
       if (op.wait_now) wait_seq = last;
     }
     for (int32_t slot : pl.new_slots) wait_seq = std::max(wait_seq, c->slot_write_seq[slot]);
+    // a matched chunk may still be LOADING from an earlier request's look-ahead prefetch: its read
+    // must have landed before this request's gather reads the slot
+    for (int32_t i = 0; i < pl.n_matched; ++i) wait_seq = std::max(wait_seq, c->slot_read_seq[pl.slots[i]]);
     if (last) c->req_load_seq[req_id] = last;
     if (wait_seq && !c->ssd->wait(wait_seq)) return fail(c, PCR_E_INTERNAL, "SSD I/O failed");
   }
@@ -937,7 +915,6 @@ pcr_status pcr_get_stats(const pcr_ctx* c, pcr_stats* out) {
   out->ce_copies = c->ce_copies;
   out->ce_layer_loads = c->ce_layer_loads;
   out->sm_layer_loads = c->sm_layer_loads;
-  out->ce_offload_layers = c->ce_offload_layers;
   return PCR_OK;
 }
 

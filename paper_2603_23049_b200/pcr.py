@@ -20,7 +20,7 @@ STATUS = {0: "OK", -1: "INVAL", -2: "NOMEM", -3: "CUDA", -4: "STATE", -5: "NOREQ
           -7: "UNSUPPORTED"}
 SHARD_HEADS, SHARD_CONTEXT = 0, 1   # pcr_config.shard_mode (SURVEY §8(e) and its context-split variant)
 MODE_OVERLAP, MODE_SYNC, MODE_ONLY_UP, MODE_ONLY_DOWN = 0, 1, 2, 3   # P:703 Up-Down, base, Only-Up, Only-Down
-LOAD_SM_GATHER, LOAD_CE_BATCH, LOAD_CE_BLOCKS, LOAD_TMA, LOAD_HYBRID, LOAD_AUTO = 0, 1, 2, 3, 4, 5
+LOAD_SM_GATHER, LOAD_CE_RUNS, LOAD_CE_BLOCKS, LOAD_TMA, LOAD_HYBRID = 0, 1, 2, 3, 4
 
 
 class PcrError(RuntimeError):
@@ -55,8 +55,7 @@ class PcrStats(ctypes.Structure):
                 ("writebacks", ctypes.c_int64), ("ssd_evictions", ctypes.c_int64),
                 ("dram_evictions", ctypes.c_int64), ("ssd_bytes_read", ctypes.c_int64),
                 ("ssd_bytes_written", ctypes.c_int64), ("ce_copies", ctypes.c_int64),
-                ("ce_layer_loads", ctypes.c_int64), ("sm_layer_loads", ctypes.c_int64),
-                ("ce_offload_layers", ctypes.c_int64)]
+                ("ce_layer_loads", ctypes.c_int64), ("sm_layer_loads", ctypes.c_int64)]
 
 
 class PcrRunOpts(ctypes.Structure):

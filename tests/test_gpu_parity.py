@@ -13,7 +13,9 @@ from oracle.tree import PlanOracle  # noqa: E402
 from oracle.tiny_model import TinyModel  # noqa: E402
 from pcrgen import (appendix_c_trace, f32_to_bf16_bits, make_rng, pack_store_slots,  # noqa: E402
                     stress_values)
-from tests._gpu_harness import (TOL_MAX_ABS, TOL_REL_L2, Rig, check_attention, sample_rows,  # noqa: E402
+from oracle.attention import bf16_bits_to_f64, suffix_attention_blocked  # noqa: E402
+from oracle.kvload import append_layer, load_layer  # noqa: E402
+from tests._gpu_harness import (TOL_MAX_ABS, TOL_REL_L2, Rig, check_attention, rel_l2, sample_rows,  # noqa: E402
                                 to_dev, to_host)
 
 
@@ -97,13 +99,10 @@ def test_attention_and_pool_vs_oracle(kind, case):
     rig, plan, q, k, v, out = _single_request(kind, L, Hq, Hkv, d, C, S, N1, N2, seed=zlib.crc32(repr((kind,) + case).encode()) % 1000)
     pool = rig.pool_np()
     for l in range(L):
+        # O3: the WHOLE pool layer bit-exact (the request's pages, the tail rows of its last page
+        # -- zero-filled by the append, a kernel property -- and every other page, still zero)
         exp_pool = rig.expected_pool(plan, k[:, N1:], v[:, N1:], l)
-        pg = plan["pages"]
-        for t in range(N1 + N2):                   # O3: bit-exact at every token position
-            assert np.array_equal(pool[l, pg[t // S], :, :, t % S], exp_pool[l, pg[t // S], :, :, t % S]), (l, t)
-        tail = [(t, pg[t // S]) for t in range(N1 + N2, len(pg) * S)]
-        for t, p in tail:                          # kernel property: tail rows are zero (finite)
-            assert not pool[l, p, :, :, t % S].any()
+        assert np.array_equal(pool[l], exp_pool[l]), l
         kc, vc = rig.expected_context(plan, k[:, N1:], v[:, N1:], l)
         assert np.array_equal(kc, k[l]) and np.array_equal(vc, v[l])
         r, m = check_attention(out[l], q[l], kc, vc, N1, blocked=True)
@@ -139,13 +138,13 @@ def test_overlap_sync_and_per_layer_api_are_bitwise_identical():
     assert np.array_equal(to_host(o), out)
 
 
-@pytest.mark.parametrize("mode,load_mode,ring", [(0, 0, 2), (1, 0, 0), (0, 5, 2), (0, 5, 0), (1, 5, 2)])
+@pytest.mark.parametrize("mode,load_mode,ring", [(0, 0, 2), (1, 0, 0), (0, 0, 0), (0, 1, 2), (1, 1, 2), (0, 2, 0)])
 def test_host_io_matches_device_buffers(mode, load_mode, ring):
     """pcr_run_prefill_ex with host_io: page-locked HOST q/k/v/out, staged per layer by the library
-    (in OVERLAP mode the inputs ride in the layer's load: before the gather kernel, or inside the
-    copy-engine batch with load_mode auto), gives the device-buffer result bit for bit (OVERLAP and
-    SYNC); 5 layers with a 2-deep staging ring so it wraps, and the default (whole-request) ring;
-    pageable host memory is refused."""
+    (in OVERLAP mode the inputs ride in the layer's load: inside the gather launch with the SM
+    gather, one cudaMemcpyAsync each ahead of the copy-engine baselines), gives the device-buffer
+    result bit for bit (OVERLAP and SYNC); 5 layers with a 2-deep staging ring so it wraps, and the
+    default (whole-request) ring; pageable host memory is refused."""
     L, n1, n2 = 5, 1024, 130
     rig, plan, q, k, v, out = _single_request("iid", L, 32, 8, 128, 256, 64, n1, n2, seed=9, load_mode=load_mode)
     rig.ctx.release(1, True)
@@ -250,24 +249,38 @@ def test_appendix_c_trace_tiny_model():
         orc.release(i, True)
 
 
-@pytest.mark.parametrize("load_mode", [0, 5])
-def test_l8_full_size_sampled(load_mode):
-    """configs[1] at full size in the bench's launch configuration (OVERLAP, 32 layers, load_mode
-    auto = the copy-engine batch bench.py times, and the SM gather kernel;
-    4096 cached + 128 query): sampled rows vs the oracle on layers 0, 15, 31; pool bit-exact
-    on those layers."""
+def test_l8_full_size_full_check():
+    """configs[1] at full size in the bench's launch configuration (OVERLAP, 32 layers, SM gather,
+    4096 cached + 128 query): EVERY output row of every head of all 32 layers against the fp64
+    oracle ("Full checks run on T and L8"), and the WHOLE pool array bit-exact
+    (O3): a stray 16-byte store into another page or layer fails it.  Prints the worst
+    (layer, head)."""
     L, Hq, Hkv, d, C, S, N1, N2 = 32, 32, 8, 128, 256, 64, 4096, 128
-    rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, N1, N2, seed=1, load_mode=load_mode)
+    rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, N1, N2, seed=1)
     st = rig.ctx.stats
-    assert st["ce_layer_loads" if load_mode == 5 else "sm_layer_loads"] == L   # the mover bench.py times
-    rows = sample_rows(N2, N1, C, S, k=64, seed=1)
+    assert st["sm_layer_loads"] == L and st["ce_layer_loads"] == 0   # the mover bench.py times
     pool = rig.pool_np()
-    for l in (0, 15, 31):
-        exp_pool = rig.expected_pool(plan, k[:, N1:], v[:, N1:], l)
-        assert np.array_equal(pool[l][plan["pages"]], exp_pool[l][plan["pages"]])
+    exp_pool = np.zeros_like(pool)
+    for l in range(L):
+        load_layer(exp_pool, rig.store, plan["slots"], plan["pages"], l, N1, C, S)
+        append_layer(exp_pool, k[l, N1:], v[l, N1:], plan["pages"], l, N1, S)
+    assert np.array_equal(pool, exp_pool)
+    worst = (0.0, None)
+    rels = []
+    for l in range(L):
         kc, vc = rig.expected_context(plan, k[:, N1:], v[:, N1:], l)
-        r, m = check_attention(out[l], q[l], kc, vc, N1, rows=rows)
+        qf, kf, vf = bf16_bits_to_f64(q[l]), bf16_bits_to_f64(kc), bf16_bits_to_f64(vc)
+        ref, _ = suffix_attention_blocked(qf, kf, vf, N1)
+        got = bf16_bits_to_f64(out[l])
+        r, m = rel_l2(got, ref), float(np.abs(got - ref).max())
+        rels.append(r)
         assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (l, r, m)
+        for h in range(Hq):
+            rh = rel_l2(got[:, h], ref[:, h])
+            if rh > worst[0]:
+                worst = (rh, (l, h))
+    print(f"L8 full check: rel-L2 mean {np.mean(rels):.3e} max {max(rels):.3e}; worst (layer, head) "
+          f"{worst[1]} rel-L2 {worst[0]:.3e}")
 
 
 def _check_sampled(rig, plan, q, k, v, out, N1, N2, C, S, layers, seed):
@@ -275,7 +288,7 @@ def _check_sampled(rig, plan, q, k, v, out, N1, N2, C, S, layers, seed):
     pool = rig.pool_np()
     for l in layers:
         exp_pool = rig.expected_pool(plan, k[:, N1:], v[:, N1:], l)
-        assert np.array_equal(pool[l][plan["pages"]], exp_pool[l][plan["pages"]]), l
+        assert np.array_equal(pool[l], exp_pool[l]), l      # whole layer of the pool
         kc, vc = rig.expected_context(plan, k[:, N1:], v[:, N1:], l)
         r, m = check_attention(out[l], q[l], kc, vc, N1, rows=rows)
         assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (l, r, m)
@@ -286,7 +299,7 @@ def test_m7_half_hit_full_size_sampled():
     OVERLAP: 32 layers, N1 = 4096 cached + N2 = 4224 computed (multi-wave attention grid, no KV
     split); sampled rows vs the oracle and the pool bit-exact on layers 0, 17, 31."""
     L, Hq, Hkv, d, C, S, N1, N2 = 32, 32, 8, 128, 256, 64, 4096, 4224
-    rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, N1, N2, seed=4, load_mode=5)
+    rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, N1, N2, seed=4)
     _check_sampled(rig, plan, q, k, v, out, N1, N2, C, S, (0, 17, 31), seed=4)
 
 
@@ -296,7 +309,7 @@ def test_l70_rank_slice_full_size_sampled():
     cached + N2 = 8320 computed; sampled rows and pool on layers 0, 41, 79."""
     L, Hq, Hkv, d, C, S, N1, N2 = 80, 64, 8, 128, 256, 64, 8192, 8320
     rig, plan, q, k, v, out = _single_request("iid", L, Hq, Hkv, d, C, S, N1, N2, seed=6, world=8, rank=5,
-                                              local_only=True, load_mode=5)
+                                              local_only=True)
     _check_sampled(rig, plan, q, k, v, out, N1, N2, C, S, (0, 41, 79), seed=6)
 
 
@@ -324,12 +337,13 @@ def test_sharded_run_with_nccl_allgather_world1():
 
 
 @pytest.mark.parametrize("fragment", [False, True])
-@pytest.mark.parametrize("load_mode,frac", [(1, 0.0), (2, 0.0), (3, 0.0), (4, 0.34), (4, 1.0), (5, 0.0)])
+@pytest.mark.parametrize("load_mode,frac", [(1, 0.0), (2, 0.0), (3, 0.0), (4, 0.34), (4, 1.0)])
 def test_copy_engine_baselines_match_gather(load_mode, frac, fragment):
-    """f4 baselines (the paper's cudaMemcpyBatchAsync / block-by-block path), the hybrid
-    copy-engine + gather-kernel load and the auto choice produce the same pool bits and outputs as
-    the SM gather kernel, and both equal the oracle's pool (O3) -- with the request's pages
-    consecutive (copy-engine runs merge to whole chunk-layers) and with a hole in them."""
+    """f4 baselines (the paper's copy-engine path: one cudaMemcpyAsync per merged run or per
+    page image), the TMA experiment and the hybrid copy-engine + gather-kernel load produce the same
+    pool bits and outputs as the SM gather kernel, and the whole pool equals the oracle's (O3) --
+    with the request's pages consecutive (copy-engine runs merge to whole chunk-layers) and with a
+    hole in them."""
     args = ("kout", 2, 32, 8, 128, 256, 16, 768, 90)
     rig0, plan0, q, k, v, out0 = _single_request(*args, seed=44, fragment=fragment)
     rig1, plan1, _, _, _, out1 = _single_request(*args, seed=44, fragment=fragment, load_mode=load_mode,
@@ -339,10 +353,10 @@ def test_copy_engine_baselines_match_gather(load_mode, frac, fragment):
         assert plan1["pages"][:3] == [0, 2, 3]
     assert np.array_equal(out0, out1)
     p0, p1 = rig0.pool_np(), rig1.pool_np()
-    assert np.array_equal(p0[:, plan0["pages"]], p1[:, plan1["pages"]])
+    assert np.array_equal(p0, p1)
     for layer in range(2):
         exp = rig1.expected_pool(plan1, k[:, 768:], v[:, 768:], layer)
-        assert np.array_equal(p1[layer][plan1["pages"]], exp[layer][plan1["pages"]])
+        assert np.array_equal(p1[layer], exp[layer])
     st = rig1.ctx.stats
     if load_mode in (1, 2):
         assert st["ce_layer_loads"] == 2 and st["sm_layer_loads"] == 0
@@ -350,30 +364,14 @@ def test_copy_engine_baselines_match_gather(load_mode, frac, fragment):
         assert st["ce_copies"] == 2 * (3 if not fragment else 4)
     if load_mode == 2:
         assert st["ce_copies"] == 2 * 3 * 16
-    if load_mode == 5:   # 8 kv heads x 2 x 16 x 128 x 2 B = 64 KiB page images, 1 MiB chunk-layers
-        assert st["ce_layer_loads"] == 2 and st["sm_layer_loads"] == 0
-
-
-def test_auto_load_mode_picks_the_gather_for_short_runs():
-    """load_mode 5 takes the SM gather when the copy runs are short (T geometry: 2 kv heads x
-    64-token chunks = 32 KiB chunk-layers) and the pool still matches the oracle bit for bit."""
-    args = ("iid", 2, 4, 2, 64, 64, 16, 256, 64)
-    rig, plan, q, k, v, out = _single_request(*args, seed=45, load_mode=5)
-    st = rig.ctx.stats
-    assert st["sm_layer_loads"] == 2 and st["ce_layer_loads"] == 0 and st["ce_copies"] == 0
-    p = rig.pool_np()
-    for layer in range(2):
-        exp = rig.expected_pool(plan, k[:, 256:], v[:, 256:], layer)
-        assert np.array_equal(p[layer][plan["pages"]], exp[layer][plan["pages"]])
 
 
 @pytest.mark.parametrize("fragment", [False, True])
-@pytest.mark.parametrize("load_mode", [0, 5])
+@pytest.mark.parametrize("load_mode", [0, 1])
 def test_offload_long_runs_store_records(load_mode, fragment):
-    """f1 offload at the L8 geometry (1 MiB chunk-layers): with load_mode auto the reserved
-    chunks go back to the store in one copy-engine D2H batch per layer (runs split where the
-    pool pages are not consecutive), otherwise through the SM scatter kernel; either way every
-    reserved slot then holds exactly the request's K/V record (bitwise, O3 in reverse)."""
+    """f1 offload at the L8 geometry (1 MiB chunk-layers) through the SM scatter kernel, with either
+    load path configured: every reserved slot then holds exactly the request's K/V record (bitwise,
+    O3 in reverse), with the request's pool pages consecutive and with a hole in them."""
     L, Hq, Hkv, d, C, S, n_doc, n2q = 2, 32, 8, 128, 256, 64, 768, 90
     rng = make_rng(77)
     rig = Rig(L, Hq, Hkv, d, C, S, store_chunks=6, n_pool_pages=40, load_mode=load_mode)
@@ -403,11 +401,10 @@ def test_offload_long_runs_store_records(load_mode, fragment):
     for c in range(3):
         got = rig.ctx.store_read(plan["slots"][c]).reshape(recs[c].shape)
         assert np.array_equal(got, recs[c]), c
-    assert rig.ctx.stats["ce_offload_layers"] == (L if load_mode == 5 else 0)
     rig.ctx.release(1, True)
 
 
-@pytest.mark.parametrize("mode,load_mode", [(0, 0), (1, 0), (2, 0), (3, 0), (0, 5), (3, 5)])
+@pytest.mark.parametrize("mode,load_mode", [(0, 0), (1, 0), (2, 0), (3, 0), (0, 1), (3, 2)])
 def test_offload_third_stream_commits_real_kv(mode, load_mode):
     """f1: the Appendix C trace where new chunks reach the store ONLY through the library's
     layer-wise offload on a third stream (pcr_run_prefill_ex); every committed slot must hold
@@ -460,7 +457,7 @@ def test_split_kv_edge_sweep(n1, n2):
     assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (r, m)
 
 
-@pytest.mark.parametrize("P,load_mode,kind", [(2, 0, "iid"), (3, 5, "advfuture"), (4, 5, "kout"), (8, 0, "q4")])
+@pytest.mark.parametrize("P,load_mode,kind", [(2, 0, "iid"), (3, 1, "advfuture"), (4, 2, "kout"), (8, 0, "q4")])
 def test_context_split_partials_merge_to_oracle(P, load_mode, kind):
     """shard_mode 1 (SURVEY §8(e) variant): P ranks (emulated on one GPU, one context each) split a
     request by chunk depth (chunk c -> rank c % P, the suffix keys -> rank n_matched % P).  Every

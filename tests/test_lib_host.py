@@ -28,7 +28,7 @@ def test_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(pcr.PROTOTYPES) == declared
-    assert lib.pcr_abi_version() == 5
+    assert lib.pcr_abi_version() == 6
 
 
 def test_blake2b_rfc7693_vectors():
@@ -174,7 +174,7 @@ def test_invalid_configs():
     with pytest.raises(pcr.PcrError):
         pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, rank=1, world=4)  # world !| Hkv
     with pytest.raises(pcr.PcrError):
-        pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=6)          # no such load path
+        pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=5)          # no such load path (ABI v6: 0-4)
     with pytest.raises(pcr.PcrError):
         pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=4, load_ce_fraction=1.5)
     pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=4, load_ce_fraction=0.5).close()
@@ -187,7 +187,7 @@ def test_invalid_configs():
 
 
 def test_pcr_run_opts_layout_matches_header():
-    """The binding's ctypes structs mirror include/pcr.h (ABI v5): field order and offsets that the
+    """The binding's ctypes structs mirror include/pcr.h (ABI v6): field order and offsets that the
     C side reads (host_io / io_ring_layers in pcr_run_opts, load_ce_fraction in pcr_config)."""
     import ctypes
     assert [f for f, _ in pcr.PcrRunOpts._fields_][-4:] == ["mode", "host_io", "io_ring_layers", "partial_all"]

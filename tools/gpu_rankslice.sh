@@ -3,7 +3,7 @@
 # for each a2 mover.
 mkdir -p gpurun_out; export PYTHONUNBUFFERED=1
 OUT=gpurun_out/rankslice.jsonl; : > $OUT
-for P in 2 4 8; do for m in auto sm ce_batch; do
+for P in 2 4 8; do for m in sm ce_runs; do
   timeout 200 python bench.py --rank-slice $P --load-mode $m --steps 30 --warmup 5 --no-e2e --no-cpu-baseline >> $OUT 2>> gpurun_out/rankslice.err
 done; done
 python - <<'PY'

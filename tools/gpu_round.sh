@@ -10,7 +10,7 @@ timeout 240 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; tail -1
 timeout 400 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?"
 timeout 400 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
 OUT=gpurun_out/modes.jsonl; : > $OUT
-for m in auto sm ce_batch ce_blocks tma; do
+for m in sm ce_runs ce_blocks tma; do
   timeout 200 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --load-mode $m >> $OUT 2>> gpurun_out/modes.err
   timeout 300 python bench.py --workload M7 --ratio 0.5 --steps 10 --warmup 2 --no-e2e --no-cpu-baseline --load-mode $m >> $OUT 2>> gpurun_out/modes.err
 done
