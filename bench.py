@@ -19,7 +19,9 @@ request is processed by all ranks, so per-GPU work shrinks with N: scaling = "st
 from __future__ import annotations
 
 import argparse
+import copy
 import json
+import socket
 import os
 import shutil
 import statistics
@@ -61,6 +63,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-target-point", action="store_true",
+                    help="skip the M7 r=0.5 north_star sub-record of the default L8 line")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch-path check: bring up the ranks (gloo, no GPU), print them, exit")
     ap.add_argument("--gather-ctas", type=int, default=0, help="CTAs of the host->HBM gather (0 = library default)")
     ap.add_argument("--profile-steps", type=int, default=5, help="extra steps with per-layer events (after timing)")
     ap.add_argument("--window", type=int, default=4, help="look-ahead window W (Z trace)")
@@ -343,19 +349,12 @@ def h2d_peak_gbs(torch, nbytes=256 << 20, reps=10):
     return nbytes / (best * 1e-3) / 1e9
 
 
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
-
-    from paper_2603_23049_b200 import MODE_OVERLAP, MODE_SYNC, Context, comm_unique_id
+def measure(args, torch, dist, world, rank, local):
+    """One workload (args.workload / args.ratio) through the hot path on this rank's GPU; returns
+    the JSON line on rank 0 (None on the other ranks)."""
+    from paper_2603_23049_b200 import MODE_SYNC, Context, comm_unique_id
     from pcrgen import make_rng, randn_bf16
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl_geo, n_doc, n_query = WORKLOADS[args.workload]
     geo = geometry(wl_geo)
     L, Hq, Hkv, d, C, S = geo["L"], geo["Hq"], geo["Hkv"], geo["d"], geo["C"], geo["S_pg"]
@@ -512,7 +511,13 @@ def run_ours(args):
         ctx.release(rid, False)
         return t
 
+    if world > 1:
+        dist.barrier()      # every rank measures its own host link at the same time: the concurrent peak
     peak_h2d_before = h2d_peak_gbs(torch)
+    peaks_all = None
+    if world > 1:
+        peaks_all = [None] * world
+        dist.all_gather_object(peaks_all, peak_h2d_before)
     for _ in range(args.warmup):
         step(q_d, k_d, v_d, out_d)
     torch.cuda.synchronize()
@@ -651,6 +656,10 @@ def run_ours(args):
     # two in-order streams, identical layers: T* = t_ld + (L-1) max(t_ld, t_at) + t_at
     ttft_pred = gather_ms + (L - 1) * max(gather_ms, attn_ms) + attn_ms if attn_tflops else None
     value = args.steps * N / (total_ms * 1e-3)
+    # T*: the pipelined bound with every load and attention at its roofline
+    t_ld_r = load_bytes / (peak_h2d * 1e9) * 1e3
+    t_at_r = attn_flops / (bf16_peak * 1e12) * 1e3
+    t_star = t_ld_r + (L - 1) * max(t_ld_r, t_at_r) + t_at_r if (t_ld_r + t_at_r) > 0 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -659,9 +668,8 @@ def run_ours(args):
                "sample": f"{n_l} of {L} layers (pool load + append + fp64 suffix attention over all heads), "
                          f"extrapolated x{L}/{n_l}"}
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
+        ctx.close()
+        return None
     dominant = "kv_gather" if N1 and (attn_ms != attn_ms or gather_ms >= attn_ms) else "suffix_attn"
     # per-launch traffic of the dominant kernels from the committed ncu capture (profiles/)
     try:
@@ -733,7 +741,12 @@ def run_ours(args):
         "match_prefix_us": statistics.median(match_us),
         "gpu_launches": launches,
         "roofline": rl_gather if dominant == "kv_gather" else rl_attn,
+        "roofline_gather": rl_gather,
         "roofline_attn": rl_attn,
+        "t_star_ms": t_star, "ttft_over_t_star": statistics.median(step_ms) / t_star if t_star else None,
+        "h2d_peak_concurrent_gbs": None if peaks_all is None else {
+            "per_rank": peaks_all, "aggregate": float(sum(peaks_all)),
+            "note": "each rank's cudaMemcpyAsync H2D peak, all ranks measuring at once after a barrier"},
         "roofline_gather_sm": rl_sm,
         "load_path": {"ce_layer_loads": ce_layers, "sm_layer_loads": stats1["sm_layer_loads"] - stats0["sm_layer_loads"],
                       "ce_copies_per_layer": ce_copies_per_layer if ce_layers else 0},
@@ -741,7 +754,62 @@ def run_ours(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
-    print(json.dumps(line), flush=True)
+    ctx.close()
+    return line
+
+
+def north_star_point(m7):
+    """The north_star target point as a sub-record of the default line: M7 at r = 0.5,
+    the SM gather sharing the GPU with the attention (OVERLAP)."""
+    rg, ra = m7["roofline_gather"], m7["roofline_attn"]
+    ov = m7.get("overlap") or {}
+    return {"workload": m7["config"]["workload"], "ttft_ms": m7["ttft_ms"],
+            "load_gbs": rg["achieved"], "load_frac_of_h2d_peak": rg["frac"], "h2d_peak_gbs": rg["peak"],
+            "attn_tflops_in_pipeline": ra["achieved"] if ra else None,
+            "attn_frac_of_bf16_peak": ra["frac"] if ra else None, "bf16_peak_tflops": ra["peak"] if ra else None,
+            "hidden_load_pct": ov.get("hidden_load_pct"), "t_star_ms": m7["t_star_ms"],
+            "ttft_over_t_star": m7["ttft_over_t_star"],
+            "targets": {"load_frac": 0.8, "attn_frac": 0.5, "hidden_load_pct": 100.0},
+            "note": "north_star: per-layer reused-KV load >= 80% of the measured host->HBM peak, fully hidden behind "
+                    "suffix attention at >= 50% of bf16 tensor peak; T* = the pipelined bound with every load and "
+                    "attention at its roofline (SURVEY §8(d))"}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dry_run:   # launch-path check on CPU (tests): gloo, report the ranks that came up
+        if world > 1:
+            dist.init_process_group("gloo")
+        ranks = [None] * world
+        if world > 1:
+            dist.all_gather_object(ranks, {"rank": rank, "local_rank": local, "pid": os.getpid()})
+        else:
+            ranks = [{"rank": 0, "local_rank": 0, "pid": os.getpid()}]
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": ranks}), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    line = measure(args, torch, dist, world, rank, local)
+    if (args.workload == "L8" and not args.no_target_point and args.rank_slice == 1 and args.shard == "heads"
+            and not args.layer_body and not args.offload):
+        sub = copy.copy(args)
+        sub.workload, sub.ratio = "M7", 0.5
+        sub.steps, sub.warmup, sub.profile_steps = max(5, min(args.steps, 10)), 3, 3
+        sub.no_e2e = sub.no_cpu_baseline = True
+        m7 = measure(sub, torch, dist, world, rank, local)
+        if rank == 0:
+            line["north_star_point"] = north_star_point(m7)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
@@ -967,8 +1035,24 @@ def run_trace_z(args):
     print(json.dumps(line), flush=True)
 
 
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # --gpus N without a launcher: start N ranks (one process per GPU) with torchrun
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")   # NCCL's init lines (nranks) go to stderr
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd, env=env))
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     if args.impl == "reference":
         run_reference(args)
     elif args.workload == "Z":

@@ -37,3 +37,17 @@ def test_our_arm_fails_loudly_without_a_gpu():
     res = _bench("--workload", "T", "--steps", "1", "--warmup", "0", "--no-cpu-baseline", "--no-e2e")
     assert res.returncode != 0
     assert not [ln for ln in res.stdout.splitlines() if ln.startswith("{")]   # no bench line
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_gpus_n_self_launches_n_ranks(n):
+    """`bench.py --gpus N` without a launcher starts N ranks itself (torchrun, 127.0.0.1); the
+    dry run brings them up on gloo and rank 0 reports every rank (no GPU needed)."""
+    res = _bench("--gpus", str(n), "--dry-run")
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    j = json.loads(lines[0])
+    assert j["dry_run"] is True and j["n_gpus"] == n
+    assert sorted(r["rank"] for r in j["ranks"]) == list(range(n))
+    assert len({r["pid"] for r in j["ranks"]}) == n          # one process per rank
