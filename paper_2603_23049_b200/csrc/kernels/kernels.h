@@ -73,6 +73,14 @@ struct AttnParams {
   // the log2-domain LSE ([N2*hq]) -- instead of the bf16 output (merged across ranks later).
   float* part_o;
   float* part_lse;
+  // Fused a3 (non-null k_new/v_new, [N2][hkv][d] device): the attention reads the suffix keys
+  // straight from k_new/v_new (TMA) instead of the pool, and the CTAs of the last M-block write
+  // them into the request's pool pages (TMA stores from the same shared-memory tiles), so no
+  // separate append kernel runs.  Rows past N2 in the last page's final 64-row box are written as
+  // zeros; rows beyond that box are not touched (the attention never reads them).
+  const uint16_t* k_new;
+  const uint16_t* v_new;
+  int32_t cluster_reduce;   // set by the launcher: split-KV partials reduced over DSMEM in-kernel
 };
 
 // Merge n_parts partials (O normalised per part, log2-domain LSE; part s at o + s*o_stride and

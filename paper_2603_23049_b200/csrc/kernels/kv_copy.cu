@@ -5,9 +5,10 @@
 // every thread streams 16-byte vectors straight out of the mapped pinned host store over PCIe
 // Gen5 (zero-copy, ld.global.cs) and writes them, 16 bytes at a time, into the pool pages of
 // the request.  The same launch can also carry a few linear host->device copies (the layer's
-// q/k/v inputs on the host_io path), so one kernel per layer moves everything the layer needs.  Measured on this pool's B200 (tools/h2d_probe.cu): 8+ CTAs x 256 threads with
-// 4 loads in flight per thread reach 51.2 GB/s = 92% of the copy engine's 55.6 GB/s, so the
-// gather needs only a handful of SMs and leaves the rest to the concurrent attention.
+// q/k/v inputs on the host_io path), so one kernel per layer moves everything the layer needs.
+// Measured on this pool's B200 (tools/h2d_probe.cu): 8+ CTAs x 256 threads with 4 loads in
+// flight per thread reach 51.2 GB/s = 92% of the copy engine's 55.6 GB/s, so the gather needs
+// only a handful of SMs and leaves the rest to the concurrent attention.
 #include <algorithm>
 
 #include "kernels.h"
@@ -63,12 +64,10 @@ __global__ void __launch_bounds__(kThreads, 6) kv_gather_kernel(const uint4* __r
                                                              int32_t ppc_log2, LinearCopies lin) {
   const int lane = threadIdx.x & 31;
   const int32_t seg16 = g.S << row16_log2;
-  int64_t lin_seg[LinearCopies::kMax + 1];
-  lin_seg[0] = 0;
-#pragma unroll
-  for (int i = 0; i < LinearCopies::kMax; ++i)
-    lin_seg[i + 1] = lin_seg[i] + (i < lin.n ? (lin.n16[i] + seg16 - 1) / seg16 : 0);
-  const int64_t n_lin = lin_seg[LinearCopies::kMax];
+  static_assert(LinearCopies::kMax == 3, "segment prefix below");
+  const int64_t e1 = lin.n > 0 ? (lin.n16[0] + seg16 - 1) / seg16 : 0;
+  const int64_t e2 = e1 + (lin.n > 1 ? (lin.n16[1] + seg16 - 1) / seg16 : 0);
+  const int64_t n_lin = e2 + (lin.n > 2 ? (lin.n16[2] + seg16 - 1) / seg16 : 0);
   const int64_t n_seg = n_lin + ((int64_t(n_chunks) * g.Hkv * 2) << ppc_log2);
   const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
   for (int64_t seg = int64_t(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5); seg < n_seg; seg += warps) {
@@ -76,13 +75,11 @@ __global__ void __launch_bounds__(kThreads, 6) kv_gather_kernel(const uint4* __r
     uint4* dst;
     int64_t len16 = seg16;
     if (seg < n_lin) {
-      int i = 0;
-#pragma unroll
-      for (int j = 1; j < LinearCopies::kMax; ++j) i += seg >= lin_seg[j];
-      const int64_t off = (seg - lin_seg[i]) * seg16;
-      src = lin.src[i] + off;
-      dst = lin.dst[i] + off;
-      len16 = min(int64_t(seg16), lin.n16[i] - off);
+      const bool c1 = seg >= e1, c2 = seg >= e2;
+      const int64_t off = (seg - (c2 ? e2 : c1 ? e1 : 0)) * seg16;
+      src = (c2 ? lin.src[2] : c1 ? lin.src[1] : lin.src[0]) + off;
+      dst = (c2 ? lin.dst[2] : c1 ? lin.dst[1] : lin.dst[0]) + off;
+      len16 = min(int64_t(seg16), (c2 ? lin.n16[2] : c1 ? lin.n16[1] : lin.n16[0]) - off);
     } else {
       int64_t s16, p16;
       segment_addrs(seg - n_lin, 0, layer, g, ppc_log2, row16_log2, slots, pages, s16, p16);

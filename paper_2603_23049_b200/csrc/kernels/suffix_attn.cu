@@ -98,7 +98,12 @@ struct Layout {
   static constexpr int kK0 = kQ0 + (PCR_Q_TMEM ? 0 : kNQ * kQTile);   // (Q in TMEM: no smem Q)
   static constexpr int kV0 = kK0 + kStages * kKVTile;
   static constexpr int kBar = kV0 + kStages * kKVTile;
-  static constexpr int kBytes = kBar + 512;
+  // split-KV cluster reduce: this CTA's row LSEs and the merged LSEs (kNQ*128 floats each); the
+  // weighted partial O of the CTA ([kNQ*128][D] fp32, 16-byte chunks XOR-swizzled by row) reuses
+  // the K/V ring once every MMA has completed
+  static constexpr int kLse = kBar + 512;
+  static constexpr int kBytes = kLse + 2 * kNQ * kBlockM * 4;
+  static_assert(2 * kStages * kKVTile >= kNQ * kBlockM * D * 4, "cluster-reduce partials must fit the K/V ring");
   static constexpr int kAlloc = kBytes + 1024;  // slack for 1024-byte alignment
   // TMEM columns: S_{t,b} (Q tile t, buffer b) at (kSBuf*t+b)*64; [Q_t at kColQ + t*D/2 (bf16
   // pairs), PCR_Q_TMEM]; O_t at kColO + t*D.
@@ -110,8 +115,40 @@ struct Layout {
 struct Bars {
   uint64_t q_full, k_full[kStages], v_full[kStages], k_empty[kStages], v_empty[kStages];
   uint64_t s_full[kNQ][2], p_full[kNQ][2], o_done[kNQ], o_full;
+  uint64_t store_done;   // fused append: the producer's pool stores have finished reading smem
   uint32_t tmem_base;
 };
+
+// ---------------------------------------------------------------- cluster (DSMEM) helpers
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float ld_dsmem_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 ld_dsmem_f32x4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr) : "memory");
+  return v;
+}
+// TMA store of one box from shared memory into the pool (bulk-group completion)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* smem_src, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(smem_u32(smem_src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m, int32_t c0, int32_t c1,
                                             int32_t c2, uint64_t* bar) {
@@ -186,6 +223,7 @@ __device__ __forceinline__ void exp2_poly2(uint64_t x2, float& y0, float& y1) {
 template <int D>
 __global__ void __maxnreg__(136)
     suffix_attn_kernel(const __grid_constant__ CUtensorMap tmap_pool, const __grid_constant__ CUtensorMap tmap_q,
+                       const __grid_constant__ CUtensorMap tmap_kn, const __grid_constant__ CUtensorMap tmap_vn,
                        const AttnParams p) {
   using Lay = Layout<D>;
   extern __shared__ uint8_t smem_raw[];
@@ -226,10 +264,19 @@ __global__ void __maxnreg__(136)
       mbar_init(&bars->o_done[t], 1);
     }
     mbar_init(&bars->o_full, 1);
+    mbar_init(&bars->store_done, 1);
     fence_mbar_init();
     tma_prefetch_desc(&tmap_pool);
     tma_prefetch_desc(&tmap_q);
+    if (p.k_new) {
+      tma_prefetch_desc(&tmap_kn);
+      tma_prefetch_desc(&tmap_vn);
+    }
   }
+  // fused append: the CTAs of the last M-block (they see every key) write the suffix K/V tiles of
+  // their key range into the pool; every other CTA only reads them (from k_new/v_new)
+  const bool fold = p.k_new != nullptr;
+  const bool writer = fold && blockIdx.x / p.hkv == 0;
   if (warp == 2) tmem_alloc<kTmemCols>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
@@ -239,6 +286,8 @@ __global__ void __maxnreg__(136)
   // append kernel before it under PDL; q and the pool are read only after it has completed.
   grid_dep_wait();
   grid_dep_launch();
+
+  float ep_lse = -INFINITY, ep_inv_l = 0.f;   // cluster reduce: this softmax thread's row LSE and 1/l
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
@@ -262,29 +311,65 @@ __global__ void __maxnreg__(136)
 #if PCR_KV_L2HINT
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(kv_policy));
 #endif
+      // Pool row of K for box b of tile `tile` (V = + S), and whether the box holds suffix keys
+      // (fused append: read from k_new/v_new; `dst` = it has a pool page to be written to).
+      auto box_rows = [&](int tile, int b, int64_t& row, bool& sfx, bool& dst) {
+        const int key = (j_begin + tile) * kBlockN + b * box;
+        const bool in_req = key / p.S < p.n_req_pages;
+        const int pidx = in_req ? key / p.S : p.n_req_pages - 1;  // clamp: finite, masked
+        if (pidx < pg_base || pidx >= pg_base + 32) {
+          pg_base = pidx;
+          pg_val = pidx + lane < p.n_req_pages ? p.pages[pidx + lane] : 0;
+        }
+        const int64_t page = __shfl_sync(0xffffffffu, pg_val, pidx - pg_base);
+        row = int64_t(p.layer) * layer_rows + ((page * p.hkv + g) * 2 + 0) * p.S + (in_req ? key % p.S : 0);
+        sfx = fold && key >= p.n1;
+        dst = sfx && in_req;
+      };
+      // fused append: write the suffix boxes of tile `tile` (its K or V stage) into the pool
+      auto store_tile = [&](int tile, bool v) {
+        const int st = tile % kStages;
+        const uint8_t* base = smem + (v ? Lay::kV0 : Lay::kK0) + st * Lay::kKVTile;
+        bool any = false;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (b < n_box) {
+            int64_t row;
+            bool sfx, dst;
+            box_rows(tile, b, row, sfx, dst);
+            if (dst && lane == 0) {
+#pragma unroll
+              for (int hf = 0; hf < Lay::kHalves; ++hf)
+                tma_store_2d(&tmap_pool, base + hf * Lay::kKVHalf + b * box * 128, hf * 64,
+                             int32_t(row + (v ? p.S : 0)));
+            }
+            any |= dst;
+          }
+        }
+        if (any && lane == 0) {
+          bulk_commit();
+          bulk_wait_read0();   // the stage may be refilled once the stores have read it
+        }
+        __syncwarp();
+      };
       // K(j) and V(j) go into stage j % kStages once their previous occupants are consumed: K after
-      // the last QK^T that read it (k_empty), V after the last PV (v_empty).
+      // the last QK^T that read it (k_empty), V after the last PV (v_empty) -- and, in a writer CTA,
+      // after the previous occupant's suffix boxes have been stored into the pool.
       for (int it = 0; it < n_iter; ++it) {
         const int st = it % kStages;
         const uint32_t ph = ((it / kStages) - 1) & 1;
         int64_t row_k[4];
+        bool sfx[4], dst_unused;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          if (b < n_box) {
-            const int key = (j_begin + it) * kBlockN + b * box;
-            const bool in_req = key / p.S < p.n_req_pages;
-            const int pidx = in_req ? key / p.S : p.n_req_pages - 1;  // clamp: finite, masked
-            if (pidx < pg_base || pidx >= pg_base + 32) {
-              pg_base = pidx;
-              pg_val = pidx + lane < p.n_req_pages ? p.pages[pidx + lane] : 0;
-            }
-            const int64_t page = __shfl_sync(0xffffffffu, pg_val, pidx - pg_base);
-            row_k[b] = int64_t(p.layer) * layer_rows + ((page * p.hkv + g) * 2 + 0) * p.S + (in_req ? key % p.S : 0);
-          }
-        }
+        for (int b = 0; b < 4; ++b)
+          if (b < n_box) box_rows(it, b, row_k[b], sfx[b], dst_unused);
+        const int sfx_row0 = (j_begin + it) * kBlockN - p.n1;   // suffix row of box 0 (fused append)
         uint8_t* ks = smem + Lay::kK0 + st * Lay::kKVTile;
         uint8_t* vs = smem + Lay::kV0 + st * Lay::kKVTile;
-        if (it >= kStages) mbar_wait(&bars->k_empty[st], ph);
+        if (it >= kStages) {
+          mbar_wait(&bars->k_empty[st], ph);
+          if (writer) store_tile(it - kStages, false);
+        }
         if (elect_one()) {
           if (PCR_ATTN_PROFILE & 4) {
             mbar_arrive(&bars->k_full[st]);
@@ -294,13 +379,21 @@ __global__ void __maxnreg__(136)
             for (int b = 0; b < 4; ++b)
 #pragma unroll
               for (int hf = 0; hf < Lay::kHalves; ++hf)
-                if (b < n_box)
-                tma_load_2d_kv(ks + hf * Lay::kKVHalf + b * box * 128, &tmap_pool, hf * 64, int32_t(row_k[b]),
-                               &bars->k_full[st], kv_policy);
+                if (b < n_box) {
+                  if (sfx[b])
+                    tma_load_3d(ks + hf * Lay::kKVHalf + b * box * 128, &tmap_kn, hf * 64, g, sfx_row0 + b * box,
+                                &bars->k_full[st]);
+                  else
+                    tma_load_2d_kv(ks + hf * Lay::kKVHalf + b * box * 128, &tmap_pool, hf * 64, int32_t(row_k[b]),
+                                   &bars->k_full[st], kv_policy);
+                }
           }
         }
         __syncwarp();
-        if (it >= kStages) mbar_wait(&bars->v_empty[st], ph);
+        if (it >= kStages) {
+          mbar_wait(&bars->v_empty[st], ph);
+          if (writer) store_tile(it - kStages, true);
+        }
         if (elect_one()) {
           if (PCR_ATTN_PROFILE & 4) {
             mbar_arrive(&bars->v_full[st]);
@@ -310,14 +403,33 @@ __global__ void __maxnreg__(136)
             for (int b = 0; b < 4; ++b)
 #pragma unroll
               for (int hf = 0; hf < Lay::kHalves; ++hf)
-                if (b < n_box)
-                tma_load_2d_kv(vs + hf * Lay::kKVHalf + b * box * 128, &tmap_pool, hf * 64,
-                               int32_t(row_k[b] + p.S), &bars->v_full[st], kv_policy);
+                if (b < n_box) {
+                  if (sfx[b])
+                    tma_load_3d(vs + hf * Lay::kKVHalf + b * box * 128, &tmap_vn, hf * 64, g, sfx_row0 + b * box,
+                                &bars->v_full[st]);
+                  else
+                    tma_load_2d_kv(vs + hf * Lay::kKVHalf + b * box * 128, &tmap_pool, hf * 64,
+                                   int32_t(row_k[b] + p.S), &bars->v_full[st], kv_policy);
+                }
           }
         }
         __syncwarp();
       }
+      if (writer) {
+        // the last kStages tiles are never refilled: store their suffix boxes once they have landed
+        for (int it = max(0, n_iter - kStages); it < n_iter; ++it) {
+          const int st = it % kStages;
+          mbar_wait(&bars->k_full[st], (it / kStages) & 1);
+          store_tile(it, false);
+          mbar_wait(&bars->v_full[st], (it / kStages) & 1);
+          store_tile(it, true);
+        }
+        if (lane == 0) bulk_wait0();   // the pool writes are complete (visible after the grid)
+        __syncwarp();
+      }
     }
+    if (writer && elect_one()) mbar_arrive(&bars->store_done);
+    __syncwarp();
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     // Converged warp; one elected lane issues each MMA group; descriptor bases precomputed.
@@ -594,7 +706,13 @@ __global__ void __maxnreg__(136)
       tc_fence_after();
     }
     const float inv_l = (n_iter > 0 && l > 0.f) ? 1.f / l : 0.f;
-    if (p.n_splits == 1 && p.part_o == nullptr) {
+    if (p.cluster_reduce) {
+      // split-KV over a cluster: publish this row's LSE; the O rows are weighted and reduced over
+      // DSMEM below, once every CTA of the cluster has published its LSEs
+      ep_lse = (n_iter > 0 && l > 0.f) ? m_raw * p.scale_log2 + __log2f(l) : -INFINITY;
+      ep_inv_l = inv_l;
+      reinterpret_cast<float*>(smem + Lay::kLse)[t * kBlockM + r] = ep_lse;
+    } else if (p.n_splits == 1 && p.part_o == nullptr) {
       uint4* dst = reinterpret_cast<uint4*>(p.out + row_id * D);
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
@@ -638,6 +756,87 @@ __global__ void __maxnreg__(136)
             (n_iter > 0 && l > 0.f) ? m_raw * p.scale_log2 + __log2f(l) : -INFINITY;
     }
     tc_fence_before();
+  }
+  if (p.cluster_reduce) {
+    // ---------------------------------------------------------------- split-KV cluster reduce
+    // The n_splits CTAs of a cluster (cluster dims (1, 1, n_splits): rank == blockIdx.z) hold the
+    // partials of the same rows over disjoint key ranges.  (1) every row's merged weights from the
+    // n_splits LSEs, (2) each CTA writes its partial O row times its weight 2^(lse_s - M) / Z into
+    // its own shared memory, (3) CTA s sums its 1/n_splits share of the (row, 8 columns) units over
+    // the cluster's DSMEM and writes the output -- no workspace, no second kernel.
+    const int nsp = p.n_splits;
+    float* lse_own = reinterpret_cast<float*>(smem + Lay::kLse);
+    float* lse_merged = lse_own + kNQ * kBlockM;
+    cluster_sync_all();   // #1: every CTA's row LSEs are visible cluster-wide
+    if (warp >= 4) {
+      const int tr = threadIdx.x - 128;   // row of this CTA's kNQ * 128
+      float M = -INFINITY;
+      for (int sp = 0; sp < nsp; ++sp) M = fmaxf(M, ld_dsmem_f32(dsmem_addr(&lse_own[tr], sp)));
+      float Z = 0.f;
+      if (M != -INFINITY)
+        for (int sp = 0; sp < nsp; ++sp) Z += ex2(ld_dsmem_f32(dsmem_addr(&lse_own[tr], sp)) - M);
+      const float w = (M == -INFINITY || ep_lse == -INFINITY) ? 0.f : ex2(ep_lse - M) / Z;
+      lse_merged[tr] = M == -INFINITY ? -INFINITY : M + __log2f(Z);
+      if (writer) mbar_wait(&bars->store_done, 0);   // the K/V ring is no longer read by pool stores
+      float4* part = reinterpret_cast<float4*>(smem + Lay::kK0) + tr * (D / 4);
+      const float sc = w * ep_inv_l;
+      const uint32_t o_col = tmem + (uint32_t(((warp & 3) * 32)) << 16) + Lay::kColO + ((warp - 4) >> 2) * D;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        float o[32];
+        if (n_iter > 0) {
+          tmem_ld32(o_col + c * 32, o);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          part[(c * 8 + e) ^ (tr & (D / 4 - 1))] =
+              make_float4(o[4 * e] * sc, o[4 * e + 1] * sc, o[4 * e + 2] * sc, o[4 * e + 3] * sc);
+      }
+    }
+    cluster_sync_all();   // #2: every CTA's weighted partials are visible
+    constexpr int kUnits = kNQ * kBlockM * (D / 8);
+    const int per = (kUnits + nsp - 1) / nsp;
+    const int u_end = min(kUnits, int(blockIdx.z + 1) * per);
+    const uint32_t part_base = smem_u32(smem + Lay::kK0);
+    for (int u = int(blockIdx.z) * per + int(threadIdx.x); u < u_end; u += kThreads) {
+      const int row = u / (D / 8), grp = u % (D / 8);
+      const int tt = row / kBlockM, rr = row % kBlockM;
+      const int ii = i0 + tt * tok_per_tile + rr / G;
+      if (ii >= p.n2) continue;
+      const int64_t row_id = int64_t(ii) * p.hq + g * G + rr % G;
+      const int sw = row & (D / 4 - 1);
+      const uint32_t off0 = uint32_t(row * (D / 4) + ((2 * grp) ^ sw)) * 16;
+      const uint32_t off1 = uint32_t(row * (D / 4) + ((2 * grp + 1) ^ sw)) * 16;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+      for (int sp = 0; sp < nsp; ++sp) {
+        uint32_t ra, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(part_base + off0), "r"(sp));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(part_base + off1), "r"(sp));
+        const float4 x = ld_dsmem_f32x4(ra), y = ld_dsmem_f32x4(rb);
+        a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+        b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
+      }
+      if (p.part_o) {
+        float4* dst = reinterpret_cast<float4*>(p.part_o + row_id * D + grp * 8);
+        dst[0] = a;
+        dst[1] = b;
+        if (grp == 0) p.part_lse[row_id] = lse_merged[row];
+      } else {
+        const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        uint32_t wv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+          wv[e] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        *reinterpret_cast<uint4*>(p.out + row_id * D + grp * 8) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      }
+    }
+    cluster_sync_all();   // #3: no CTA leaves while its shared memory may still be read
   }
   __syncthreads();
   if (warp == 2) {
@@ -736,71 +935,132 @@ bool pdl_enabled() {
 }
 
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, int cluster_z,
                        Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster_z > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = 1;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = cluster_z;
+    ++n;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// Split-KV partials are reduced inside the attention kernel over a thread-block cluster (DSMEM)
+// unless PCR_SPLIT_CLUSTER=0 (then: fp32 workspace + combine kernel, the r01 path).
+bool split_cluster_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PCR_SPLIT_CLUSTER");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 template <int D>
 cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStream_t stream, int* launches) {
-  static bool configured = false;
+  static int max_cluster = 0;   // largest cluster (split count) that can be co-scheduled: 16 or 8
   auto kern = suffix_attn_kernel<D>;
-  if (!configured) {
+  if (!max_cluster) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Layout<D>::kAlloc);
     if (e != cudaSuccess) return e;
-    configured = true;
+    max_cluster = 8;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(1, 1, 16);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = Layout<D>::kAlloc;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 1;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 16;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n >= 1) max_cluster = 16;
+    }
+    cudaGetLastError();
   }
   AttnParams p = p0;
   const int G = p.hq / p.hkv;
-  // Q tensor map over q [N2][Hq][D]: box {64, G, 128/G} lands a Q tile as rows r = t*G + gg.
-  CUtensorMap tmap_q;
   EncodeTiledFn enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
-  cuuint64_t dims[3] = {cuuint64_t(D), cuuint64_t(p.hq), cuuint64_t(p.n2)};
-  cuuint64_t strides[2] = {cuuint64_t(D) * 2, cuuint64_t(p.hq) * D * 2};
-  cuuint32_t box[3] = {64, cuuint32_t(G), cuuint32_t(kBlockM / G)};
-  cuuint32_t estr[3] = {1, 1, 1};
-  if (enc(&tmap_q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(p.q), dims, strides, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return cudaErrorInvalidValue;
+  // Q tensor map over q [N2][Hq][D]: box {64, G, 128/G} lands a Q tile as rows r = t*G + gg.
+  CUtensorMap tmap_q, tmap_kn, tmap_vn;
+  {
+    cuuint64_t dims[3] = {cuuint64_t(D), cuuint64_t(p.hq), cuuint64_t(p.n2)};
+    cuuint64_t strides[2] = {cuuint64_t(D) * 2, cuuint64_t(p.hq) * D * 2};
+    cuuint32_t box[3] = {64, cuuint32_t(G), cuuint32_t(kBlockM / G)};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&tmap_q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(p.q), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  tmap_kn = tmap_vn = tmap_q;   // (unused unless the append is fused)
+  if (p.k_new) {
+    // suffix K / V [N2][hkv][D]: box {64, 1, pool box rows} lands exactly like a pool box; rows past
+    // N2 are zero-filled by the TMA unit
+    cuuint64_t dims[3] = {cuuint64_t(D), cuuint64_t(p.hkv), cuuint64_t(p.n2)};
+    cuuint64_t strides[2] = {cuuint64_t(D) * 2, cuuint64_t(p.hkv) * D * 2};
+    cuuint32_t box[3] = {64, 1, cuuint32_t(std::min(p.S, kBlockN))};
+    cuuint32_t estr[3] = {1, 1, 1};
+    for (int kv = 0; kv < 2; ++kv)
+      if (enc(kv ? &tmap_vn : &tmap_kn, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+              const_cast<uint16_t*>(kv ? p.v_new : p.k_new), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+  }
   const int tok_per_cta = kNQ * kBlockM / G;
   const int n_mblocks = (p.n2 + tok_per_cta - 1) / tok_per_cta;
   // Split-KV when the (m-block x kv-head) grid leaves SMs idle; each split keeps >= 2 key tiles.
   const int ctas = n_mblocks * p.hkv;
   const int max_tiles = (p.n1 + p.n2 + kBlockN - 1) / kBlockN;
+  const bool cluster_ok = split_cluster_enabled();
   int splits = 1;
-  if (p.ws_o && ctas < 148) {   // (kv_len < n1 + n2 only shortens the key range: fewer tiles)
+  if ((p.ws_o || cluster_ok) && ctas < 148) {   // (kv_len < n1 + n2 only shortens the key range: fewer tiles)
     splits = std::max(1, 148 / ctas);
     splits = std::min(splits, std::max(1, max_tiles / PCR_SPLIT_MIN_TILES));
-    const int64_t per_split_bytes = int64_t(p.n2) * p.hq * (D + 1) * 4;
-    splits = int(std::min<int64_t>(splits, std::max<int64_t>(1, p.ws_bytes / per_split_bytes)));
+    if (cluster_ok) {
+      splits = std::min(splits, max_cluster);
+    } else {
+      const int64_t per_split_bytes = int64_t(p.n2) * p.hq * (D + 1) * 4;
+      splits = int(std::min<int64_t>(splits, std::max<int64_t>(1, p.ws_bytes / per_split_bytes)));
+    }
   }
   p.n_splits = splits;
+  p.cluster_reduce = (splits > 1 && cluster_ok) ? 1 : 0;
   if (p.part_o && splits == 1) {   // one split: the kernel writes the partial itself
     p.ws_o = p.part_o;
     p.ws_lse = p.part_lse;
   }
   dim3 grid(n_mblocks * p.hkv, 1, splits);
-  cudaError_t e = launch_pdl(kern, grid, dim3(kThreads), Layout<D>::kAlloc, stream, *tmap_pool, tmap_q, p);
+  cudaError_t e = launch_pdl(kern, grid, dim3(kThreads), Layout<D>::kAlloc, stream, p.cluster_reduce ? splits : 1,
+                             *tmap_pool, tmap_q, tmap_kn, tmap_vn, p);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   *launches += 1;
-  if (splits > 1) {
+  if (splits > 1 && !p.cluster_reduce) {
     const int64_t rows_total = int64_t(p.n2) * p.hq;
     int64_t blocks = (rows_total * (D / 8) + 255) / 256;
     blocks = std::min<int64_t>(blocks, 148 * 8);
-    e = launch_pdl(combine_kernel<D>, dim3(int(blocks)), dim3(256), 0, stream, (const float*)p.ws_o,
+    e = launch_pdl(combine_kernel<D>, dim3(int(blocks)), dim3(256), 0, stream, 1, (const float*)p.ws_o,
                    rows_total * D, (const float*)p.ws_lse, rows_total, p.out, p.part_o, p.part_lse, rows_total,
                    splits);
     if (e == cudaSuccess) e = cudaGetLastError();

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -158,6 +159,13 @@ int32_t* d_own_slots_of(pcr_ctx* c, const Request* r) { return d_slots_of(c, r) 
 int32_t* d_vpages_of(pcr_ctx* c, const Request* r) { return d_own_slots_of(c, r) + c->chunk_cap; }
 int32_t* d_own_res_slots_of(pcr_ctx* c, const Request* r) { return d_vpages_of(c, r) + c->region_page_cap; }
 int32_t* d_own_res_pages_of(pcr_ctx* c, const Request* r) { return d_own_res_slots_of(c, r) + c->chunk_cap; }
+bool fused_append_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PCR_FUSED_APPEND");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 bool owns_chunk(const pcr_ctx* c, int32_t depth) { return !c->ctx_split || depth % c->cfg.world == c->cfg.rank; }
 
 // First device call of a request uploads its page/slot tables; later calls (on any stream)
@@ -320,8 +328,19 @@ pcr_status enqueue_attn(pcr_ctx* c, Request* r, int32_t layer, const void* q, co
   const int64_t n1 = c->ctx_split ? int64_t(r->ctx_n_own) * c->cfg.chunk_tokens : r->plan.n1, n2 = r->plan.n2;
   const int32_t n_pages = c->ctx_split ? r->ctx_n_vpages : static_cast<int32_t>(r->plan.pages.size());
   const int32_t* pages = c->ctx_split ? d_vpages_of(c, r) : d_pages_of(c, r);
-  CUDA_TRY(c, pcr::launch_kv_append(k, v, c->cfg.pool, pages, n1, n2, n_pages, layer, c->geom, s));
+  // a3: fused into the attention (its last M-block's CTAs store the suffix K/V tiles they read into
+  // the pool) -- except under the context split, where every rank appends the suffix (its reserved
+  // chunks are offloaded from there) but only one attends to it, and with PCR_FUSED_APPEND=0
+  const bool fused = !c->ctx_split && fused_append_enabled();
+  if (!fused) {
+    CUDA_TRY(c, pcr::launch_kv_append(k, v, c->cfg.pool, pages, n1, n2, n_pages, layer, c->geom, s));
+    c->launches += 1;
+  }
   pcr::AttnParams p{};
+  if (fused) {
+    p.k_new = static_cast<const uint16_t*>(k);
+    p.v_new = static_cast<const uint16_t*>(v);
+  }
   p.q = static_cast<const uint16_t*>(q);
   p.out = static_cast<uint16_t*>(out);
   p.pages = pages;
@@ -348,7 +367,7 @@ pcr_status enqueue_attn(pcr_ctx* c, Request* r, int32_t layer, const void* q, co
   p.ws_bytes = c->ws_floats * 4;
   int n = 0;
   cudaError_t e = pcr::launch_suffix_attn(&c->tmap, p, c->cfg.head_dim, s, &n);
-  c->launches += 1 + n;
+  c->launches += n;
   if (e != cudaSuccess) return cuda_fail(c, e, "launch_suffix_attn");
   return PCR_OK;
 }

@@ -534,11 +534,51 @@ def test_context_split_partials_merge_to_oracle(P, load_mode, kind):
 
 _PDL_SCRIPT = """
 import sys, zlib
+import numpy as np
 sys.path.insert(0, {root!r})
 from tests.test_gpu_parity import _single_request
 rig, plan, q, k, v, out = _single_request("iid", 3, 32, 8, 128, 256, 64, 1024, 130, seed=5)
+np.save({out_path!r}, out)
+np.save({pool_path!r}, rig.pool_np())
 print("CRC", zlib.crc32(out.tobytes()))
 """
+
+
+def _run_variant(env_over, tmp_path):
+    """The 3-layer L8-geometry request (split-KV at this shape) in a subprocess with experiment env
+    switches; returns its output and pool arrays."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out_p, pool_p = str(tmp_path / "out.npy"), str(tmp_path / "pool.npy")
+    res = subprocess.run([sys.executable, "-c", _PDL_SCRIPT.format(root=root, out_path=out_p, pool_path=pool_p)],
+                         env=dict(os.environ, **env_over), capture_output=True, text=True, timeout=300, cwd=root)
+    assert res.returncode == 0, res.stderr[-2000:]
+    return np.load(out_p), np.load(pool_p)
+
+
+def test_fused_append_and_cluster_reduce_match_the_unfused_path(tmp_path):
+    """The default attention (suffix K/V read from k_new/v_new and stored into the pool by the
+    kernel; split-KV partials reduced over a thread-block cluster's DSMEM) against the r01 path
+    (separate append kernel; fp32 workspace + combine kernel): the pool is bit-identical (the
+    whole array), the output identical within the split-KV merge's rounding (different summation
+    order), and both within the oracle tolerance."""
+    L, N1, N2 = 3, 1024, 130
+    rig, plan, q, k, v, out = _single_request("iid", L, 32, 8, 128, 256, 64, N1, N2, seed=5)
+    out_old, pool_old = _run_variant({"PCR_FUSED_APPEND": "0", "PCR_SPLIT_CLUSTER": "0"}, tmp_path)
+    pool = rig.pool_np()
+    # the unfused append also zero-fills rows past N1+N2 of the last page; the fused one writes
+    # only the final 64-row box (zeros past N2), which here ends the page: identical arrays
+    assert np.array_equal(pool, pool_old)
+    a, b = bf16_bits_to_f64(out), bf16_bits_to_f64(out_old)
+    assert rel_l2(a, b) <= 2e-3 and np.abs(a - b).max() <= 1e-2
+    for l in range(L):
+        kc, vc = rig.expected_context(plan, k[:, N1:], v[:, N1:], l)
+        r, m = check_attention(out[l], q[l], kc, vc, N1, blocked=True)
+        assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (l, r, m)
+    out_fa, _ = _run_variant({"PCR_FUSED_APPEND": "0"}, tmp_path)     # only the append differs
+    assert np.array_equal(out_fa, out)
 
 
 def test_programmatic_dependent_launch_off_is_bitwise_identical():
@@ -550,8 +590,9 @@ def test_programmatic_dependent_launch_off_is_bitwise_identical():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     _, _, _, _, _, out = _single_request("iid", 3, 32, 8, 128, 256, 64, 1024, 130, seed=5)
     env = dict(os.environ, PCR_PDL="0")
-    res = subprocess.run([sys.executable, "-c", _PDL_SCRIPT.format(root=root)], env=env, capture_output=True,
-                         text=True, timeout=300, cwd=root)
+    res = subprocess.run([sys.executable, "-c", _PDL_SCRIPT.format(root=root, out_path="/tmp/pcr_pdl_out.npy",
+                                                               pool_path="/tmp/pcr_pdl_pool.npy")],
+                         env=env, capture_output=True, text=True, timeout=300, cwd=root)
     assert res.returncode == 0, res.stderr[-2000:]
     crc = int([ln for ln in res.stdout.splitlines() if ln.startswith("CRC")][0].split()[1])
     assert crc == zlib.crc32(out.tobytes())
