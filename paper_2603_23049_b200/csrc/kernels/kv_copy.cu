@@ -10,6 +10,7 @@
 // flight per thread reach 51.2 GB/s = 92% of the copy engine's 55.6 GB/s, so the gather needs
 // only a handful of SMs and leaves the rest to the concurrent attention.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "sm100_ptx.cuh"
@@ -236,7 +237,16 @@ cudaError_t launch_kv_gather(const void* store, void* pool, const int32_t* d_slo
   }
   if (n_seg <= 0) return cudaSuccess;
   const int64_t ctas = std::min<int64_t>(target_ctas, (n_seg + kThreads / 32 - 1) / (kThreads / 32));
-  kv_gather_kernel<<<int(ctas), kThreads, 0, stream>>>(static_cast<const uint4*>(store), static_cast<uint4*>(pool),
+  // experiment (PCR_GATHER_SMEM=bytes): reserve dynamic shared memory the kernel does not use, so
+  // a gather CTA cannot share an SM with an attention CTA (~194 KB) -- the SMs split instead
+  static const int smem = [] {
+    const char* e = std::getenv("PCR_GATHER_SMEM");
+    int v = e ? std::atoi(e) : 0;
+    v = std::max(0, std::min(v, 200 << 10));
+    if (v > (48 << 10)) cudaFuncSetAttribute(kv_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+    return v;
+  }();
+  kv_gather_kernel<<<int(ctas), kThreads, smem, stream>>>(static_cast<const uint4*>(store), static_cast<uint4*>(pool),
                                                        d_slots, d_pages, std::max(n_matched, 0), layer, g,
                                                        ilog2(g.d / 8), ilog2(g.C / g.S), l);
   return cudaGetLastError();

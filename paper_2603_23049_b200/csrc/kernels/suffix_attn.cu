@@ -961,40 +961,61 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
-// Split-KV partials are reduced inside the attention kernel over a thread-block cluster (DSMEM)
-// unless PCR_SPLIT_CLUSTER=0 (then: fp32 workspace + combine kernel, the r01 path).
+// Experiment (PCR_SPLIT_CLUSTER=1): split-KV partials reduced inside the attention kernel over a
+// thread-block cluster (DSMEM) instead of the fp32 workspace + combine kernel.  Measured slower on
+// this pool's B200 (profiles/r02_split_cluster.txt): only 15 clusters of 8 fit at once (GPC sizes),
+// and the in-kernel epilogue costs more than the combine launch it saves, so it is off by default.
 bool split_cluster_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PCR_SPLIT_CLUSTER");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }
 
+// SMs the split-KV sizing may count on (PCR_ATTN_SMS; default all 148).
+int attn_sm_budget() {
+  static const int n = [] {
+    const char* e = std::getenv("PCR_ATTN_SMS");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 && v <= 148 ? v : 148;
+  }();
+  return n;
+}
+
 template <int D>
 cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStream_t stream, int* launches) {
-  static int max_cluster = 0;   // largest cluster (split count) that can be co-scheduled: 16 or 8
+  // act[s] = clusters of s CTAs (one per SM: ~194 KB smem) that can be resident at once, s <= 16.
+  // GPCs differ in SM count, so e.g. 16 clusters of 9 may not fit in one wave while 16 of 8 do.
+  static int act[17] = {0};
+  static bool configured = false;
   auto kern = suffix_attn_kernel<D>;
-  if (!max_cluster) {
+  if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Layout<D>::kAlloc);
     if (e != cudaSuccess) return e;
-    max_cluster = 8;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+    const bool np = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+    for (int cs = 1; cs <= (np ? 16 : 8); ++cs) {
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(1, 1, 16);
+      cfg.gridDim = dim3(1, 1, cs);
       cfg.blockDim = dim3(kThreads);
       cfg.dynamicSmemBytes = Layout<D>::kAlloc;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
       attr[0].val.clusterDim.x = 1;
       attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 16;
+      attr[0].val.clusterDim.z = cs;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n >= 1) max_cluster = 16;
+      act[cs] = cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess ? n : 0;
     }
     cudaGetLastError();
+    if (const char* dbg = std::getenv("PCR_DEBUG"); dbg && dbg[0] == '1') {
+      std::fprintf(stderr, "suffix_attn<%d> max active clusters by size:", D);
+      for (int cs = 1; cs <= 16; ++cs) std::fprintf(stderr, " %d:%d", cs, act[cs]);
+      std::fprintf(stderr, "\n");
+    }
+    configured = true;
   }
   AttnParams p = p0;
   const int G = p.hq / p.hkv;
@@ -1034,11 +1055,15 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
   const int max_tiles = (p.n1 + p.n2 + kBlockN - 1) / kBlockN;
   const bool cluster_ok = split_cluster_enabled();
   int splits = 1;
-  if ((p.ws_o || cluster_ok) && ctas < 148) {   // (kv_len < n1 + n2 only shortens the key range: fewer tiles)
-    splits = std::max(1, 148 / ctas);
+  const int sms = attn_sm_budget();
+  if ((p.ws_o || cluster_ok) && ctas < sms) {   // (kv_len < n1 + n2 only shortens the key range: fewer tiles)
+    splits = std::max(1, sms / ctas);
     splits = std::min(splits, std::max(1, max_tiles / PCR_SPLIT_MIN_TILES));
     if (cluster_ok) {
-      splits = std::min(splits, max_cluster);
+      // the largest cluster size whose clusters all fit in one wave beside each other
+      const char* cap = std::getenv("PCR_MAX_CLUSTER");
+      splits = std::min(splits, cap ? std::max(1, std::atoi(cap)) : 16);
+      while (splits > 1 && act[splits] < ctas) --splits;
     } else {
       const int64_t per_split_bytes = int64_t(p.n2) * p.hq * (D + 1) * 4;
       splits = int(std::min<int64_t>(splits, std::max<int64_t>(1, p.ws_bytes / per_split_bytes)));

@@ -560,25 +560,27 @@ def _run_variant(env_over, tmp_path):
 
 def test_fused_append_and_cluster_reduce_match_the_unfused_path(tmp_path):
     """The default attention (suffix K/V read from k_new/v_new and stored into the pool by the
-    kernel; split-KV partials reduced over a thread-block cluster's DSMEM) against the r01 path
-    (separate append kernel; fp32 workspace + combine kernel): the pool is bit-identical (the
-    whole array), the output identical within the split-KV merge's rounding (different summation
-    order), and both within the oracle tolerance."""
+    kernel itself) against the separate append kernel (PCR_FUSED_APPEND=0): output and the whole
+    pool bit-identical.  The experimental cluster split-KV reduce (PCR_SPLIT_CLUSTER=1: partials
+    merged over DSMEM in-kernel) gives the same pool and the output within the split merge's
+    rounding (another summation order), inside the oracle tolerance."""
     L, N1, N2 = 3, 1024, 130
     rig, plan, q, k, v, out = _single_request("iid", L, 32, 8, 128, 256, 64, N1, N2, seed=5)
-    out_old, pool_old = _run_variant({"PCR_FUSED_APPEND": "0", "PCR_SPLIT_CLUSTER": "0"}, tmp_path)
     pool = rig.pool_np()
+    out_fa, pool_fa = _run_variant({"PCR_FUSED_APPEND": "0"}, tmp_path)
     # the unfused append also zero-fills rows past N1+N2 of the last page; the fused one writes
-    # only the final 64-row box (zeros past N2), which here ends the page: identical arrays
-    assert np.array_equal(pool, pool_old)
-    a, b = bf16_bits_to_f64(out), bf16_bits_to_f64(out_old)
+    # the final 64-row box (zeros past N2), which here ends the page: identical arrays
+    assert np.array_equal(out_fa, out)
+    assert np.array_equal(pool, pool_fa)
+    out_cl, pool_cl = _run_variant({"PCR_SPLIT_CLUSTER": "1"}, tmp_path)
+    assert np.array_equal(pool, pool_cl)
+    a, b = bf16_bits_to_f64(out), bf16_bits_to_f64(out_cl)
     assert rel_l2(a, b) <= 2e-3 and np.abs(a - b).max() <= 1e-2
     for l in range(L):
         kc, vc = rig.expected_context(plan, k[:, N1:], v[:, N1:], l)
-        r, m = check_attention(out[l], q[l], kc, vc, N1, blocked=True)
-        assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (l, r, m)
-    out_fa, _ = _run_variant({"PCR_FUSED_APPEND": "0"}, tmp_path)     # only the append differs
-    assert np.array_equal(out_fa, out)
+        for o in (out, out_cl):
+            r, m = check_attention(o[l], q[l], kc, vc, N1, blocked=True)
+            assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (l, r, m)
 
 
 def test_programmatic_dependent_launch_off_is_bitwise_identical():
