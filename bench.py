@@ -737,7 +737,7 @@ def measure(args, torch, dist, world, rank, local):
         "ttft_pred_ms": ttft_pred, "sync_bound_ms": L * (gather_ms + attn_ms) if attn_tflops else None,
         "gather_ms_per_layer": gather_ms,
         "gather_ms_per_layer_evented": gather_ms_evented if attn_tflops else None,
-        "attn_ms_per_layer": attn_ms if attn_tflops else None, "gather_ctas": args.gather_ctas or 16,
+        "attn_ms_per_layer": attn_ms if attn_tflops else None, "gather_ctas": args.gather_ctas or 8,
         "match_prefix_us": statistics.median(match_us),
         "gpu_launches": launches,
         "roofline": rl_gather if dominant == "kv_gather" else rl_attn,

@@ -23,6 +23,10 @@ namespace {
 // layer l+1 are never queued behind the attention grid of layer l.
 constexpr int kThreads = 256;
 constexpr int kUnroll = 4;
+// The gather keeps 4 loads of 16 bytes in flight per lane: 128 KiB for the default 8 CTAs, about
+// the host link's bandwidth-latency product (~51 GB/s x ~2.5 us); 8 unrolled loads need more than
+// the 40 registers that let a gather CTA share an SM with an attention CTA (they spill).
+constexpr int kGatherUnroll = 4;
 
 __device__ __forceinline__ uint4 ld_host_stream(const uint4* p) {
   uint4 v;
@@ -87,13 +91,13 @@ __global__ void __launch_bounds__(kThreads, 6) kv_gather_kernel(const uint4* __r
       src = store + s16;
       dst = pool + p16;
     }
-    for (int64_t base = lane; base < len16; base += 32 * kUnroll) {
-      uint4 v[kUnroll];
+    for (int64_t base = lane; base < len16; base += 32 * kGatherUnroll) {
+      uint4 v[kGatherUnroll];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
+      for (int u = 0; u < kGatherUnroll; ++u)
         if (base + 32 * u < len16) v[u] = ld_host_stream(src + base + 32 * u);
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
+      for (int u = 0; u < kGatherUnroll; ++u)
         if (base + 32 * u < len16) dst[base + 32 * u] = v[u];
     }
   }

@@ -54,7 +54,7 @@ struct pcr_ctx {
   int64_t launches = 0;
   int64_t ce_copies = 0, ce_layer_loads = 0, sm_layer_loads = 0;   // a2 load-path counters (pcr_stats)
   pcr::KvGeom geom{};
-  int32_t gather_ctas = 16;
+  int32_t gather_ctas = 8;   // (profiles/r02_sm_partition.txt: 8 CTAs load as fast as 16, and slow the attention beside them less)
   // split-KV workspace, one slice of ws_region_floats per plan region: ws_floats partial-O
   // floats followed by the LSE floats
   float* ws = nullptr;
