@@ -84,6 +84,9 @@ def parse():
                                               "Poisson arrivals at rho x the measured service rate")
     ap.add_argument("--ssd-frac", type=float, default=0.0, help="Z: SSD tier size / distinct chunks (0 = none)")
     ap.add_argument("--ssd-path", default="/tmp/pcr_ssd_tier.bin", help="Z: SSD tier file")
+    ap.add_argument("--z-windows", default="", help="Z sweep: comma list of look-ahead windows (one line per pass)")
+    ap.add_argument("--z-store-fracs", default="", help="Z sweep: comma list of DRAM store fractions")
+    ap.add_argument("--z-log", default="", help="Z: directory for per-pass plan logs (oracle replay)")
     ap.add_argument("--ce-frac", type=float, default=0.5, help="--load-mode hybrid: copy-engine share of the chunks")
     ap.add_argument("--shard", default="heads", choices=["heads", "context"],
                     help="how P GPUs (or --rank-slice P) split a request: KV heads (north_star) or the "
@@ -884,44 +887,50 @@ def _z_request_with_body(torch, ctx, rid, n2, geo, body, out, cs, ls, os_):
     cs.wait_stream(os_)
 
 
-def _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=None, body=None):
+def _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=None, body=None, window=None):
     """One pass of the Z trace on a fresh Context (cold store).  queue=None: every request is
     waiting from the start (saturated queue, pending = next W); else a VirtualQueue.
     body: the f3 layer body around the attention (per-layer calls); args.no_reuse: nothing is
-    cacheable (every request recomputes its whole context: the no-PCR baseline)."""
+    cacheable (every request recomputes its whole context: the no-PCR baseline).
+    --rank-slice P: the per-GPU work of rank 0 of a P-GPU KV-head-sharded run (its head slice of
+    every chunk; the host decisions are the same on every rank).  Every pcr_match_prefix input
+    (pending ids) and its decisions are logged in r["log"] for the oracle replay."""
     from paper_2603_23049_b200 import MODE_OVERLAP, Context
     geo = geometry("L8")
     L, Hq, Hkv, d, C, S = geo["L"], geo["Hq"], geo["Hkv"], geo["d"], geo["C"], geo["S_pg"]
+    P = max(1, args.rank_slice)
+    hq, hkv = Hq // P, Hkv // P
+    W = args.window if window is None else window
     max_n = max(len(r) for r in reqs)
     t0 = time.perf_counter()
-    ctx = Context(L, Hq, Hkv, d, C, S, cap, args.window, device=0, pool=pool, max_tokens=max_n,
+    ctx = Context(L, Hq, Hkv, d, C, S, cap, W, device=0, pool=pool, max_tokens=max_n, rank=0, world=P,
                   gather_ctas=args.gather_ctas, ssd_path=args.ssd_path if ssd_chunks else None,
-                  ssd_chunks=ssd_chunks,
-                  load_mode=LOAD_MODES[args.load_mode],
-                  load_ce_fraction=args.ce_frac)
+                  ssd_chunks=ssd_chunks, load_mode=LOAD_MODES[args.load_mode], load_ce_fraction=args.ce_frac)
     t_pin = time.perf_counter() - t0
     q_d, k_d, v_d, o_d = bufs
     cs, ls, os_ = torch.cuda.Stream(), torch.cuda.Stream(priority=-1), torch.cuda.Stream()
     for i, (t, n) in enumerate(zip(reqs, ndoc)):
         ctx.submit(i, t, 0 if args.no_reuse else n)
     r = {"ttft": [], "wall": [], "ttft_q": [], "pending": [], "hits": 0, "chunks": 0, "toks": 0, "n1s": [],
-         "plan_us": [], "t_pin": t_pin}
+         "plan_us": [], "t_pin": t_pin, "log": []}
     launches0 = ctx.kernel_launches
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     ev0.record(cs)
     for i in range(len(reqs)):
-        pend = queue.start(i) if queue else list(range(i + 1, min(len(reqs), i + 1 + args.window)))
+        pend = queue.start(i) if queue else list(range(i + 1, min(len(reqs), i + 1 + W)))
         r["pending"].append(len(pend))
         tp = time.perf_counter()
         plan = ctx.match_prefix(i, pend)
         r["plan_us"].append((time.perf_counter() - tp) * 1e6)
+        r["log"].append({"i": i, "pend": pend, "nm": plan["n_matched"], "nr": plan["n_reserved"],
+                         "slots": plan["slots"], "ev": [s_ for _, s_ in plan["evicted"]], "ssd": plan["n_from_ssd"]})
         n2 = plan["n2"]
         # contiguous [L][N2][H][d] views over the front of the max-size buffers
-        q = q_d.view(-1)[: L * n2 * Hq * d].view(L, n2, Hq, d)
-        k = k_d.view(-1)[: L * n2 * Hkv * d].view(L, n2, Hkv, d)
-        v = v_d.view(-1)[: L * n2 * Hkv * d].view(L, n2, Hkv, d)
-        o = o_d.view(-1)[: L * n2 * Hq * d].view(L, n2, Hq, d)
+        q = q_d.view(-1)[: L * n2 * hq * d].view(L, n2, hq, d)
+        k = k_d.view(-1)[: L * n2 * hkv * d].view(L, n2, hkv, d)
+        v = v_d.view(-1)[: L * n2 * hkv * d].view(L, n2, hkv, d)
+        o = o_d.view(-1)[: L * n2 * hq * d].view(L, n2, hq, d)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(cs)
         ls.wait_event(a)
@@ -950,89 +959,130 @@ def _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=None, bo
     return r
 
 
+def _write_plan_log(path, header, log):
+    """gzip JSON lines: the pass header, then one record per pcr_match_prefix call (its inputs and
+    decisions) -- replayed through the oracle by tests/test_z_replay.py."""
+    import gzip
+    os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+    with gzip.open(path, "wt") as f:
+        f.write(json.dumps(header) + "\n")
+        for rec in log:
+            f.write(json.dumps(rec, separators=(",", ":")) + "\n")
+
+
 def run_trace_z(args):
     """configs[4]: the Zipf RAG trace end to end on one GPU (look-ahead LRU + layer overlap +
     layer-wise offload of new chunks on a third stream, committed at release).  One step = one
     request; value = trace context tokens / device time; TTFT per request from CUDA events.
     --rho r1,r2,...: after the saturated pass (which measures the mean service time), one more
     pass per rho with Poisson arrivals at rho x that service rate (virtual-time FIFO queue; TTFT
-    then includes queueing)."""
+    then includes queueing).  --z-windows / --z-store-fracs: a sweep, one JSON line per pass
+    (SURVEY §8(d) preset Z: W in {0, 2, 4, 6, 8} x store {10, 25, 50}%).  --z-log DIR: every pass's
+    pcr_match_prefix inputs and decisions, for the oracle replay (tests/test_z_replay.py)."""
     import torch
 
     from pcrgen import make_rng, randn_bf16, zipf_trace
     torch.cuda.set_device(0)
     geo = geometry("L8")
     L, Hq, Hkv, d, C, S = geo["L"], geo["Hq"], geo["Hkv"], geo["d"], geo["C"], geo["S_pg"]
+    P = max(1, args.rank_slice)
+    hq, hkv = Hq // P, Hkv // P
     reqs, _, ndoc = zipf_trace(seed=4, n_requests=args.requests, C=C)
     distinct = set()
     for r, n in zip(reqs, ndoc):
         for c in range(n // C):
             distinct.add(r[: (c + 1) * C].tobytes())
-    cap = max(8, int(args.store_frac * len(distinct)))
     max_n = max(len(r) for r in reqs)
     pages_req = -(-max_n // S)
-    page_elems = L * Hkv * 2 * S * d
-    pool = torch.empty(2 * pages_req * page_elems + page_elems, dtype=torch.int16, device="cuda")
+    page_elems = L * hkv * 2 * S * d
+    n_pool_pages = 2 * pages_req + 1
+    pool = torch.empty(n_pool_pages * page_elems, dtype=torch.int16, device="cuda")
     ssd_chunks = int(args.ssd_frac * len(distinct))
+    rec = L * hkv * 2 * C * d * 2
     if ssd_chunks:
         # the tier file is pre-sized: refuse (loudly) rather than fill the disk
-        rec = L * Hkv * 2 * C * d * 2
         free = shutil.disk_usage(os.path.dirname(os.path.abspath(args.ssd_path))).free
         if ssd_chunks * rec > 0.8 * free:
             sys.exit(f"bench: SSD tier of {ssd_chunks} x {rec >> 20} MiB = {ssd_chunks * rec / 1e9:.0f} GB does not "
                      f"fit in 80% of the {free / 1e9:.0f} GB free under {args.ssd_path}; lower --ssd-frac or --requests")
     rng = make_rng(11)
-    bufs = tuple(torch.from_numpy(randn_bf16(rng, (L, max_n, h, d)).view(np.int16)).cuda() for h in (Hq, Hkv, Hkv))
+    bufs = tuple(torch.from_numpy(randn_bf16(rng, (L, max_n, h, d)).view(np.int16)).cuda() for h in (hq, hkv, hkv))
     bufs = bufs + (torch.empty_like(bufs[0]),)
     body = _z_layer_body(torch, geo, max_n) if args.layer_body else None
-    clocks = ClockSampler(0, pci_bus_id(torch, 0))
-    clocks.start()
-    clocks.begin()
-    r = _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, body=body)
+    windows = [int(x) for x in args.z_windows.split(",")] if args.z_windows else [args.window]
+    fracs = [float(x) for x in args.z_store_fracs.split(",")] if args.z_store_fracs else [args.store_frac]
     rhos = [float(x) for x in args.rho.split(",")] if args.rho else []
-    service_ms = args.rho_service_ms or float(np.mean(r["wall"]))
-    poisson = []
-    for rho in rhos:
-        arr = poisson_arrivals(len(reqs), rho, service_ms)
-        rq = _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=VirtualQueue(arr, args.window),
-                     body=body)
-        tq = np.array(rq["ttft_q"])
-        poisson.append({
-            "rho": rho, "rho_service_ms": service_ms, "arrival_rate_per_s": 1e3 * rho / service_ms,
-            "ttft_ms_mean": float(tq.mean()), "ttft_ms_p50": float(np.percentile(tq, 50)),
-            "ttft_ms_p95": float(np.percentile(tq, 95)), "ttft_ms_p99": float(np.percentile(tq, 99)),
-            "service_ms_mean": float(np.mean(rq["wall"])), "device_ttft_ms_mean": float(np.mean(rq["ttft"])),
-            "mean_pending": float(np.mean(rq["pending"])), "chunk_hit_ratio": rq["hits"] / max(1, rq["chunks"]),
-        })
-    clk = clocks.stop()
-    tt = np.array(r["ttft"])
-    wall = r["wall"]
-    line = {
-        "metric": "Z trace: context tokens/s over 1000 Zipf RAG requests (TTFT per request in ttft_ms_*)",
-        "value": r["toks"] / (r["total_ms"] * 1e-3), "unit": "tokens/s", "n_gpus": 1, "steps": len(reqs),
-        "warmup": 0, "ms_per_step": r["total_ms"] / len(reqs), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None,
-        "dtype": "bf16", "data": "synthetic (seeded Zipf(1.0) corpus of 1000 docs x 4-16 chunks, 2 docs + "
-                                   "128-256 query tokens per request; random bf16 KV)",
-        "config": {"workload": f"Z: L8 shape, W={args.window}, store={cap} chunks "
-                               f"({args.store_frac:.0%} of {len(distinct)} distinct), ssd={ssd_chunks} chunks, "
-                               f"offload on" + (", +layer body (f3)" if body is not None else "")
-                               + (", NO REUSE (full recompute baseline)" if args.no_reuse else ""),
-                   "requests": len(reqs), "window": args.window, "store_chunks": cap, "ssd_chunks": ssd_chunks},
-        "ttft_wall_ms_mean": float(np.mean(wall)), "ttft_wall_ms_p95": float(np.percentile(wall, 95)),
-        "tier_stats": r["stats"],
-        "ttft_ms_mean": float(tt.mean()), "ttft_ms_p50": float(np.percentile(tt, 50)),
-        "ttft_ms_p95": float(np.percentile(tt, 95)), "ttft_ms_p99": float(np.percentile(tt, 99)),
-        "chunk_hit_ratio": r["hits"] / max(1, r["chunks"]), "mean_n1_tokens": float(np.mean(r["n1s"])),
-        "match_prefix_us_p50": float(np.percentile(r["plan_us"], 50)), "store_pin_s": r["t_pin"],
-        "gpu_launches": r["launches"], "clocks": clk,
-    }
-    if poisson:
-        line["poisson"] = poisson
-        line["poisson_note"] = ("saturated pass first (every request waiting from t=0; its mean wall service "
-                                "time sets the rate), then one cold-store pass per rho with Poisson arrivals; "
-                                "ttft_ms_* there = queueing + service (virtual-time FIFO over measured service)")
-    print(json.dumps(line), flush=True)
+
+    def header(W, cap, kind, rho=None, service_ms=None):
+        return {"trace": "zipf_trace(seed=4)", "requests": len(reqs), "C": C, "S_pg": S, "L": L, "P": P,
+                "window": W, "store_chunks": cap, "ssd_chunks": ssd_chunks, "n_pool_pages": n_pool_pages,
+                "distinct_chunks": len(distinct), "pass": kind, "rho": rho, "rho_service_ms": service_ms,
+                "no_reuse": bool(args.no_reuse)}
+
+    def emit(r, W, cap, frac, clk, poisson=None):
+        tt = np.array(r["ttft"])
+        wall = r["wall"]
+        line = {
+            "metric": "Z trace: context tokens/s over the Zipf RAG requests (TTFT per request in ttft_ms_*)",
+            "value": r["toks"] / (r["total_ms"] * 1e-3), "unit": "tokens/s", "n_gpus": 1, "steps": len(reqs),
+            "warmup": 0, "ms_per_step": r["total_ms"] / len(reqs), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded Zipf(1.0) corpus of 1000 docs x 4-16 chunks, 2 docs + "
+                                       "128-256 query tokens per request; random bf16 KV)",
+            "config": {"workload": f"Z: L8 shape{f' (rank 0 of a KV-head shard x{P})' if P > 1 else ''}, W={W}, "
+                                   f"store={cap} chunks ({frac:.0%} of {len(distinct)} distinct), "
+                                   f"ssd={ssd_chunks} chunks, offload on"
+                                   + (", +layer body (f3)" if body is not None else "")
+                                   + (", NO REUSE (full recompute baseline)" if args.no_reuse else ""),
+                       "requests": len(reqs), "window": W, "store_chunks": cap, "store_frac": frac,
+                       "ssd_chunks": ssd_chunks, "rank_slice": P, "chunk_bytes": rec},
+            "ttft_wall_ms_mean": float(np.mean(wall)), "ttft_wall_ms_p95": float(np.percentile(wall, 95)),
+            "tier_stats": r["stats"],
+            "ttft_ms_mean": float(tt.mean()), "ttft_ms_p50": float(np.percentile(tt, 50)),
+            "ttft_ms_p95": float(np.percentile(tt, 95)), "ttft_ms_p99": float(np.percentile(tt, 99)),
+            "chunk_hit_ratio": r["hits"] / max(1, r["chunks"]), "mean_n1_tokens": float(np.mean(r["n1s"])),
+            "match_prefix_us_p50": float(np.percentile(r["plan_us"], 50)), "store_pin_s": r["t_pin"],
+            "gpu_launches": r["launches"], "clocks": clk,
+        }
+        if poisson:
+            line["poisson"] = poisson
+            line["poisson_note"] = ("saturated pass first (every request waiting from t=0; its mean wall service "
+                                    "time sets the rate), then one cold-store pass per rho with Poisson arrivals; "
+                                    "ttft_ms_* there = queueing + service (virtual-time FIFO over measured service)")
+        print(json.dumps(line), flush=True)
+
+    for frac in fracs:
+        cap = max(8, int(frac * len(distinct)))
+        for W in windows:
+            clocks = ClockSampler(0, pci_bus_id(torch, 0))
+            clocks.start()
+            clocks.begin()
+            r = _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, body=body, window=W)
+            if args.z_log:
+                _write_plan_log(os.path.join(args.z_log, f"z_P{P}_W{W}_store{round(frac * 100)}_ssd"
+                                             f"{round(args.ssd_frac * 100)}_sat.jsonl.gz"), header(W, cap, "saturated"),
+                                r["log"])
+            service_ms = args.rho_service_ms or float(np.mean(r["wall"]))
+            poisson = []
+            for rho in rhos:
+                arr = poisson_arrivals(len(reqs), rho, service_ms)
+                rq = _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=VirtualQueue(arr, W),
+                             body=body, window=W)
+                if args.z_log:
+                    _write_plan_log(os.path.join(args.z_log, f"z_P{P}_W{W}_store{round(frac * 100)}_ssd"
+                                                 f"{round(args.ssd_frac * 100)}_rho{rho}.jsonl.gz"),
+                                    header(W, cap, "poisson", rho, service_ms), rq["log"])
+                tq = np.array(rq["ttft_q"])
+                poisson.append({
+                    "rho": rho, "rho_service_ms": service_ms, "arrival_rate_per_s": 1e3 * rho / service_ms,
+                    "ttft_ms_mean": float(tq.mean()), "ttft_ms_p50": float(np.percentile(tq, 50)),
+                    "ttft_ms_p95": float(np.percentile(tq, 95)), "ttft_ms_p99": float(np.percentile(tq, 99)),
+                    "service_ms_mean": float(np.mean(rq["wall"])), "device_ttft_ms_mean": float(np.mean(rq["ttft"])),
+                    "mean_pending": float(np.mean(rq["pending"])), "chunk_hit_ratio": rq["hits"] / max(1, rq["chunks"]),
+                    "tier_stats": rq["stats"],
+                })
+            emit(r, W, cap, frac, clocks.stop(), poisson)
+
 
 
 def _free_port():
