@@ -100,8 +100,12 @@ PROTOTYPES = {
 _lib = None
 
 
-def load_library(path: str = LIB_PATH):
+def load_library(path: str = None):
+    """Load libpcr.so (PCR_LIB_PATH overrides the in-tree build, e.g. the sanitizer build the
+    tests make).  Fails loudly when it is missing: there is no fallback."""
     global _lib
+    if path is None:
+        path = os.environ.get("PCR_LIB_PATH", LIB_PATH)
     if _lib is None:
         if not os.path.exists(path):
             raise ImportError(f"{path} not built: run `python -m paper_2603_23049_b200.build` "
