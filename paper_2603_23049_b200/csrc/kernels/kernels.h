@@ -25,6 +25,7 @@ struct LinearCopies {
   const uint4* src[kMax];
   uint4* dst[kMax];
   int64_t n16[kMax];
+  int64_t src_stride16[kMax], dst_stride16[kMax];   // per-layer advance (streamed gather; 0 otherwise)
 };
 
 // a2: pool[layer][pages[t/S]][h][kv][t%S] = store[slots[t/C]][layer][(t%C)/S][h][kv][t%S], t < n_matched*C.
@@ -33,6 +34,14 @@ struct LinearCopies {
 cudaError_t launch_kv_gather(const void* store, void* pool, const int32_t* d_slots, const int32_t* d_pages,
                              int32_t n_matched, int32_t layer, const KvGeom& g, int32_t target_ctas,
                              cudaStream_t stream, const LinearCopies* lin = nullptr);
+
+// a2, streamed: every layer of the request in one launch (layers in order); after its share of
+// layer l each warp adds 1 to ready[l] with release semantics, so layer l is complete when
+// ready[l] == *warps_out (the attention acquires it).  ready[0..L) must be zero before the launch.
+// Linear copy i of layer l: src[i] + l*src_stride16[i] -> dst[i] + l*dst_stride16[i].
+cudaError_t launch_kv_gather_stream(const void* store, void* pool, const int32_t* d_slots, const int32_t* d_pages,
+                                    int32_t n_matched, const KvGeom& g, int32_t target_ctas, const LinearCopies* lin,
+                                    int32_t* ready, cudaStream_t stream, int32_t* warps_out);
 
 // a2 variant (load_mode 3, experiment): same copy with TMA bulk copies (host -> smem -> pool).
 cudaError_t launch_kv_gather_tma(const void* store, void* pool, const int32_t* d_slots, const int32_t* d_pages,
@@ -81,6 +90,10 @@ struct AttnParams {
   const uint16_t* k_new;
   const uint16_t* v_new;
   int32_t cluster_reduce;   // set by the launcher: split-KV partials reduced over DSMEM in-kernel
+  // Streamed gather (non-null): the TMA producer waits until ready[layer] >= ready_target (acquire)
+  // before its first load -- the layer's pool pages (and host_io inputs) have landed.
+  const int32_t* ready;
+  int32_t ready_target;
 };
 
 // Merge n_parts partials (O normalised per part, log2-domain LSE; part s at o + s*o_stride and

@@ -60,31 +60,30 @@ __device__ __forceinline__ void segment_addrs(int64_t seg, int32_t chunk0, int32
 
 // Segments [0, n_lin_seg) are pieces of the linear copies (each copy cut into seg16-unit pieces,
 // the last one ragged), the rest are page segments.  The linear copies come first: the layer's
-// inputs are needed by the attention as soon as its KV has landed.
-__global__ void __launch_bounds__(kThreads, 6) kv_gather_kernel(const uint4* __restrict__ store,
-                                                             uint4* __restrict__ pool,
-                                                             const int32_t* __restrict__ slots,
-                                                             const int32_t* __restrict__ pages, int32_t n_chunks,
-                                                             int32_t layer, KvGeom g, int32_t row16_log2,
-                                                             int32_t ppc_log2, LinearCopies lin) {
-  const int lane = threadIdx.x & 31;
+// inputs are needed by the attention as soon as its KV has landed.  Warp `warp` of `warps` takes
+// segments warp, warp + warps, ...
+__device__ __forceinline__ void gather_layer(const uint4* __restrict__ store, uint4* __restrict__ pool,
+                                             const int32_t* __restrict__ slots, const int32_t* __restrict__ pages,
+                                             int32_t n_chunks, int32_t layer, const KvGeom& g, int32_t row16_log2,
+                                             int32_t ppc_log2, const LinearCopies& lin, int64_t warp, int64_t warps,
+                                             int lane) {
   const int32_t seg16 = g.S << row16_log2;
   static_assert(LinearCopies::kMax == 3, "segment prefix below");
   const int64_t e1 = lin.n > 0 ? (lin.n16[0] + seg16 - 1) / seg16 : 0;
   const int64_t e2 = e1 + (lin.n > 1 ? (lin.n16[1] + seg16 - 1) / seg16 : 0);
   const int64_t n_lin = e2 + (lin.n > 2 ? (lin.n16[2] + seg16 - 1) / seg16 : 0);
   const int64_t n_seg = n_lin + ((int64_t(n_chunks) * g.Hkv * 2) << ppc_log2);
-  const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
-  for (int64_t seg = int64_t(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5); seg < n_seg; seg += warps) {
+  for (int64_t seg = warp; seg < n_seg; seg += warps) {
     const uint4* src;
     uint4* dst;
     int64_t len16 = seg16;
     if (seg < n_lin) {
       const bool c1 = seg >= e1, c2 = seg >= e2;
+      const int i = c2 ? 2 : c1 ? 1 : 0;
       const int64_t off = (seg - (c2 ? e2 : c1 ? e1 : 0)) * seg16;
-      src = (c2 ? lin.src[2] : c1 ? lin.src[1] : lin.src[0]) + off;
-      dst = (c2 ? lin.dst[2] : c1 ? lin.dst[1] : lin.dst[0]) + off;
-      len16 = min(int64_t(seg16), (c2 ? lin.n16[2] : c1 ? lin.n16[1] : lin.n16[0]) - off);
+      src = lin.src[i] + lin.src_stride16[i] * layer + off;
+      dst = lin.dst[i] + lin.dst_stride16[i] * layer + off;
+      len16 = min(int64_t(seg16), lin.n16[i] - off);
     } else {
       int64_t s16, p16;
       segment_addrs(seg - n_lin, 0, layer, g, ppc_log2, row16_log2, slots, pages, s16, p16);
@@ -100,6 +99,36 @@ __global__ void __launch_bounds__(kThreads, 6) kv_gather_kernel(const uint4* __r
       for (int u = 0; u < kGatherUnroll; ++u)
         if (base + 32 * u < len16) dst[base + 32 * u] = v[u];
     }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 6) kv_gather_kernel(const uint4* __restrict__ store,
+                                                             uint4* __restrict__ pool,
+                                                             const int32_t* __restrict__ slots,
+                                                             const int32_t* __restrict__ pages, int32_t n_chunks,
+                                                             int32_t layer, KvGeom g, int32_t row16_log2,
+                                                             int32_t ppc_log2, LinearCopies lin) {
+  gather_layer(store, pool, slots, pages, n_chunks, layer, g, row16_log2, ppc_log2, lin,
+               int64_t(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5), int64_t(gridDim.x) * (kThreads / 32),
+               threadIdx.x & 31);
+}
+
+// Streamed gather (one launch per request): every layer in order.  A warp that has copied its
+// share of layer l publishes it -- release add on ready[l] (cumulative over the warp's lanes
+// through __syncwarp) -- and moves on to layer l+1 without waiting for the other warps; layer l
+// is in the pool once ready[l] counts every warp of the grid (the attention of layer l waits for
+// that with an acquire load, suffix_attn.cu).
+__global__ void __launch_bounds__(kThreads, 6) kv_gather_stream_kernel(
+    const uint4* __restrict__ store, uint4* __restrict__ pool, const int32_t* __restrict__ slots,
+    const int32_t* __restrict__ pages, int32_t n_chunks, int32_t n_layers, KvGeom g, int32_t row16_log2,
+    int32_t ppc_log2, LinearCopies lin, int32_t* __restrict__ ready) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = int64_t(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5);
+  const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
+  for (int32_t layer = 0; layer < n_layers; ++layer) {
+    gather_layer(store, pool, slots, pages, n_chunks, layer, g, row16_log2, ppc_log2, lin, warp, warps, lane);
+    __syncwarp();
+    if (lane == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(ready + layer) : "memory");
   }
 }
 
@@ -253,6 +282,26 @@ cudaError_t launch_kv_gather(const void* store, void* pool, const int32_t* d_slo
   kv_gather_kernel<<<int(ctas), kThreads, smem, stream>>>(static_cast<const uint4*>(store), static_cast<uint4*>(pool),
                                                        d_slots, d_pages, std::max(n_matched, 0), layer, g,
                                                        ilog2(g.d / 8), ilog2(g.C / g.S), l);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kv_gather_stream(const void* store, void* pool, const int32_t* d_slots, const int32_t* d_pages,
+                                    int32_t n_matched, const KvGeom& g, int32_t target_ctas, const LinearCopies* lin,
+                                    int32_t* ready, cudaStream_t stream, int32_t* warps_out) {
+  LinearCopies l{};
+  if (lin) l = *lin;
+  if (l.n < 0 || l.n > LinearCopies::kMax || !ready) return cudaErrorInvalidValue;
+  const int64_t seg16 = int64_t(g.S) * (g.d / 8);
+  int64_t n_seg = int64_t(std::max(n_matched, 0)) * g.Hkv * 2 * (g.C / g.S);
+  for (int i = 0; i < l.n; ++i) {
+    if (l.n16[i] < 0) return cudaErrorInvalidValue;
+    n_seg += (l.n16[i] + seg16 - 1) / seg16;
+  }
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(target_ctas, (n_seg + kThreads / 32 - 1) / (kThreads / 32)));
+  *warps_out = int32_t(ctas * (kThreads / 32));
+  kv_gather_stream_kernel<<<int(ctas), kThreads, 0, stream>>>(
+      static_cast<const uint4*>(store), static_cast<uint4*>(pool), d_slots, d_pages, std::max(n_matched, 0), g.L, g,
+      ilog2(g.d / 8), ilog2(g.C / g.S), l, ready);
   return cudaGetLastError();
 }
 

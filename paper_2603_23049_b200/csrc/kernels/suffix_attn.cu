@@ -119,6 +119,17 @@ struct Bars {
   uint32_t tmem_base;
 };
 
+__device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ---------------------------------------------------------------- cluster (DSMEM) helpers
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -295,6 +306,25 @@ __global__ void __maxnreg__(136)
     // 32 pages, read by shuffles), one elected lane issues the TMA copies.
     if (n_iter > 0) {
       const int lane = threadIdx.x & 31;
+      if (p.ready) {
+        // streamed gather: wait until every warp of the gather kernel has published this layer,
+        // then order the TMA (async-proxy) reads after the generic-proxy writes just acquired
+        if (lane == 0) {
+          const uint64_t t0 = globaltimer_ns();
+          uint32_t ns = 32;
+          while (ld_acquire_gpu(p.ready + p.layer) < p.ready_target) {
+            __nanosleep(ns);
+            ns = min(ns * 2, 1024u);
+            if (globaltimer_ns() - t0 > 10ull * 1000 * 1000 * 1000) {   // 10 s: never hang the GPU
+              printf("suffix_attn: layer %d load never completed (ready %d of %d)\n", p.layer,
+                     ld_acquire_gpu(p.ready + p.layer), p.ready_target);
+              __trap();
+            }
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        __syncwarp();
+      }
       if (!PCR_Q_TMEM && elect_one()) {
         mbar_arrive_expect_tx(&bars->q_full, kNQ * Lay::kQTile);
         for (int t = 0; t < kNQ; ++t)

@@ -79,6 +79,12 @@ struct pcr_ctx {
   cudaStream_t ce_stream = nullptr;
   cudaEvent_t ev_ce_fork = nullptr, ev_ce_join = nullptr;
   cudaEvent_t ev_io_join = nullptr;
+  // streamed gather: per plan region, L per-layer completion counters (device); the ones the
+  // attention launches of the current pcr_run_prefill call wait on (null outside such a call)
+  int32_t* d_ready = nullptr;
+  cudaEvent_t ev_ready_zero = nullptr;
+  const int32_t* cur_ready = nullptr;
+  int32_t cur_ready_target = 0;
 };
 
 namespace {
@@ -159,6 +165,13 @@ int32_t* d_own_slots_of(pcr_ctx* c, const Request* r) { return d_slots_of(c, r) 
 int32_t* d_vpages_of(pcr_ctx* c, const Request* r) { return d_own_slots_of(c, r) + c->chunk_cap; }
 int32_t* d_own_res_slots_of(pcr_ctx* c, const Request* r) { return d_vpages_of(c, r) + c->region_page_cap; }
 int32_t* d_own_res_pages_of(pcr_ctx* c, const Request* r) { return d_own_res_slots_of(c, r) + c->chunk_cap; }
+bool stream_gather_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PCR_STREAM_GATHER");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 bool fused_append_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PCR_FUSED_APPEND");
@@ -337,6 +350,8 @@ pcr_status enqueue_attn(pcr_ctx* c, Request* r, int32_t layer, const void* q, co
     c->launches += 1;
   }
   pcr::AttnParams p{};
+  p.ready = c->cur_ready;
+  p.ready_target = c->cur_ready_target;
   if (fused) {
     p.k_new = static_cast<const uint16_t*>(k);
     p.v_new = static_cast<const uint16_t*>(v);
@@ -512,10 +527,50 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
                                 kv_layer * 2, cudaMemcpyHostToDevice, cs));
     return PCR_OK;
   };
+  // Streamed gather (OVERLAP loads, SM gather, head sharding): ONE gather launch moves every layer
+  // in order and publishes each layer through a per-layer counter that the attention of that layer
+  // acquires in-kernel -- no per-layer launch, event or ramp-up on the load stream.  With host_io
+  // the inputs ride along when the staging ring holds every layer (no buffer reuse to wait for).
+  const int32_t L = c->cfg.n_layers;
+  const bool host_io_mapped = o.host_io && q_dev && k_dev && v_dev && (q_layer * 2) % 16 == 0 && (kv_layer * 2) % 16 == 0;
+  const bool streamed = up && !c->ctx_split && c->cfg.load_mode == 0 && stream_gather_enabled() &&
+                        (r->plan.n_matched > 0 || o.host_io) && (!o.host_io || (host_io_mapped && ring >= L));
+  struct ReadyReset {   // the counters belong to this call only (also on an early error return)
+    pcr_ctx* c;
+    ~ReadyReset() { c->cur_ready = nullptr; c->cur_ready_target = 0; }
+  } ready_reset{c};
+  if (streamed) {
+    int32_t* ready = c->d_ready + int64_t(r->plan.region) * L;
+    CUDA_TRY(c, cudaMemsetAsync(ready, 0, sizeof(int32_t) * L, ls));
+    CUDA_TRY(c, cudaEventRecord(c->ev_ready_zero, ls));
+    CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_ready_zero, 0));   // (not the gather itself)
+    pcr::LinearCopies lin{};
+    if (o.host_io) {
+      const void* srcs[3] = {q_dev, k_dev, v_dev};
+      const int64_t off[3] = {0, q_layer, q_layer + kv_layer}, n[3] = {q_layer, kv_layer, kv_layer};
+      lin.n = 3;
+      for (int i = 0; i < 3; ++i) {
+        lin.src[i] = static_cast<const uint4*>(srcs[i]);
+        lin.dst[i] = reinterpret_cast<uint4*>(c->io_buf + off[i]);
+        lin.n16[i] = n[i] * 2 / 16;
+        lin.src_stride16[i] = n[i] * 2 / 16;
+        lin.dst_stride16[i] = io_layer * 2 / 16;
+      }
+    }
+    if (times) CUDA_TRY(c, cudaEventRecord(c->ev_t[0], ls));
+    int32_t warps = 0;
+    CUDA_TRY(c, pcr::launch_kv_gather_stream(c->store_dev, c->cfg.pool, d_slots_of(c, r), d_pages_of(c, r),
+                                             r->plan.n_matched, c->geom, c->gather_ctas, &lin, ready, ls, &warps));
+    if (times) CUDA_TRY(c, cudaEventRecord(c->ev_t[1], ls));
+    c->launches += 1;
+    if (r->plan.n_matched > 0) c->sm_layer_loads += L;
+    c->cur_ready = ready;
+    c->cur_ready_target = warps;
+  }
   for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
     cudaEvent_t* et = &c->ev_t[6 * l];
     H2dCopies in;
-    if (o.host_io && up) {   // layer l's inputs join its KV load batch
+    if (o.host_io && up && !streamed) {   // layer l's inputs join its KV load batch
       uint16_t* b = buf_of(l);
       if (l >= ring) CUDA_TRY(c, cudaStreamWaitEvent(ls, c->ev_attn[l - ring], 0));  // buffer free
       auto at = [](const void* base, int64_t elems) -> const void* {
@@ -535,12 +590,14 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
       in.src_dev[2] = at(v_dev, l * kv_layer);
       in.bytes[2] = kv_layer * 2;
     }
-    if (times) CUDA_TRY(c, cudaEventRecord(et[0], ls));
-    if ((st = enqueue_gather(c, r, l, ls, &in)) != PCR_OK) return st;
-    if (times) CUDA_TRY(c, cudaEventRecord(et[1], ls));
-    if (up) {
-      CUDA_TRY(c, cudaEventRecord(c->ev_load[l], ls));
-      CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_load[l], 0));
+    if (!streamed) {
+      if (times) CUDA_TRY(c, cudaEventRecord(et[0], ls));
+      if ((st = enqueue_gather(c, r, l, ls, &in)) != PCR_OK) return st;
+      if (times) CUDA_TRY(c, cudaEventRecord(et[1], ls));
+      if (up) {
+        CUDA_TRY(c, cudaEventRecord(c->ev_load[l], ls));
+        CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_load[l], 0));
+      }
     }
     const uint16_t *q_l = static_cast<const uint16_t*>(q_all) + l * q_layer,
                    *k_l = static_cast<const uint16_t*>(k_all) + l * kv_layer,
@@ -615,9 +672,12 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
   }
   if (times) {
     CUDA_TRY(c, cudaStreamSynchronize(cs));
+    float streamed_ms = 0.f;   // streamed gather: one launch for all layers, reported as its mean per layer
+    if (streamed) CUDA_TRY(c, cudaEventElapsedTime(&streamed_ms, c->ev_t[0], c->ev_t[1]));
     for (int32_t l = 0; l < c->cfg.n_layers; ++l) {
       cudaEvent_t* et = &c->ev_t[6 * l];
-      CUDA_TRY(c, cudaEventElapsedTime(&times[times_stride * l], et[0], et[1]));
+      if (streamed) times[times_stride * l] = streamed_ms / L;
+      else CUDA_TRY(c, cudaEventElapsedTime(&times[times_stride * l], et[0], et[1]));
       CUDA_TRY(c, cudaEventElapsedTime(&times[times_stride * l + 1], et[2], et[3]));
       if (times_stride > 2) {
         times[times_stride * l + 2] = 0.f;
@@ -746,6 +806,9 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
       if (e == cudaSuccess) cp->ev_load.push_back(ev);
     }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cp->ev_join, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cp->ev_ready_zero, cudaEventDisableTiming);
+    if (e == cudaSuccess)
+      e = cudaMalloc(reinterpret_cast<void**>(&cp->d_ready), sizeof(int32_t) * k.n_layers * c->max_regions);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cp->ev_comm, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cp->ev_off, cudaEventDisableTiming);
     for (int l = 0; e == cudaSuccess && l < k.n_layers; ++l) {
@@ -790,6 +853,8 @@ void pcr_destroy(pcr_ctx* c) {
     for (auto e : c->ev_load) cudaEventDestroy(e);
     for (auto e : c->ev_t) cudaEventDestroy(e);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->ev_ready_zero) cudaEventDestroy(c->ev_ready_zero);
+    if (c->d_ready) cudaFree(c->d_ready);
     if (c->ev_comm) cudaEventDestroy(c->ev_comm);
     if (c->ev_off) cudaEventDestroy(c->ev_off);
     for (auto e : c->ev_attn) cudaEventDestroy(e);
