@@ -76,6 +76,13 @@ constexpr int kPolyPairs = PCR_POLY_PAIRS;
 #ifndef PCR_SPLIT_MIN_TILES
 #define PCR_SPLIT_MIN_TILES 4
 #endif
+// Row sum l (reading R18): accumulates the fp32 weights before their bf16 rounding -- one FADD2 per
+// pair inside the exponential loop -- rather than the rounded weights (PCR_ROWSUM_F32=0: one
+// FHADD.BF16 per weight after P is published).  +4% on the M7 r=0.5 shape, +2.5% on L70, others
+// within noise (profiles/r02_rowsum_variant.txt).
+#ifndef PCR_ROWSUM_F32
+#define PCR_ROWSUM_F32 1
+#endif
 #ifndef PCR_ATTN_TIMING
 #define PCR_ATTN_TIMING 0
 #endif
@@ -560,7 +567,7 @@ __global__ void __maxnreg__(136)
     // Per tile of 64 keys: (1) row max of S (two 32-column TMEM loads, four FMNMX3 chains);
     // (2) P = bf16(2^(s*scale - m)) via FFMA2 + ex2 (MUFU, or a polynomial on the FMA pipe for
     // kPolyPairs of every 16 pairs), written over the S columns it came from, and the row sum
-    // of the same bf16-rounded weights via FADD2 (R18).
+    // of the fp32 weights via FADD2 (R18).
     float m_raw = -INFINITY, l = 0.f;
 #if PCR_Q_TMEM
     if (n_iter > 0) {
@@ -661,6 +668,7 @@ __global__ void __maxnreg__(136)
       // P = bf16(2^(s*scale - m)) (MUFU, or the FMA-pipe polynomial for kPolyPairs of every 16
       // pairs), written over the S columns it came from
       uint32_t pk[2][16];
+      uint64_t rs2 = 0;   // PCR_ROWSUM_F32: packed fp32 row sum of the unrounded weights
       auto exp_chunk = [&](float* v, int c) {
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
@@ -676,6 +684,7 @@ __global__ void __maxnreg__(136)
           }
           __nv_bfloat162 b = __floats2bfloat162_rn(y0, y1);
           pk[c][e / 2] = *reinterpret_cast<uint32_t*>(&b);
+          if (PCR_ROWSUM_F32) rs2 = fadd2(rs2, f2_pack(y0, y1));
         }
         tmem_st16(s_col + c * 16, pk[c]);   // P chunk c -> columns [16c, 16c+16): already read
       };
@@ -710,13 +719,17 @@ __global__ void __maxnreg__(136)
       // row sum of the same bf16-rounded weights (R18), off the MMA warp's critical path:
       // fp32 += bf16 (FHADD.BF16), four independent chains
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      if (PCR_ROWSUM_F32) {
+        f2_unpack(rs2, acc[0], acc[1]);
+      } else {
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
-              "add.rn.f32.bf16 %0, lo, %0;\n\tadd.rn.f32.bf16 %1, hi, %1;\n\t}"
-              : "+f"(acc[(e & 1) * 2]), "+f"(acc[(e & 1) * 2 + 1]) : "r"(pk[c][e]));
+          for (int e = 0; e < 16; ++e)
+            asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
+                "add.rn.f32.bf16 %0, lo, %0;\n\tadd.rn.f32.bf16 %1, hi, %1;\n\t}"
+                : "+f"(acc[(e & 1) * 2]), "+f"(acc[(e & 1) * 2 + 1]) : "r"(pk[c][e]));
+      }
       l = l * alpha + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
       PCR_TICK(4);
       m_raw = m_use;
