@@ -61,10 +61,12 @@ constexpr int kSBuf = PCR_Q_TMEM ? 1 : 2;   // S buffers per Q tile
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 // Pairs (of 16 per 32-column chunk) whose exp2 runs as a polynomial on the FMA pipe instead of
-// MUFU.EX2: at d = 128 the MUFU rate (16/clk/SM) equals the tensor rate per score, so moving
-// a quarter of the exponentials to the FMA pipe lets the softmax keep up with the MMAs.
+// MUFU.EX2: at d = 128 the MUFU rate (16/clk/SM) equals the tensor rate per score, so moving some
+// exponentials to the FMA pipe helps the softmax keep up with the MMAs.  Round 1 measured 4 of 16
+// best; with the row sum on the FMA pipe too (FADD2, R18) 1 of 16 is (+8% on the M7 shape,
+// profiles/r02_poly_pairs_sweep.txt).
 #ifndef PCR_POLY_PAIRS
-#define PCR_POLY_PAIRS 4
+#define PCR_POLY_PAIRS 1
 #endif
 constexpr int kPolyPairs = PCR_POLY_PAIRS;
 // Experiment knob (never set by the default build), a bit mask: 1 = skip the softmax arithmetic
