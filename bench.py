@@ -686,16 +686,27 @@ def measure(args, torch, dist, world, rank, local):
     else:
         load_kernel = {4: f"kv_gather + copy engines ({args.ce_frac:.2f} of the chunks)", 3: "kv_gather_tma"}.get(
             load_mode, "kv_gather")
-    rl_gather = {"bound": "host-link", "kernel": load_kernel, "achieved": gather_gbs, "peak": peak_h2d,
-                 "unit": "GB/s", "frac": gather_gbs / peak_h2d,
-                 "traffic": ncu_t.get("gather", {}).get("pcie_read_bytes") if args.workload == "L8" and not ce_layers
-                 else None,
-                 "traffic_note": "PCIe read bytes per launch (ncu pcie__read_bytes x duration, L8 capture in "
-                                 "profiles/ncu_traffic.json); DRAM bytes per launch ~7.7 KB: pool writes stay in L2",
+    # the streamed gather (one launch per request: OVERLAP loads, SM gather, head sharding) or one
+    # kv_gather launch per layer; "per launch" below = per layer either way (streamed: its time / L)
+    streamed = (load_mode == 0 and args.mode in ("overlap", "only-up") and not ctx_split and body is None
+                and os.environ.get("PCR_STREAM_GATHER", "1") != "0")
+    tr = ncu_t.get("gather_stream" if streamed else "gather", {}) if args.workload == "L8" and not ce_layers \
+        and shard == 1 else {}
+    per = L if streamed else 1
+    rl_gather = {"bound": "host-link", "kernel": load_kernel + (" (streamed: one launch per request)" if streamed
+                                                                 else ""),
+                 "achieved": gather_gbs, "peak": peak_h2d, "unit": "GB/s", "frac": gather_gbs / peak_h2d,
+                 "traffic": tr["dram_bytes"] / per if tr else None,
+                 "traffic_pcie_read": tr["pcie_read_bytes"] / per if tr else None,
+                 "traffic_note": "per layer, from the committed ncu --set full capture of this build "
+                                 "(profiles/ncu_traffic.json): DRAM read+write bytes (the pool writes) and PCIe read "
+                                 "bytes (incl. protocol; 1.094 x algorithmic: 128-byte read completions)",
                  "peak_source": f"live: cudaMemcpyAsync H2D, 256 MiB, best of 10 from torch-pinned and from "
                                 f"hugepage-backed registered memory, max of a "
                                 f"measurement before the warm-up ({peak_h2d_before:.1f}) and after the timed region "
                                 f"({peak_h2d_after:.1f})",
+                 "sm_read_ceiling_note": "SM-originated host reads top out at 51.1-51.5 GB/s on this link for every "
+                                         "load width / TMA variant (tools/h2d_probe2.cu): 0.92 of the copy engine",
                  "algorithmic_bytes_per_launch": load_bytes, "avg_launch_ms": gather_ms}
     rl_sm = None
     if sm_leg is not None:
@@ -709,7 +720,8 @@ def measure(args, torch, dist, world, rank, local):
     rl_attn = None if attn_tflops is None else {
         "bound": "tensor", "kernel": "kv_append+suffix_attn", "achieved": attn_tflops, "peak": bf16_peak,
         "unit": "TFLOP/s", "frac": attn_tflops / bf16_peak,
-        "traffic": ncu_t.get("attn_M7_r05", {}).get("dram_bytes") if (args.workload, args.ratio) == ("M7", 0.5) else None,
+        "traffic": ncu_t.get("attn_M7_r05", {}).get("dram_bytes") if (args.workload, args.ratio, shard) == ("M7", 0.5, 1)
+        else None,
         "peak_source": bf16_src,
         "algorithmic_flops_per_launch": attn_flops, "avg_launch_ms": attn_ms,
         "note": "append+attention per layer as it runs in the pipeline (beside the next layer's gather "
@@ -771,7 +783,7 @@ def north_star_point(m7):
             "attn_tflops_in_pipeline": ra["achieved"] if ra else None,
             "attn_frac_of_bf16_peak": ra["frac"] if ra else None, "bf16_peak_tflops": ra["peak"] if ra else None,
             "hidden_load_pct": ov.get("hidden_load_pct"), "t_star_ms": m7["t_star_ms"],
-            "ttft_over_t_star": m7["ttft_over_t_star"],
+            "ttft_over_t_star": m7["ttft_over_t_star"], "clocks": m7["clocks"],
             "targets": {"load_frac": 0.8, "attn_frac": 0.5, "hidden_load_pct": 100.0},
             "note": "north_star: per-layer reused-KV load >= 80% of the measured host->HBM peak, fully hidden behind "
                     "suffix attention at >= 50% of bf16 tensor peak; T* = the pipelined bound with every load and "
