@@ -598,3 +598,85 @@ def test_programmatic_dependent_launch_off_is_bitwise_identical():
     assert res.returncode == 0, res.stderr[-2000:]
     crc = int([ln for ln in res.stdout.splitlines() if ln.startswith("CRC")][0].split()[1])
     assert crc == zlib.crc32(out.tobytes())
+
+
+def test_layer_body_reuse_equals_full_recompute():
+    """f3 + O5 on the GPU: a tiny pre-norm GQA decoder (oracle/tiny_model.py weights) runs its
+    SUFFIX through the per-layer C-ABI calls -- load(l) on the load stream, then on the compute
+    stream RMSNorm -> Wq/Wk/Wv -> RoPE (torch fp32, rounded to bf16) -> pcr_prefill_attn_layer ->
+    Wo -> MLP -- with the PREFIX's K/V reused from the DRAM store (computed once by the fp64
+    model and committed).  The final hidden states of the suffix must equal the fp64 model's full
+    recompute of the whole sequence (reuse-then-attend == full prefill) within the
+    bf16 rounding of K/V/Q/attention output; a wrong chunk (the prefix of another document)
+    breaks it by far."""
+    L, Hq, Hkv, d, C, S = 2, 4, 2, 64, 64, 16
+    m = TinyModel(L=L, Hq=Hq, Hkv=Hkv, d=d, d_model=96, d_ff=128, vocab=1000, seed=3)
+    rng = make_rng(8)
+    prefix = rng.integers(0, 1000, 4 * C, dtype=np.uint32)
+    suffix = rng.integers(0, 1000, 60, dtype=np.uint32)
+    toks = np.concatenate([prefix, suffix])
+    N1, N2 = len(prefix), len(suffix)
+    ref_full, _, _ = m.forward(toks)                       # full recompute (fp64)
+    _, kv_pre, _ = m.forward(prefix)                       # the cached prefix KV (fp64)
+    dev = torch.device("cuda")
+
+    def run(kv_source):
+        rig = Rig(L, Hq, Hkv, d, C, S, store_chunks=8, n_pool_pages=64)
+        rig.ctx.submit(0, np.concatenate([prefix, [1]]).astype(np.uint32))
+        warm = rig.ctx.match_prefix(0, [])
+        kk = np.stack([f32_to_bf16_bits(kv_source[l][0].astype(np.float32)) for l in range(L)])
+        vv = np.stack([f32_to_bf16_bits(kv_source[l][1].astype(np.float32)) for l in range(L)])
+        recs = pack_store_slots(kk, vv, N1 // C, C)
+        for c, s_ in enumerate(warm["slots"]):
+            rig.write_slot(s_, recs[c])
+        rig.ctx.release(0, True)
+        rig.ctx.submit(1, toks, n_cacheable=N1)
+        plan = rig.ctx.match_prefix(1, [])
+        assert plan["n1"] == N1 and plan["n2"] == N2
+        W = [{k: torch.tensor(v, dtype=torch.float32, device=dev) for k, v in lw.items()} for lw in m.layers]
+        x = torch.tensor(m.emb[toks[N1:].astype(np.int64)], dtype=torch.float32, device=dev)
+        pos = torch.arange(N1, N1 + N2, dtype=torch.float64, device=dev)
+        half = d // 2
+        inv = 10000.0 ** (-torch.arange(half, dtype=torch.float64, device=dev) / half)
+        ang = pos[:, None] * inv[None, :]
+        cos, sin = torch.cos(ang)[:, None, :].float(), torch.sin(ang)[:, None, :].float()
+
+        def rope(t):
+            t1, t2 = t[..., :half], t[..., half:]
+            return torch.cat([t1 * cos - t2 * sin, t1 * sin + t2 * cos], dim=-1)
+
+        def rms(t):
+            return t / torch.sqrt((t * t).mean(dim=-1, keepdim=True) + 1e-6)
+
+        out = torch.empty((L, N2, Hq, d), dtype=torch.int16, device=dev)
+        ev = [torch.cuda.Event() for _ in range(L)]
+        rig.ls.wait_stream(torch.cuda.current_stream())
+        rig.cs.wait_stream(torch.cuda.current_stream())
+        for l in range(L):
+            rig.ctx.load_layer_kv(1, l, rig.ls)
+            ev[l].record(rig.ls)
+            with torch.cuda.stream(rig.cs):
+                h = rms(x)
+                q = rope((h @ W[l]["wq"]).view(N2, Hq, d)).to(torch.bfloat16).contiguous()
+                k = rope((h @ W[l]["wk"]).view(N2, Hkv, d)).to(torch.bfloat16).contiguous()
+                v = (h @ W[l]["wv"]).view(N2, Hkv, d).to(torch.bfloat16).contiguous()
+                rig.cs.wait_event(ev[l])
+                rig.ctx.prefill_attn_layer(1, l, q.view(torch.int16), k.view(torch.int16), v.view(torch.int16),
+                                           out[l], rig.cs)
+                x = x + out[l].view(torch.bfloat16).float().reshape(N2, Hq * d) @ W[l]["wo"]
+                h = rms(x)
+                a = h @ W[l]["w1"]
+                x = x + (torch.nn.functional.silu(a) * (h @ W[l]["w3"])) @ W[l]["w2"]
+        rig.cs.synchronize()
+        rig.ctx.release(1, False)
+        return x.double().cpu().numpy()
+
+    ref = ref_full[N1:]
+    got = run(kv_pre)
+    err = rel_l2(got, ref)
+    print(f"layer-body reuse vs full recompute: rel-L2 {err:.2e}")
+    assert err <= 2e-2, err
+    # negative control: the prefix KV of a different document (same positions) must not pass
+    other = rng.integers(0, 1000, 4 * C, dtype=np.uint32)
+    _, kv_other, _ = m.forward(other)
+    assert rel_l2(run(kv_other), ref) > 10 * err

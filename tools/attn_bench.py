@@ -79,9 +79,12 @@ if __name__ == "__main__":
     ap.add_argument("--iters", type=int, default=40)
     ap.add_argument("--small", action="store_true",
                     help="short-suffix shapes only: L8 at P=1/2/4/8 head slices, L70 r=1 rank slice of 8")
+    ap.add_argument("--shape", default="", help="one shape n1,n2,hq,hkv")
     args = ap.parse_args()
     shapes = [(0, 8320, 32, 8), (4096, 4224, 32, 8), (6144, 2176, 32, 8), (4096, 128, 32, 8), (8192, 8320, 64, 8)]
     if args.small:
         shapes = [(4096, 128, 32, 8), (4096, 128, 16, 4), (4096, 128, 8, 2), (4096, 128, 4, 1), (16384, 128, 8, 1)]
+    if args.shape:
+        shapes = [tuple(int(x) for x in args.shape.split(","))]
     for n1, n2, hq, hkv in shapes:
         print(json.dumps(run(n1, n2, hq, hkv, iters=args.iters)), flush=True)
