@@ -44,7 +44,13 @@ namespace {
 using namespace ptx;
 
 constexpr int kBlockM = 128;   // rows per Q tile (= TMEM lanes)
-constexpr int kBlockN = 64;    // keys per tile (64: S fits double-buffered per Q tile in TMEM)
+// Keys per tile: 64, so S fits double-buffered per Q tile in TMEM (2 x 2 x 64 + 2 x 128 O = 512
+// columns) and the softmax of S_t(j+1) can start while PV_t(j) runs.  A 128-key variant (S
+// single-buffered per Q tile, QK^T with N = 128, each row's scores streamed from TMEM in two
+// 64-column halves -- the softmax below is written for any multiple of 64) measured 7% slower on
+// the M7 shapes (profiles/r02_block_n_128.txt): the lost S double-buffering costs more than the
+// halved barrier round trips and operand traffic save.
+constexpr int kBlockN = 64;
 constexpr int kNQ = 2;         // Q tiles per CTA
 #ifndef PCR_KV_STAGES
 #define PCR_KV_STAGES 4
@@ -58,6 +64,7 @@ constexpr int kThreads = 128 + kNQ * 128;
 #define PCR_Q_TMEM 0
 #endif
 constexpr int kSBuf = PCR_Q_TMEM ? 1 : 2;   // S buffers per Q tile
+constexpr int kMaxBox = kBlockN / 16;   // TMA boxes per key tile (pool boxes are >= 16 rows)
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 // Pairs (of 16 per 32-column chunk) whose exp2 runs as a polynomial on the FMA pipe instead of
@@ -344,7 +351,7 @@ __global__ void __maxnreg__(136)
       __syncwarp();
       const int64_t layer_rows = p.n_pool_pages * p.hkv * 2 * p.S;
       const int box = min(p.S, kBlockN);  // rows per TMA box (the pool tensor map's box height)
-      const int n_box = kBlockN / box;    // 1, 2 or 4 (S_pg >= 16)
+      const int n_box = kBlockN / box;    // 1 .. kMaxBox (S_pg >= 16)
       int pg_base = -64, pg_val = 0;
       uint64_t kv_policy = 0;
 #if PCR_KV_L2HINT
@@ -371,7 +378,7 @@ __global__ void __maxnreg__(136)
         const uint8_t* base = smem + (v ? Lay::kV0 : Lay::kK0) + st * Lay::kKVTile;
         bool any = false;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < kMaxBox; ++b) {
           if (b < n_box) {
             int64_t row;
             bool sfx, dst;
@@ -397,10 +404,10 @@ __global__ void __maxnreg__(136)
       for (int it = 0; it < n_iter; ++it) {
         const int st = it % kStages;
         const uint32_t ph = ((it / kStages) - 1) & 1;
-        int64_t row_k[4];
-        bool sfx[4], dst_unused;
+        int64_t row_k[kMaxBox];
+        bool sfx[kMaxBox], dst_unused;
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
+        for (int b = 0; b < kMaxBox; ++b)
           if (b < n_box) box_rows(it, b, row_k[b], sfx[b], dst_unused);
         const int sfx_row0 = (j_begin + it) * kBlockN - p.n1;   // suffix row of box 0 (fused append)
         uint8_t* ks = smem + Lay::kK0 + st * Lay::kKVTile;
@@ -415,7 +422,7 @@ __global__ void __maxnreg__(136)
           } else {
             mbar_arrive_expect_tx(&bars->k_full[st], Lay::kKVTile);
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
+            for (int b = 0; b < kMaxBox; ++b)
 #pragma unroll
               for (int hf = 0; hf < Lay::kHalves; ++hf)
                 if (b < n_box) {
@@ -439,7 +446,7 @@ __global__ void __maxnreg__(136)
           } else {
             mbar_arrive_expect_tx(&bars->v_full[st], Lay::kKVTile);
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
+            for (int b = 0; b < kMaxBox; ++b)
 #pragma unroll
               for (int hf = 0; hf < Lay::kHalves; ++hf)
                 if (b < n_box) {
@@ -615,25 +622,34 @@ __global__ void __maxnreg__(136)
         mbar_arrive(&bars->p_full[t][it % kSBuf]);
         continue;
       }
+      // the tile's scores in 64-column halves (two with 128-key tiles): the row max over all of
+      // them first, the last half loaded being half 0, which pass 2 then uses without a reload
+      constexpr int kH = kBlockN / 64;
       float va[32], vb[32];
-      tmem_ld32(s_col, va);
-      tmem_ld32(s_col + 32, vb);
-      tmem_ld_wait();
-      PCR_TICK(1);
-      if (diag) {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          va[e] = (key0 + e <= limit) ? va[e] : -INFINITY;
-          vb[e] = (key0 + 32 + e <= limit) ? vb[e] : -INFINITY;
-        }
-      }
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      auto load_half = [&](int hh) {
+        tmem_ld32(s_col + hh * 64, va);
+        tmem_ld32(s_col + hh * 64 + 32, vb);
+        tmem_ld_wait();
+        if (diag) {
 #pragma unroll
-      for (int e = 0; e < 32; e += 4) {
-        mx4[(e >> 2) & 1] = fmax3(mx4[(e >> 2) & 1], va[e], va[e + 1]);
-        mx4[((e >> 2) & 1) + 2] = fmax3(mx4[((e >> 2) & 1) + 2], va[e + 2], va[e + 3]);
-        mx4[(e >> 2) & 1] = fmax3(mx4[(e >> 2) & 1], vb[e], vb[e + 1]);
-        mx4[((e >> 2) & 1) + 2] = fmax3(mx4[((e >> 2) & 1) + 2], vb[e + 2], vb[e + 3]);
+          for (int e = 0; e < 32; ++e) {
+            va[e] = (key0 + hh * 64 + e <= limit) ? va[e] : -INFINITY;
+            vb[e] = (key0 + hh * 64 + 32 + e <= limit) ? vb[e] : -INFINITY;
+          }
+        }
+      };
+#pragma unroll 1
+      for (int hh = kH - 1; hh >= 0; --hh) {
+        load_half(hh);
+        if (hh == kH - 1) PCR_TICK(1);
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          mx4[(e >> 2) & 1] = fmax3(mx4[(e >> 2) & 1], va[e], va[e + 1]);
+          mx4[((e >> 2) & 1) + 2] = fmax3(mx4[((e >> 2) & 1) + 2], va[e + 2], va[e + 3]);
+          mx4[(e >> 2) & 1] = fmax3(mx4[(e >> 2) & 1], vb[e], vb[e + 1]);
+          mx4[((e >> 2) & 1) + 2] = fmax3(mx4[((e >> 2) & 1) + 2], vb[e + 2], vb[e + 3]);
+        }
       }
       const float rowmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
       const float m_new = fmaxf(m_raw, rowmax);
@@ -685,10 +701,12 @@ __global__ void __maxnreg__(136)
             y1 = ex2(x1);
           }
           __nv_bfloat162 b = __floats2bfloat162_rn(y0, y1);
-          pk[c][e / 2] = *reinterpret_cast<uint32_t*>(&b);
+          pk[c & 1][e / 2] = *reinterpret_cast<uint32_t*>(&b);
           if (PCR_ROWSUM_F32) rs2 = fadd2(rs2, f2_pack(y0, y1));
         }
-        tmem_st16(s_col + c * 16, pk[c]);   // P chunk c -> columns [16c, 16c+16): already read
+        // P chunk c -> columns [16c, 16c+16): scores already consumed (128-key tiles: chunks 2, 3
+        // land on half 0's columns 32-63, written after half 0 was used and half 1 reloaded)
+        tmem_st16(s_col + c * 16, pk[c & 1]);
       };
 #if PCR_EXP_PINGPONG
       // The two warpgroups take turns on the exponentials (they share each SMSP's MUFU): wait for
@@ -703,8 +721,12 @@ __global__ void __maxnreg__(136)
       named_bar_sync(1 + t, 256);
       PCR_TICK(7);
 #endif
-      exp_chunk(va, 0);
-      exp_chunk(vb, 1);
+#pragma unroll 1
+      for (int hh = 0; hh < kH; ++hh) {
+        if (hh > 0) load_half(hh);
+        exp_chunk(va, 2 * hh);
+        exp_chunk(vb, 2 * hh + 1);
+      }
 #if PCR_EXP_PINGPONG
       if (!(t == 1 && it == n_iter - 1)) named_bar_arrive(2 - t, 256);
 #endif
@@ -724,6 +746,7 @@ __global__ void __maxnreg__(136)
       if (PCR_ROWSUM_F32) {
         f2_unpack(rs2, acc[0], acc[1]);
       } else {
+        static_assert(PCR_ROWSUM_F32 || kBlockN == 64, "rounded-weight row sum: 64-key tiles only");
 #pragma unroll
         for (int c = 0; c < 2; ++c)
 #pragma unroll
