@@ -871,7 +871,7 @@ def _z_layer_body(torch, geo, max_n):
                 ev_at=[torch.cuda.Event() for _ in range(geo["L"])])
 
 
-def _z_request_with_body(torch, ctx, rid, n2, geo, body, out, cs, ls, os_):
+def _z_request_with_body(torch, ctx, rid, n2, geo, body, out, cs, ls, os_, done=None):
     """One request through the per-layer C-ABI calls with the layer body around the attention:
     load(l) on ls || QKV projection on cs; attention(l); offload(l) on os_ || O projection + MLP.
     Only the N2 computed tokens go through the GEMMs (the reused prefix needs no hidden states)."""
@@ -895,6 +895,8 @@ def _z_request_with_body(torch, ctx, rid, n2, geo, body, out, cs, ls, os_):
             ctx.offload_layer_kv(rid, l, os_)
             x = x + out[l].view(torch.bfloat16).view(n2, hq * d) @ b["wo"]
             x = x + (torch.nn.functional.silu(x @ b["wg"]) * (x @ b["wu"])) @ b["wd"]
+    if done is not None:
+        done.record(cs)     # prefill complete (the last offloads may still run)
     cs.wait_stream(ls)
     cs.wait_stream(os_)
 
@@ -923,8 +925,8 @@ def _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=None, bo
     cs, ls, os_ = torch.cuda.Stream(), torch.cuda.Stream(priority=-1), torch.cuda.Stream()
     for i, (t, n) in enumerate(zip(reqs, ndoc)):
         ctx.submit(i, t, 0 if args.no_reuse else n)
-    r = {"ttft": [], "wall": [], "ttft_q": [], "pending": [], "hits": 0, "chunks": 0, "toks": 0, "n1s": [],
-         "plan_us": [], "t_pin": t_pin, "log": []}
+    r = {"ttft": [], "step": [], "wall": [], "ttft_q": [], "pending": [], "hits": 0, "chunks": 0, "toks": 0,
+         "n1s": [], "plan_us": [], "t_pin": t_pin, "log": []}
     launches0 = ctx.kernel_launches
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -944,16 +946,19 @@ def _z_pass(args, torch, reqs, ndoc, cap, ssd_chunks, pool, bufs, queue=None, bo
         v = v_d.view(-1)[: L * n2 * hkv * d].view(L, n2, hkv, d)
         o = o_d.view(-1)[: L * n2 * hq * d].view(L, n2, hq, d)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        done = torch.cuda.Event(enable_timing=True)
+        done.record(cs)      # (creates the event; the library records it again)
         a.record(cs)
         ls.wait_event(a)
         os_.wait_event(a)
         if body is not None:
-            _z_request_with_body(torch, ctx, i, n2, geometry("L8"), body, o, cs, ls, os_)
+            _z_request_with_body(torch, ctx, i, n2, geometry("L8"), body, o, cs, ls, os_, done=done)
         else:
-            ctx.run_prefill_ex(i, q, k, v, o, cs, ls, offload_stream=os_, mode=MODE_OVERLAP)
+            ctx.run_prefill_ex(i, q, k, v, o, cs, ls, offload_stream=os_, mode=MODE_OVERLAP, prefill_done_event=done)
         b.record(cs)
         b.synchronize()
-        r["ttft"].append(a.elapsed_time(b))
+        r["ttft"].append(a.elapsed_time(done))     # prefill complete: the request's first token
+        r["step"].append(a.elapsed_time(b))        # + the tail of its layer-wise offload
         r["wall"].append((time.perf_counter() - tp) * 1e3)   # host plan (+ on-demand SSD loads) + GPU
         ctx.release(i, True)
         if queue:
@@ -1052,6 +1057,9 @@ def run_trace_z(args):
             "tier_stats": r["stats"],
             "ttft_ms_mean": float(tt.mean()), "ttft_ms_p50": float(np.percentile(tt, 50)),
             "ttft_ms_p95": float(np.percentile(tt, 95)), "ttft_ms_p99": float(np.percentile(tt, 99)),
+            "ttft_note": "device time from the request's start to its prefill_done_event (last layer's attention; "
+                         "first token); step_ms_* add the tail of its layer-wise offload",
+            "step_ms_mean": float(np.mean(r["step"])), "step_ms_p95": float(np.percentile(r["step"], 95)),
             "chunk_hit_ratio": r["hits"] / max(1, r["chunks"]), "mean_n1_tokens": float(np.mean(r["n1s"])),
             "match_prefix_us_p50": float(np.percentile(r["plan_us"], 50)), "store_pin_s": r["t_pin"],
             "gpu_launches": r["launches"], "clocks": clk,

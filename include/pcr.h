@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define PCR_ABI_VERSION 6
+#define PCR_ABI_VERSION 7
 
 typedef struct pcr_ctx pcr_ctx;
 
@@ -319,6 +319,10 @@ typedef struct pcr_run_opts {
                             * ([N2][Hq][d], normalised by its own row sums) followed by its
                             * log2-domain LSE ([N2][Hq]; -inf for rows that see no key here).
                             * out_all is not written (may be NULL) unless gathered_all is set. */
+  void* prefill_done_event; /* nullable cudaEvent_t: recorded on compute_stream right after the last
+                            * layer's attention, before the offload / all-gather / host_io streams are
+                            * joined -- the request's prefill (its first token) is complete when it
+                            * completes, while layer-wise offloads may still be running */
 } pcr_run_opts;
 
 /* The full per-request pipeline: pcr_run_prefill + (optional) offload on a third stream, the

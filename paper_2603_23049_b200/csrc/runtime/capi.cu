@@ -654,6 +654,8 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
       if (rr != 0) return fail(c, PCR_E_CUDA, "ncclAllGather failed");
     }
   }
+  if (o.prefill_done_event)
+    CUDA_TRY(c, cudaEventRecord(static_cast<cudaEvent_t>(o.prefill_done_event), cs));
   if (up) {
     CUDA_TRY(c, cudaEventRecord(c->ev_join, ls));
     CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_join, 0));

@@ -63,7 +63,7 @@ class PcrRunOpts(ctypes.Structure):
                 ("offload_stream", ctypes.c_void_p), ("comm_stream", ctypes.c_void_p),
                 ("gathered_all", ctypes.c_void_p), ("layer_times_ms", ctypes.POINTER(ctypes.c_float)),
                 ("mode", ctypes.c_int32), ("host_io", ctypes.c_int32), ("io_ring_layers", ctypes.c_int32),
-                ("partial_all", ctypes.POINTER(ctypes.c_float))]
+                ("partial_all", ctypes.POINTER(ctypes.c_float)), ("prefill_done_event", ctypes.c_void_p)]
 
 
 # Every exported symbol of include/pcr.h with its prototype (restype, argtypes).
@@ -132,6 +132,15 @@ def _stream(s):
     if hasattr(s, "cuda_stream"):
         return ctypes.c_void_p(s.cuda_stream)
     return ctypes.c_void_p(int(s))
+
+
+def _event(e):
+    """cudaEvent_t handle of a torch.cuda.Event (or a raw handle), None passes through."""
+    if e is None:
+        return None
+    if hasattr(e, "cuda_event"):
+        return ctypes.c_void_p(e.cuda_event)
+    return ctypes.c_void_p(int(e))
 
 
 def blake2b(data: bytes, digest_len: int = 64, key: bytes = b"") -> bytes:
@@ -287,7 +296,8 @@ class Context:
 
     def run_prefill_ex(self, req_id, q_all, k_all, v_all, out_all, compute_stream, load_stream=None,
                        offload_stream=None, comm_stream=None, gathered_all=None, mode=MODE_OVERLAP,
-                       layer_times=False, host_io=False, io_ring_layers=0, partial_all=None):
+                       layer_times=False, host_io=False, io_ring_layers=0, partial_all=None,
+                       prefill_done_event=None):
         """Full pipeline (P:480 three streams): returns [L][3] ms (gather, append+attn, offload) if
         layer_times, else None.  host_io: q/k/v/out are page-locked HOST tensors; the library
         stages them per layer on its own copy streams (the e2e path)."""
@@ -296,7 +306,8 @@ class Context:
                        _stream(comm_stream), _ptr(gathered_all),
                        ctypes.cast(times, _P(ctypes.c_float)) if times is not None else None, mode,
                        1 if host_io else 0, int(io_ring_layers),
-                       ctypes.cast(_ptr(partial_all), _P(ctypes.c_float)) if partial_all is not None else None)
+                       ctypes.cast(_ptr(partial_all), _P(ctypes.c_float)) if partial_all is not None else None,
+                       _event(prefill_done_event))
         self._check(self.lib.pcr_run_prefill_ex(self.h, req_id, _ptr(q_all), _ptr(k_all), _ptr(v_all),
                                                 _ptr(out_all), ctypes.byref(o)), "pcr_run_prefill_ex")
         if layer_times:

@@ -395,8 +395,15 @@ def test_offload_long_runs_store_records(load_mode, fragment):
     os_ = torch.cuda.Stream()
     qd, kd, vd = to_dev(q), to_dev(k), to_dev(v)
     od = torch.empty_like(qd)
-    rig.ctx.run_prefill_ex(1, qd, kd, vd, od, rig.cs, rig.ls, offload_stream=os_)
+    done = torch.cuda.Event(enable_timing=True)
+    done.record(rig.cs)
+    a = torch.cuda.Event(enable_timing=True)
+    a.record(rig.cs)
+    rig.ctx.run_prefill_ex(1, qd, kd, vd, od, rig.cs, rig.ls, offload_stream=os_, prefill_done_event=done)
+    b = torch.cuda.Event(enable_timing=True)
+    b.record(rig.cs)
     rig.cs.synchronize()
+    assert 0 < a.elapsed_time(done) <= a.elapsed_time(b)   # prefill done before the offload join
     recs = pack_store_slots(k, v, 3, C)
     for c in range(3):
         got = rig.ctx.store_read(plan["slots"][c]).reshape(recs[c].shape)

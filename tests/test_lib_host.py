@@ -28,7 +28,7 @@ def test_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(pcr.PROTOTYPES) == declared
-    assert lib.pcr_abi_version() == 6
+    assert lib.pcr_abi_version() == 7
 
 
 def test_blake2b_rfc7693_vectors():
@@ -187,10 +187,11 @@ def test_invalid_configs():
 
 
 def test_pcr_run_opts_layout_matches_header():
-    """The binding's ctypes structs mirror include/pcr.h (ABI v6): field order and offsets that the
+    """The binding's ctypes structs mirror include/pcr.h (ABI v7): field order and offsets that the
     C side reads (host_io / io_ring_layers in pcr_run_opts, load_ce_fraction in pcr_config)."""
     import ctypes
-    assert [f for f, _ in pcr.PcrRunOpts._fields_][-4:] == ["mode", "host_io", "io_ring_layers", "partial_all"]
+    assert [f for f, _ in pcr.PcrRunOpts._fields_][-5:] == ["mode", "host_io", "io_ring_layers", "partial_all",
+                                                         "prefill_done_event"]
     assert pcr.PcrConfig.load_ce_fraction.offset == pcr.PcrConfig.load_mode.offset + 4
     assert pcr.PcrConfig.ssd_path.offset % ctypes.alignment(ctypes.c_void_p) == 0
 
