@@ -415,6 +415,7 @@ def measure(args, torch, dist, world, rank, local):
     # N > 1: the library re-assembles each layer's head-sharded output with an NCCL all-gather on
     # a comm stream, overlapped with the next layer (pcr_run_prefill_sharded)
     gathered, xs, lib_comm = None, None, False
+    share_gpu = os.environ.get("PCR_BENCH_SHARE_GPU") == "1"   # functional N-rank check on one GPU
     part_d = None     # context split on one process: this rank's partials (the merge needs every rank)
     if ctx_split and world == 1:
         part_d = torch.empty((L, N2 * hq * (d + 1)), dtype=torch.float32, device="cuda")
@@ -423,6 +424,8 @@ def measure(args, torch, dist, world, rank, local):
                     torch.empty((L, world) + tuple(out_d.shape[1:]), dtype=out_d.dtype, device="cuda"))
         xs = torch.cuda.Stream()
         try:
+            if share_gpu:
+                raise RuntimeError("PCR_BENCH_SHARE_GPU: NCCL refuses two ranks on one GPU")
             uid = [comm_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
             ctx.comm_init(uid[0])
@@ -502,7 +505,7 @@ def measure(args, torch, dist, world, rank, local):
         else:
             t = ctx.run_prefill(rid, q, k, v, out, cs, ls, mode=mode if step_mode is None else step_mode,
                                 layer_times=times)
-            if world > 1:   # fallback re-assembly (rank-major [P][L][N2][Hq/P][d] instead of per layer)
+            if world > 1 and not share_gpu:   # fallback re-assembly (rank-major [P][L][N2][Hq/P][d])
                 with torch.cuda.stream(cs):
                     dist.all_gather_into_tensor(gathered.view(-1), out.view(-1))
         if load_events:
@@ -814,9 +817,18 @@ def run_ours(args):
         if world > 1:
             dist.destroy_process_group()
         return
+    share_gpu = os.environ.get("PCR_BENCH_SHARE_GPU") == "1"
+    if share_gpu:
+        # functional check of the N-rank path with every rank on GPU 0 (timings meaningless; NCCL
+        # refuses two ranks on one device, so gloo carries the control collectives and the outputs
+        # are not re-assembled)
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     line = measure(args, torch, dist, world, rank, local)
     if (args.workload == "L8" and not args.no_target_point and args.rank_slice == 1 and args.shard == "heads"
             and not args.layer_body and not args.offload):
