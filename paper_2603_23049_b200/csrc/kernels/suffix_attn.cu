@@ -92,6 +92,12 @@ constexpr int kPolyPairs = PCR_POLY_PAIRS;
 #ifndef PCR_ROWSUM_F32
 #define PCR_ROWSUM_F32 1
 #endif
+// Two TMA producer warps (warp 0: Q + K, warp 3: V) instead of one: +5-10% on the long-suffix
+// shapes on a typical box, +30% on a box where the default measured 885 TF/s
+// (profiles/r02_split_producer.txt).  PCR_SPLIT_PRODUCER=0 restores the single producer.
+#ifndef PCR_SPLIT_PRODUCER
+#define PCR_SPLIT_PRODUCER 1
+#endif
 #ifndef PCR_ATTN_TIMING
 #define PCR_ATTN_TIMING 0
 #endif
@@ -291,7 +297,7 @@ __global__ void __maxnreg__(136)
       mbar_init(&bars->o_done[t], 1);
     }
     mbar_init(&bars->o_full, 1);
-    mbar_init(&bars->store_done, 1);
+    mbar_init(&bars->store_done, PCR_SPLIT_PRODUCER ? 2 : 1);   // one arrival per producer warp
     fence_mbar_init();
     tma_prefetch_desc(&tmap_pool);
     tma_prefetch_desc(&tmap_q);
@@ -316,10 +322,14 @@ __global__ void __maxnreg__(136)
 
   float ep_lse = -INFINITY, ep_inv_l = 0.f;   // cluster reduce: this softmax thread's row LSE and 1/l
 
-  if (warp == 0) {
-    // ---------------------------------------------------------------- TMA producer
-    // Converged warp: the lanes hold the page ids of 32 consecutive pages (one coalesced load per
-    // 32 pages, read by shuffles), one elected lane issues the TMA copies.
+  if (warp == 0 || (PCR_SPLIT_PRODUCER && warp == 3)) {
+    // ---------------------------------------------------------------- TMA producers
+    // Converged warps: the lanes hold the page ids of 32 consecutive pages (one coalesced load per
+    // 32 pages, read by shuffles), one elected lane issues the TMA copies.  Warp 0 loads Q and the
+    // K tiles, warp 3 the V tiles (PCR_SPLIT_PRODUCER; else warp 0 does both): K(j) is needed two
+    // iterations before V(j) (S(j+2) is issued right after PV(j)), and a single producer issues
+    // K(j) only after V(j-1), which waits for the PV that freed its stage.
+    const bool do_k = warp == 0, do_v = warp == 3 || !PCR_SPLIT_PRODUCER;
     if (n_iter > 0) {
       const int lane = threadIdx.x & 31;
       if (p.ready) {
@@ -341,7 +351,7 @@ __global__ void __maxnreg__(136)
         }
         __syncwarp();
       }
-      if (!PCR_Q_TMEM && elect_one()) {
+      if (do_k && !PCR_Q_TMEM && elect_one()) {
         mbar_arrive_expect_tx(&bars->q_full, kNQ * Lay::kQTile);
         for (int t = 0; t < kNQ; ++t)
           for (int hf = 0; hf < Lay::kHalves; ++hf)
@@ -398,77 +408,72 @@ __global__ void __maxnreg__(136)
         }
         __syncwarp();
       };
-      // K(j) and V(j) go into stage j % kStages once their previous occupants are consumed: K after
-      // the last QK^T that read it (k_empty), V after the last PV (v_empty) -- and, in a writer CTA,
-      // after the previous occupant's suffix boxes have been stored into the pool.
-      for (int it = 0; it < n_iter; ++it) {
+      // load the K (or V) tile `it` into stage it % kStages (boxes from the pool, or -- suffix keys,
+      // fused append -- from k_new / v_new)
+      auto load_tile = [&](int it, bool v) {
         const int st = it % kStages;
-        const uint32_t ph = ((it / kStages) - 1) & 1;
         int64_t row_k[kMaxBox];
         bool sfx[kMaxBox], dst_unused;
 #pragma unroll
         for (int b = 0; b < kMaxBox; ++b)
           if (b < n_box) box_rows(it, b, row_k[b], sfx[b], dst_unused);
         const int sfx_row0 = (j_begin + it) * kBlockN - p.n1;   // suffix row of box 0 (fused append)
-        uint8_t* ks = smem + Lay::kK0 + st * Lay::kKVTile;
-        uint8_t* vs = smem + Lay::kV0 + st * Lay::kKVTile;
-        if (it >= kStages) {
-          mbar_wait(&bars->k_empty[st], ph);
-          if (writer) store_tile(it - kStages, false);
-        }
+        uint8_t* dst_s = smem + (v ? Lay::kV0 : Lay::kK0) + st * Lay::kKVTile;
+        uint64_t* full = v ? &bars->v_full[st] : &bars->k_full[st];
         if (elect_one()) {
           if (PCR_ATTN_PROFILE & 4) {
-            mbar_arrive(&bars->k_full[st]);
+            mbar_arrive(full);
           } else {
-            mbar_arrive_expect_tx(&bars->k_full[st], Lay::kKVTile);
+            mbar_arrive_expect_tx(full, Lay::kKVTile);
 #pragma unroll
             for (int b = 0; b < kMaxBox; ++b)
 #pragma unroll
               for (int hf = 0; hf < Lay::kHalves; ++hf)
                 if (b < n_box) {
                   if (sfx[b])
-                    tma_load_3d(ks + hf * Lay::kKVHalf + b * box * 128, &tmap_kn, hf * 64, g, sfx_row0 + b * box,
-                                &bars->k_full[st]);
+                    tma_load_3d(dst_s + hf * Lay::kKVHalf + b * box * 128, v ? &tmap_vn : &tmap_kn, hf * 64, g,
+                                sfx_row0 + b * box, full);
                   else
-                    tma_load_2d_kv(ks + hf * Lay::kKVHalf + b * box * 128, &tmap_pool, hf * 64, int32_t(row_k[b]),
-                                   &bars->k_full[st], kv_policy);
+                    tma_load_2d_kv(dst_s + hf * Lay::kKVHalf + b * box * 128, &tmap_pool, hf * 64,
+                                   int32_t(row_k[b] + (v ? p.S : 0)), full, kv_policy);
                 }
           }
         }
         __syncwarp();
-        if (it >= kStages) {
-          mbar_wait(&bars->v_empty[st], ph);
-          if (writer) store_tile(it - kStages, true);
-        }
-        if (elect_one()) {
-          if (PCR_ATTN_PROFILE & 4) {
-            mbar_arrive(&bars->v_full[st]);
-          } else {
-            mbar_arrive_expect_tx(&bars->v_full[st], Lay::kKVTile);
-#pragma unroll
-            for (int b = 0; b < kMaxBox; ++b)
-#pragma unroll
-              for (int hf = 0; hf < Lay::kHalves; ++hf)
-                if (b < n_box) {
-                  if (sfx[b])
-                    tma_load_3d(vs + hf * Lay::kKVHalf + b * box * 128, &tmap_vn, hf * 64, g, sfx_row0 + b * box,
-                                &bars->v_full[st]);
-                  else
-                    tma_load_2d_kv(vs + hf * Lay::kKVHalf + b * box * 128, &tmap_pool, hf * 64,
-                                   int32_t(row_k[b] + p.S), &bars->v_full[st], kv_policy);
-                }
+      };
+      // K(j) and V(j) go into stage j % kStages once their previous occupants are consumed: K after
+      // the last QK^T that read it (k_empty), V after the last PV (v_empty) -- and, in a writer CTA,
+      // after the previous occupant's suffix boxes have been stored into the pool.
+      for (int it = 0; it < n_iter; ++it) {
+        const int st = it % kStages;
+        const uint32_t ph = ((it / kStages) - 1) & 1;
+        if (do_k) {
+          if (it >= kStages) {
+            mbar_wait(&bars->k_empty[st], ph);
+            if (writer) store_tile(it - kStages, false);
           }
+          load_tile(it, false);
         }
-        __syncwarp();
+        if (do_v) {
+          if (it >= kStages) {
+            mbar_wait(&bars->v_empty[st], ph);
+            if (writer) store_tile(it - kStages, true);
+          }
+          load_tile(it, true);
+        }
       }
       if (writer) {
         // the last kStages tiles are never refilled: store their suffix boxes once they have landed
         for (int it = max(0, n_iter - kStages); it < n_iter; ++it) {
           const int st = it % kStages;
-          mbar_wait(&bars->k_full[st], (it / kStages) & 1);
-          store_tile(it, false);
-          mbar_wait(&bars->v_full[st], (it / kStages) & 1);
-          store_tile(it, true);
+          if (do_k) {
+            mbar_wait(&bars->k_full[st], (it / kStages) & 1);
+            store_tile(it, false);
+          }
+          if (do_v) {
+            mbar_wait(&bars->v_full[st], (it / kStages) & 1);
+            store_tile(it, true);
+          }
         }
         if (lane == 0) bulk_wait0();   // the pool writes are complete (visible after the grid)
         __syncwarp();
