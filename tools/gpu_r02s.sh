@@ -1,0 +1,9 @@
+#!/bin/bash
+# compute-sanitizer on the final build (split K/V producers, fused append, streamed gather)
+mkdir -p gpurun_out; export PYTHONUNBUFFERED=1
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python __graft_entry__.py smoke > gpurun_out/r02s_$tool.log 2>&1; echo "$tool smoke rc=$?"; tail -1 gpurun_out/r02s_$tool.log
+done
+timeout 1200 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x -k "overlap_sync or host_io_matches_device_buffers or split_kv_edge or offload_third_stream or layer_body" > gpurun_out/r02s_memcheck_tests.log 2>&1; echo "memcheck tests rc=$?"; tail -2 gpurun_out/r02s_memcheck_tests.log
+timeout 1200 compute-sanitizer --tool synccheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x -k "overlap_sync or split_kv_edge" > gpurun_out/r02s_synccheck_tests.log 2>&1; echo "synccheck tests rc=$?"; tail -2 gpurun_out/r02s_synccheck_tests.log
+timeout 1200 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x -k "overlap_sync" > gpurun_out/r02s_racecheck_tests.log 2>&1; echo "racecheck tests rc=$?"; tail -2 gpurun_out/r02s_racecheck_tests.log
