@@ -63,7 +63,21 @@ constexpr int kThreads = 128 + kNQ * 128;
 #ifndef PCR_Q_TMEM
 #define PCR_Q_TMEM 0
 #endif
-constexpr int kSBuf = PCR_Q_TMEM ? 1 : 2;   // S buffers per Q tile
+constexpr int kSBuf = PCR_Q_TMEM ? 1 : 2;   // S buffers per Q tile (barrier parity domain)
+// PCR_Q0_TMEM=1: Q tile 0 lives in TMEM and its QK^T runs as a TS MMA (A from TMEM: no shared-
+// memory traffic for A), Q tile 1 stays in shared memory (SS).  The 64 TMEM columns for Q0 come
+// from sharing THREE rotating S buffers between the two tiles instead of two per tile: S_t(j) goes
+// to buffer (2j + t) % 3, and the MMA issue order [P0(j)] PV0(j) S1(j+1) [P1(j)] PV1(j) S0(j+2)
+// only ever writes the buffer the PV just issued has read (MMAs of one thread run in order).
+#ifndef PCR_Q0_TMEM
+#define PCR_Q0_TMEM 0
+#endif
+static_assert(!(PCR_Q0_TMEM && PCR_Q_TMEM), "one Q-in-TMEM mode at a time");
+constexpr int kSCols = PCR_Q0_TMEM ? 3 * kBlockN : kSBuf * kNQ * kBlockN;   // TMEM columns of S
+// TMEM column (relative) of S_t(it)
+__device__ __forceinline__ uint32_t s_buf_col(int t, int it) {
+  return PCR_Q0_TMEM ? uint32_t(((2 * it + t) % 3) * kBlockN) : uint32_t((kSBuf * t + it % kSBuf) * kBlockN);
+}
 constexpr int kMaxBox = kBlockN / 16;   // TMA boxes per key tile (pool boxes are >= 16 rows)
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
@@ -117,7 +131,7 @@ struct Layout {
   static constexpr int kKVHalf = kBlockN * 128;                // 64 keys x 128 B
   static constexpr int kKVTile = kHalves * kKVHalf;
   static constexpr int kQ0 = 0;
-  static constexpr int kK0 = kQ0 + (PCR_Q_TMEM ? 0 : kNQ * kQTile);   // (Q in TMEM: no smem Q)
+  static constexpr int kK0 = kQ0 + (PCR_Q_TMEM ? 0 : (PCR_Q0_TMEM ? kNQ - 1 : kNQ) * kQTile);   // smem Q tiles
   static constexpr int kV0 = kK0 + kStages * kKVTile;
   static constexpr int kBar = kV0 + kStages * kKVTile;
   // split-KV cluster reduce: this CTA's row LSEs and the merged LSEs (kNQ*128 floats each); the
@@ -129,8 +143,8 @@ struct Layout {
   static constexpr int kAlloc = kBytes + 1024;  // slack for 1024-byte alignment
   // TMEM columns: S_{t,b} (Q tile t, buffer b) at (kSBuf*t+b)*64; [Q_t at kColQ + t*D/2 (bf16
   // pairs), PCR_Q_TMEM]; O_t at kColO + t*D.
-  static constexpr uint32_t kColQ = kSBuf * kNQ * kBlockN;
-  static constexpr uint32_t kColO = kColQ + (PCR_Q_TMEM ? kNQ * D / 2 : 0);
+  static constexpr uint32_t kColQ = kSCols;
+  static constexpr uint32_t kColO = kColQ + (PCR_Q_TMEM ? kNQ * D / 2 : PCR_Q0_TMEM ? D / 2 : 0);
   static_assert(kColO + kNQ * D <= kTmemCols, "TMEM columns");
 };
 
@@ -282,7 +296,7 @@ __global__ void __maxnreg__(136)
   const int n_iter = max(0, j_end - j_begin);
 
   if (threadIdx.x == 0) {
-    mbar_init(&bars->q_full, PCR_Q_TMEM ? kNQ * 128 : 1);
+    mbar_init(&bars->q_full, PCR_Q_TMEM ? kNQ * 128 : PCR_Q0_TMEM ? 1 + 128 : 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&bars->k_full[s], 1);
       mbar_init(&bars->v_full[s], 1);
@@ -352,10 +366,11 @@ __global__ void __maxnreg__(136)
         __syncwarp();
       }
       if (do_k && !PCR_Q_TMEM && elect_one()) {
-        mbar_arrive_expect_tx(&bars->q_full, kNQ * Lay::kQTile);
-        for (int t = 0; t < kNQ; ++t)
+        constexpr int t0 = PCR_Q0_TMEM ? 1 : 0;   // (Q0 mode: tile 0 goes to TMEM via its softmax warps)
+        mbar_arrive_expect_tx(&bars->q_full, (kNQ - t0) * Lay::kQTile);
+        for (int t = t0; t < kNQ; ++t)
           for (int hf = 0; hf < Lay::kHalves; ++hf)
-            tma_load_3d(smem + Lay::kQ0 + t * Lay::kQTile + hf * Lay::kQHalf, &tmap_q, hf * 64, g * G,
+            tma_load_3d(smem + Lay::kQ0 + (t - t0) * Lay::kQTile + hf * Lay::kQHalf, &tmap_q, hf * 64, g * G,
                         i0 + t * tok_per_tile, &bars->q_full);
       }
       __syncwarp();
@@ -492,16 +507,16 @@ __global__ void __maxnreg__(136)
       const uint64_t k_desc0 = smem_desc_sw128(smem_u32(smem + Lay::kK0), 16, 1024);
       const uint64_t v_desc0 = smem_desc_sw128(smem_u32(smem + Lay::kV0), Lay::kKVHalf, 1024);
       auto issue_s = [&](int t, int it) {
-        const uint64_t qd = q_desc0 + uint64_t(t * Lay::kQTile >> 4);
+        const uint64_t qd = q_desc0 + uint64_t((t - (PCR_Q0_TMEM ? 1 : 0)) * Lay::kQTile >> 4);
         const uint64_t kd = k_desc0 + uint64_t((it % kStages) * Lay::kKVTile >> 4);
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < D / 16 && (PCR_ATTN_PROFILE & 2) == 0; ++kk) {
-            if (PCR_Q_TMEM)
-              mma_bf16_ts(tmem + (kSBuf * t + (it % kSBuf)) * kBlockN, tmem + Lay::kColQ + t * (D / 2) + kk * 8,
+            if (PCR_Q_TMEM || (PCR_Q0_TMEM && t == 0))
+              mma_bf16_ts(tmem + s_buf_col(t, it), tmem + Lay::kColQ + (PCR_Q0_TMEM ? 0 : t * (D / 2)) + kk * 8,
                           kd + (((kk >> 2) * Lay::kKVHalf + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
             else
-              mma_bf16_ss(tmem + (kSBuf * t + (it % kSBuf)) * kBlockN,
+              mma_bf16_ss(tmem + s_buf_col(t, it),
                           qd + (((kk >> 2) * Lay::kQHalf + (kk & 3) * 32) >> 4),
                           kd + (((kk >> 2) * Lay::kKVHalf + (kk & 3) * 32) >> 4), idesc_s, kk > 0);
           }
@@ -515,7 +530,7 @@ __global__ void __maxnreg__(136)
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < kBlockN / 16 && (PCR_ATTN_PROFILE & 2) == 0; ++kk)
-            mma_bf16_ts(tmem + Lay::kColO + t * D, tmem + (kSBuf * t + (it % kSBuf)) * kBlockN + kk * 8,
+            mma_bf16_ts(tmem + Lay::kColO + t * D, tmem + s_buf_col(t, it) + kk * 8,
                         vd + (kk * 2048 >> 4), idesc_o, (it > 0 || kk > 0));
           // O_t rescale fence for the last tile only (earlier rescales wait on s_full, below); with
           // one S buffer the wait for S_t(it) already covers PV_t(it-1)
@@ -524,10 +539,22 @@ __global__ void __maxnreg__(136)
         }
         __syncwarp();
       };
-      for (int it = 0; it < min(kSBuf, n_iter); ++it) {
-        mbar_wait(&bars->k_full[it], 0);
+      if (PCR_Q0_TMEM) {   // S0(0), S1(0), S0(1): the three rotating S buffers
+        mbar_wait(&bars->k_full[0], 0);
         tc_fence_after();
-        for (int t = 0; t < kNQ; ++t) issue_s(t, it);
+        issue_s(0, 0);
+        issue_s(1, 0);
+        if (n_iter > 1) {
+          mbar_wait(&bars->k_full[1], 0);
+          tc_fence_after();
+          issue_s(0, 1);
+        }
+      } else {
+        for (int it = 0; it < min(kSBuf, n_iter); ++it) {
+          mbar_wait(&bars->k_full[it], 0);
+          tc_fence_after();
+          for (int t = 0; t < kNQ; ++t) issue_s(t, it);
+        }
       }
       // Per Q tile: O_t += P_t(it) V(it), then S_t(it+2) into the buffer P_t(it) just left (MMAs of
       // one thread run in issue order).  Tile 0's next S does not wait for tile 1's P, so the two
@@ -551,13 +578,21 @@ __global__ void __maxnreg__(136)
         tc_fence_after();
         PCR_MTICK(1);
         issue_pv(0, it);
-        if (more) issue_s(0, it + kSBuf);
+        if (PCR_Q0_TMEM) {
+          if (it + 1 < n_iter) issue_s(1, it + 1);   // into the buffer PV0(it) just read
+        } else if (more) {
+          issue_s(0, it + kSBuf);
+        }
         PCR_MTICK(2);
         if ((PCR_ATTN_PROFILE & 8) == 0) mbar_wait(&bars->p_full[1][it % kSBuf], (it / kSBuf) & 1);
         tc_fence_after();
         PCR_MTICK(1);
         issue_pv(1, it);
-        if (more) issue_s(1, it + kSBuf);
+        if (PCR_Q0_TMEM) {
+          if (it + 2 < n_iter) issue_s(0, it + 2);   // into the buffer PV1(it) just read
+        } else if (more) {
+          issue_s(1, it + kSBuf);
+        }
       }
 #if PCR_ATTN_TIMING
       if ((threadIdx.x & 31) == 0 && (blockIdx.x == 0 || blockIdx.x == 300) && blockIdx.z == 0)
@@ -603,6 +638,41 @@ __global__ void __maxnreg__(136)
     if (t == 1 && n_iter > 0) named_bar_arrive(1, 256);  // tile 0 takes the first turn
 #endif
     const uint64_t scale2 = f2_pack(p.scale_log2, p.scale_log2);
+    // Before publishing P_t(it) the warpgroup checks that the tiles the MMA warp reads right after
+    // it have landed (the MMA warp waits only for P): PV_t(it) reads V(it); the S issued next reads
+    // K(it+2) (two S buffers per tile), or in the Q0 mode K(it+1) after P0 and K(it+2) after P1.
+    auto wait_kv_for_next_mmas = [&](int it) {
+      if (PCR_Q0_TMEM) {
+        if (t == 0) {
+          mbar_wait(&bars->v_full[it % kStages], (it / kStages) & 1);
+          if (it + 1 < n_iter) mbar_wait(&bars->k_full[(it + 1) % kStages], ((it + 1) / kStages) & 1);
+        } else if (it + 2 < n_iter) {
+          mbar_wait(&bars->k_full[(it + 2) % kStages], ((it + 2) / kStages) & 1);
+        }
+      } else if (t == 0) {
+        mbar_wait(&bars->v_full[it % kStages], (it / kStages) & 1);
+        if (it + kSBuf < n_iter) mbar_wait(&bars->k_full[(it + kSBuf) % kStages], ((it + kSBuf) / kStages) & 1);
+      }
+    };
+#if PCR_Q0_TMEM
+    if (t == 0 && n_iter > 0) {
+      // Q tile 0 -> TMEM columns kColQ.. (bf16 pairs, lane = row; zero past N2).  With the streamed
+      // gather (host_io: q itself arrives through the gather) every thread first acquires the layer.
+      if (p.ready)
+        while (ld_acquire_gpu(p.ready + p.layer) < p.ready_target) __nanosleep(64);
+      const uint4* src = reinterpret_cast<const uint4*>(p.q + (int64_t(i) * p.hq + qh) * D);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        uint4 v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = i < p.n2 ? src[c * 8 + e] : make_uint4(0, 0, 0, 0);
+        tmem_st32(lane_base + Lay::kColQ + c * 32, reinterpret_cast<const float*>(v));
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bars->q_full);
+    }
+#endif
 #if PCR_ATTN_TIMING
     long long tm_[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tc_ = clock64();
 #define PCR_TICK(k) do { const long long n_ = clock64(); tm_[k] += n_ - tc_; tc_ = n_; } while (0)
@@ -612,18 +682,14 @@ __global__ void __maxnreg__(136)
     for (int it = 0; it < n_iter; ++it) {
       const int key0 = (j_begin + it) * kBlockN;
       const bool diag = key0 + kBlockN - 1 > tile_first_key_limit;  // tile crosses this Q tile's diagonal
-      const uint32_t s_col = lane_base + (kSBuf * t + (it % kSBuf)) * kBlockN;
+      const uint32_t s_col = lane_base + s_buf_col(t, it);
       PCR_TICK(5);
       mbar_wait(&bars->s_full[t][it % kSBuf], (it / kSBuf) & 1);
       tc_fence_after();
       PCR_TICK(0);
       if (PCR_ATTN_PROFILE & 1) {
         tc_fence_before();
-        if (t == 0) {
-          mbar_wait(&bars->v_full[it % kStages], (it / kStages) & 1);
-          if (it + kSBuf < n_iter)
-            mbar_wait(&bars->k_full[(it + kSBuf) % kStages], ((it + kSBuf) / kStages) & 1);
-        }
+        wait_kv_for_next_mmas(it);
         mbar_arrive(&bars->p_full[t][it % kSBuf]);
         continue;
       }
@@ -718,10 +784,7 @@ __global__ void __maxnreg__(136)
       // the other one to finish its exp phase, run ours, hand the turn back.  Tile 0 first checks
       // that V(it) and K(it+2) have landed (the MMA warp issues PV(it) and S(it+2) on P_0(it) alone);
       // those waits hide inside the wait for the turn.
-      if (t == 0) {
-        mbar_wait(&bars->v_full[it % kStages], (it / kStages) & 1);
-        if (it + kSBuf < n_iter) mbar_wait(&bars->k_full[(it + kSBuf) % kStages], ((it + kSBuf) / kStages) & 1);
-      }
+      wait_kv_for_next_mmas(it);
       PCR_TICK(6);
       named_bar_sync(1 + t, 256);
       PCR_TICK(7);
@@ -739,10 +802,7 @@ __global__ void __maxnreg__(136)
       tmem_st_wait();
       tc_fence_before();
 #if !PCR_EXP_PINGPONG
-      if (t == 0) {  // the MMA warp issues PV(it) and S(it+kSBuf) on P_0(it) alone
-        mbar_wait(&bars->v_full[it % kStages], (it / kStages) & 1);
-        if (it + kSBuf < n_iter) mbar_wait(&bars->k_full[(it + kSBuf) % kStages], ((it + kSBuf) / kStages) & 1);
-      }
+      wait_kv_for_next_mmas(it);
 #endif
       mbar_arrive(&bars->p_full[t][it % kSBuf]);
       // row sum of the same bf16-rounded weights (R18), off the MMA warp's critical path:
