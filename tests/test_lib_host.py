@@ -174,7 +174,7 @@ def test_invalid_configs():
     with pytest.raises(pcr.PcrError):
         pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, rank=1, world=4)  # world !| Hkv
     with pytest.raises(pcr.PcrError):
-        pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=5)          # no such load path (ABI v6: 0-4)
+        pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=5)          # no such load path (0-4 since ABI v6)
     with pytest.raises(pcr.PcrError):
         pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=4, load_ce_fraction=1.5)
     pcr.Context(2, 4, 2, 64, 64, 16, 4, 0, device=-1, pool_bytes=0, load_mode=4, load_ce_fraction=0.5).close()

@@ -3,7 +3,7 @@ timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/gpu_tests.log 2>&1;
 timeout 240 python __graft_entry__.py smoke 2>&1 | tail -1
 timeout 400 python bench.py > gpurun_out/bench_auto.json 2> gpurun_out/bench_auto.err; echo "bench rc=$?"; tail -3 gpurun_out/bench_auto.err
 OUT=gpurun_out/m7.jsonl; : > $OUT
-for m in auto sm; do for r in 0.5 0.75 1.0; do
+for m in sm ce_runs; do for r in 0.5 0.75 1.0; do
 timeout 300 python bench.py --workload M7 --ratio $r --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --load-mode $m >> $OUT 2>> gpurun_out/m7.err
 done; done
 python - <<'PY'
