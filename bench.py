@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0, help="CPU seconds for the oracle baseline sample")
     ap.add_argument("--no-target-point", action="store_true",
                     help="skip the M7 r=0.5 north_star sub-record of the default L8 line")
     ap.add_argument("--dry-run", action="store_true",
@@ -699,7 +700,7 @@ def measure(args, torch, dist, world, rank, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        t_layer, n_l = oracle_sample(geo, n1_here, N2, hkv, hq, budget_s=15.0)
+        t_layer, n_l = oracle_sample(geo, n1_here, N2, hkv, hq, budget_s=args.cpu_budget_s)
         cpu = {"value": N / (t_layer * L), "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
                "sample": f"{n_l} of {L} layers (pool load + append + fp64 suffix attention over all heads), "
                          f"extrapolated x{L}/{n_l}"}
