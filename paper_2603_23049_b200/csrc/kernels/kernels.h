@@ -94,6 +94,10 @@ struct AttnParams {
   // before its first load -- the layer's pool pages (and host_io inputs) have landed.
   const int32_t* ready;
   int32_t ready_target;
+  // Split-KV reduce inside the attention through L2 (set by the launcher when the whole grid is one
+  // wave): spin_ctr = [2][256] uint32 per plan region (arrival counts, generations), zeroed once.
+  uint32_t* spin_ctr;
+  int32_t spin_reduce;
 };
 
 // Merge n_parts partials (O normalised per part, log2-domain LSE; part s at o + s*o_stride and

@@ -160,6 +160,22 @@ __device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t* p) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// L2 loads (cache-global: never a stale L1 line of another CTA's partial)
+__device__ __forceinline__ float ld_cg_f32(const float* p) {
+  float v;
+  asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float4 ld_cg_f4(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -890,6 +906,79 @@ __global__ void __maxnreg__(136)
     }
     tc_fence_before();
   }
+  if (p.spin_reduce) {
+    // ---------------------------------------------------------------- split-KV reduce through L2
+    // The n_splits CTAs of an (M block, kv head) group wrote their partials (O normalised by their
+    // own row sums, log2 LSE) to the workspace above.  The whole grid is resident (one wave, checked
+    // by the launcher), so each CTA can wait for its group: thread 0 publishes the CTA's partial
+    // (fence + arrival count); the last arrival resets the count and bumps the group's generation
+    // (release); the others acquire the generation change.  Then CTA z merges 1/n_splits of the
+    // group's (row, 8 columns) units -- out = sum_s 2^(lse_s - M) O_s / sum_s 2^(lse_s - M) -- from
+    // L2, so no combine kernel runs.
+    const int nsp = p.n_splits;
+    uint32_t* cnt = p.spin_ctr + blockIdx.x;
+    uint32_t* gen = p.spin_ctr + 256 + blockIdx.x;
+    __syncthreads();   // every row of this CTA's partial is written
+    if (threadIdx.x == 0) {
+      const uint32_t my_gen = ld_acquire_gpu_u32(gen);
+      __threadfence();
+      const uint32_t old = atomicAdd(cnt, 1u);
+      if (old == uint32_t(nsp - 1)) {
+        *cnt = 0u;
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gen) : "memory");
+      } else {
+        const uint64_t t0 = globaltimer_ns();
+        while (ld_acquire_gpu_u32(gen) == my_gen) {
+          __nanosleep(64);
+          if (globaltimer_ns() - t0 > 10ull * 1000 * 1000 * 1000) {   // 10 s: never hang the GPU
+            printf("suffix_attn: split group %d never completed\n", blockIdx.x);
+            __trap();
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int64_t rows_total = int64_t(p.n2) * p.hq;
+    constexpr int kUnits = kNQ * kBlockM * (D / 8);
+    const int per = (kUnits + nsp - 1) / nsp;
+    const int u_end = min(kUnits, int(blockIdx.z + 1) * per);
+    for (int u = int(blockIdx.z) * per + int(threadIdx.x); u < u_end; u += kThreads) {
+      const int row = u / (D / 8), grp = u % (D / 8);
+      const int tt = row / kBlockM, rr = row % kBlockM;
+      const int ii = i0 + tt * tok_per_tile + rr / G;
+      if (ii >= p.n2) continue;
+      const int64_t row_id = int64_t(ii) * p.hq + g * G + rr % G;
+      float mx = -INFINITY;
+      for (int sp = 0; sp < nsp; ++sp) mx = fmaxf(mx, ld_cg_f32(p.ws_lse + sp * rows_total + row_id));
+      float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, wsum = 0.f;
+      if (mx != -INFINITY) {
+        for (int sp = 0; sp < nsp; ++sp) {
+          const float w = ex2(ld_cg_f32(p.ws_lse + sp * rows_total + row_id) - mx);
+          const float4* src = reinterpret_cast<const float4*>(p.ws_o + (sp * rows_total + row_id) * D + grp * 8);
+          const float4 x = ld_cg_f4(src), y = ld_cg_f4(src + 1);
+          wsum += w;
+          a[0] += w * x.x; a[1] += w * x.y; a[2] += w * x.z; a[3] += w * x.w;
+          a[4] += w * y.x; a[5] += w * y.y; a[6] += w * y.z; a[7] += w * y.w;
+        }
+      }
+      const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+      if (p.part_o) {
+        float4* dst = reinterpret_cast<float4*>(p.part_o + row_id * D + grp * 8);
+        dst[0] = make_float4(a[0] * inv, a[1] * inv, a[2] * inv, a[3] * inv);
+        dst[1] = make_float4(a[4] * inv, a[5] * inv, a[6] * inv, a[7] * inv);
+        if (grp == 0) p.part_lse[row_id] = wsum > 0.f ? mx + __log2f(wsum) : -INFINITY;
+      } else {
+        uint32_t wv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(a[2 * e] * inv, a[2 * e + 1] * inv);
+          wv[e] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        *reinterpret_cast<uint4*>(p.out + row_id * D + grp * 8) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      }
+    }
+  }
   if (p.cluster_reduce) {
     // ---------------------------------------------------------------- split-KV cluster reduce
     // The n_splits CTAs of a cluster (cluster dims (1, 1, n_splits): rank == blockIdx.z) hold the
@@ -1106,6 +1195,16 @@ bool split_cluster_enabled() {
   return on;
 }
 
+// Split-KV partials merged inside the attention kernel through L2 when its grid is one wave
+// (PCR_SPLIT_SPIN=0: the combine kernel instead).
+bool split_spin_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PCR_SPLIT_SPIN");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // SMs the split-KV sizing may count on (PCR_ATTN_SMS; default all 148).
 int attn_sm_budget() {
   static const int n = [] {
@@ -1204,6 +1303,10 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
   }
   p.n_splits = splits;
   p.cluster_reduce = (splits > 1 && cluster_ok) ? 1 : 0;
+  // in-kernel reduce through L2 when the whole grid is one wave (every group's splits resident)
+  p.spin_reduce = (splits > 1 && !p.cluster_reduce && p.spin_ctr && split_spin_enabled() && ctas <= 256 &&
+                   int64_t(ctas) * splits <= act[1])
+                      ? 1 : 0;
   if (p.part_o && splits == 1) {   // one split: the kernel writes the partial itself
     p.ws_o = p.part_o;
     p.ws_lse = p.part_lse;
@@ -1214,7 +1317,7 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   *launches += 1;
-  if (splits > 1 && !p.cluster_reduce) {
+  if (splits > 1 && !p.cluster_reduce && !p.spin_reduce) {
     const int64_t rows_total = int64_t(p.n2) * p.hq;
     int64_t blocks = (rows_total * (D / 8) + 255) / 256;
     blocks = std::min<int64_t>(blocks, 148 * 8);

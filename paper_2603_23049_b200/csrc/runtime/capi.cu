@@ -59,6 +59,7 @@ struct pcr_ctx {
   // floats followed by the LSE floats
   float* ws = nullptr;
   int64_t ws_floats = 0, ws_region_floats = 0;
+  int32_t device_active = 0;       // planned requests whose device work has been issued (not released)
   // multi-GPU output re-assembly (§8(e))
   void* nccl_comm = nullptr;
   std::unique_ptr<pcr::SsdIo> ssd;    // SSD tier I/O thread (f2)
@@ -191,6 +192,7 @@ pcr_status ensure_tables(pcr_ctx* c, Request* r, cudaStream_t s) {
                                 cudaMemcpyHostToDevice, s));
     CUDA_TRY(c, cudaEventRecord(c->region_ev[reg], s));
     r->tables_uploaded = true;
+    c->device_active += 1;   // (a request with device work issued; until its release)
   } else {
     CUDA_TRY(c, cudaStreamWaitEvent(s, c->region_ev[reg], 0));
   }
@@ -380,6 +382,11 @@ pcr_status enqueue_attn(pcr_ctx* c, Request* r, int32_t layer, const void* q, co
   p.ws_o = ws;
   p.ws_lse = ws ? ws + c->ws_floats : nullptr;
   p.ws_bytes = c->ws_floats * 4;
+  // The in-kernel split reduce waits for every split of a group, so it needs the whole grid resident:
+  // only when no other request's device work can be running beside this one (its kernels could
+  // hold the SMs a waiting group needs); otherwise the combine kernel merges the splits.
+  p.spin_ctr = (ws && c->device_active <= 1) ? reinterpret_cast<uint32_t*>(ws + c->ws_floats + c->ws_floats / 64 + 64)
+                                             : nullptr;
   int n = 0;
   cudaError_t e = pcr::launch_suffix_attn(&c->tmap, p, c->cfg.head_dim, s, &n);
   c->launches += n;
@@ -820,8 +827,10 @@ pcr_status pcr_create(const pcr_config* cfg, pcr_ctx** out) {
     }
     if (e == cudaSuccess) {
       cp->ws_floats = (int64_t(32) << 20) / 4;  // 32 MiB of partial O (+ LSE) per region
-      cp->ws_region_floats = cp->ws_floats + cp->ws_floats / 64 + 64;
+      // + 512 words: the in-kernel split reduce's per-group arrival counts and generations
+      cp->ws_region_floats = cp->ws_floats + cp->ws_floats / 64 + 64 + 512;
       e = cudaMalloc(reinterpret_cast<void**>(&cp->ws), cp->ws_region_floats * c->max_regions * 4);
+      if (e == cudaSuccess) e = cudaMemset(cp->ws, 0, cp->ws_region_floats * c->max_regions * 4);
     }
     for (int l = 0; e == cudaSuccess && l < 6 * k.n_layers; ++l) {
       cudaEvent_t ev;
@@ -979,7 +988,10 @@ pcr_status pcr_release(pcr_ctx* c, int64_t req_id, int32_t commit) {
   }
   std::string err;
   std::vector<pcr::IoOp> writes;
+  const Request* rel = c->planner->find(req_id);
+  const bool had_device_work = rel && rel->tables_uploaded;
   int32_t s = c->planner->release(req_id, commit != 0, &err, &writes);
+  if (s == 0 && had_device_work) c->device_active -= 1;
   if (s != 0) return fail(c, static_cast<pcr_status>(s), err);
   c->req_load_seq.erase(req_id);
   uint8_t* store = static_cast<uint8_t*>(c->store);

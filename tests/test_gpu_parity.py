@@ -567,8 +567,9 @@ def _run_variant(env_over, tmp_path):
 
 def test_fused_append_and_cluster_reduce_match_the_unfused_path(tmp_path):
     """The default attention (suffix K/V read from k_new/v_new and stored into the pool by the
-    kernel itself) against the separate append kernel (PCR_FUSED_APPEND=0): output and the whole
-    pool bit-identical.  The experimental cluster split-KV reduce (PCR_SPLIT_CLUSTER=1: partials
+    kernel itself; split-KV partials merged in-kernel through L2) against the separate append
+    kernel (PCR_FUSED_APPEND=0) and against the split-KV combine kernel (PCR_SPLIT_SPIN=0): output
+    and the whole pool bit-identical.  The experimental cluster split-KV reduce (PCR_SPLIT_CLUSTER=1: partials
     merged over DSMEM in-kernel) gives the same pool and the output within the split merge's
     rounding (another summation order), inside the oracle tolerance."""
     L, N1, N2 = 3, 1024, 130
@@ -579,6 +580,9 @@ def test_fused_append_and_cluster_reduce_match_the_unfused_path(tmp_path):
     # the final 64-row box (zeros past N2), which here ends the page: identical arrays
     assert np.array_equal(out_fa, out)
     assert np.array_equal(pool, pool_fa)
+    out_cb, pool_cb = _run_variant({"PCR_SPLIT_SPIN": "0"}, tmp_path)   # combine kernel instead of the
+    assert np.array_equal(pool, pool_cb)                                 # in-kernel reduce: same formula,
+    assert np.array_equal(out_cb, out)                                   # same order -> same bits
     out_cl, pool_cl = _run_variant({"PCR_SPLIT_CLUSTER": "1"}, tmp_path)
     assert np.array_equal(pool, pool_cl)
     a, b = bf16_bits_to_f64(out), bf16_bits_to_f64(out_cl)
@@ -687,3 +691,51 @@ def test_layer_body_reuse_equals_full_recompute():
     other = rng.integers(0, 1000, 4 * C, dtype=np.uint32)
     _, kv_other, _ = m.forward(other)
     assert rel_l2(run(kv_other), ref) > 10 * err
+
+
+def test_two_requests_in_flight_on_two_streams():
+    """Two planned requests with device work at once (max_inflight regions, separate compute and
+    load streams): each has its own tables, split-KV workspace and layer counters; the in-kernel
+    split reduce (which needs its whole grid resident) steps aside for the combine kernel while
+    another request is active.  Both outputs match the oracle and the whole pool holds both."""
+    L, Hq, Hkv, d, C, S = 2, 32, 8, 128, 256, 64
+    N1, N2 = 1024, 128
+    rng = make_rng(71)
+    rig = Rig(L, Hq, Hkv, d, C, S, store_chunks=12, n_pool_pages=64)
+    reqs = []
+    for rid, seed in ((1, 72), (2, 73)):
+        q, k, v = [], [], []
+        for l in range(L):
+            ql, kl, vl = stress_values("iid", seed * 10 + l, N1, N2, Hq, Hkv, d)
+            q.append(ql)
+            k.append(kl)
+            v.append(vl)
+        q, k, v = np.stack(q), np.stack(k), np.stack(v)
+        doc = rng.integers(0, 1000, N1, dtype=np.uint32)
+        _warm_prefix(rig, 100 + rid, doc, k[:, :N1], v[:, :N1], N1 // C)
+        rig.ctx.submit(rid, np.concatenate([doc, rng.integers(0, 1000, N2, dtype=np.uint32)]), n_cacheable=N1)
+        reqs.append((rid, q, k, v))
+    plans, outs, streams = {}, {}, {}
+    for rid, q, k, v in reqs:
+        plans[rid] = rig.ctx.match_prefix(rid, [])
+        assert plans[rid]["n1"] == N1
+    for rid, q, k, v in reqs:
+        cs, ls = torch.cuda.Stream(), torch.cuda.Stream()
+        qd, kd, vd = to_dev(q), to_dev(k[:, N1:]), to_dev(v[:, N1:])
+        od = torch.empty_like(qd)
+        rig.ctx.run_prefill(rid, qd, kd, vd, od, cs, ls)
+        outs[rid], streams[rid] = (od, qd, kd, vd), cs
+    for rid in streams:
+        streams[rid].synchronize()
+    pool = rig.pool_np()
+    for rid, q, k, v in reqs:
+        out = to_host(outs[rid][0])
+        for l in range(L):
+            kc, vc = rig.expected_context(plans[rid], k[:, N1:], v[:, N1:], l)
+            r, m = check_attention(out[l], q[l], kc, vc, N1, blocked=True)
+            assert r <= TOL_REL_L2 and m <= TOL_MAX_ABS, (rid, l, r, m)
+            exp = rig.expected_pool(plans[rid], k[:, N1:], v[:, N1:], l)
+            pg = plans[rid]["pages"]
+            assert np.array_equal(pool[l][pg], exp[l][pg]), (rid, l)
+    for rid, *_ in reqs:
+        rig.ctx.release(rid, False)
