@@ -1195,12 +1195,15 @@ bool split_cluster_enabled() {
   return on;
 }
 
-// Split-KV partials merged inside the attention kernel through L2 when its grid is one wave
-// (PCR_SPLIT_SPIN=0: the combine kernel instead).
+// Experiment (PCR_SPLIT_SPIN=1): split-KV partials merged inside the attention kernel through L2
+// when its grid is one wave and no other request is active, instead of the combine kernel.
+// Bit-identical output, half the launches, but no faster: the short-suffix layer measured 29.3-29.5
+// vs 27.7-27.8 us alone and 10.58 vs 10.66 ms L8 TTFT in the pipeline (profiles/r02_split_spin.txt)
+// -- the combine kernel's launch is already hidden by PDL -- so it is off by default.
 bool split_spin_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PCR_SPLIT_SPIN");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }

@@ -567,8 +567,8 @@ def _run_variant(env_over, tmp_path):
 
 def test_fused_append_and_cluster_reduce_match_the_unfused_path(tmp_path):
     """The default attention (suffix K/V read from k_new/v_new and stored into the pool by the
-    kernel itself; split-KV partials merged in-kernel through L2) against the separate append
-    kernel (PCR_FUSED_APPEND=0) and against the split-KV combine kernel (PCR_SPLIT_SPIN=0): output
+    kernel itself) against the separate append kernel (PCR_FUSED_APPEND=0), and the split-KV
+    combine kernel against the experimental in-kernel reduce through L2 (PCR_SPLIT_SPIN=1): output
     and the whole pool bit-identical.  The experimental cluster split-KV reduce (PCR_SPLIT_CLUSTER=1: partials
     merged over DSMEM in-kernel) gives the same pool and the output within the split merge's
     rounding (another summation order), inside the oracle tolerance."""
@@ -580,9 +580,9 @@ def test_fused_append_and_cluster_reduce_match_the_unfused_path(tmp_path):
     # the final 64-row box (zeros past N2), which here ends the page: identical arrays
     assert np.array_equal(out_fa, out)
     assert np.array_equal(pool, pool_fa)
-    out_cb, pool_cb = _run_variant({"PCR_SPLIT_SPIN": "0"}, tmp_path)   # combine kernel instead of the
-    assert np.array_equal(pool, pool_cb)                                 # in-kernel reduce: same formula,
-    assert np.array_equal(out_cb, out)                                   # same order -> same bits
+    out_sp, pool_sp = _run_variant({"PCR_SPLIT_SPIN": "1"}, tmp_path)   # in-kernel reduce through L2
+    assert np.array_equal(pool, pool_sp)                                 # instead of the combine kernel:
+    assert np.array_equal(out_sp, out)                                   # same formula and order, same bits
     out_cl, pool_cl = _run_variant({"PCR_SPLIT_CLUSTER": "1"}, tmp_path)
     assert np.array_equal(pool, pool_cl)
     a, b = bf16_bits_to_f64(out), bf16_bits_to_f64(out_cl)
@@ -695,9 +695,9 @@ def test_layer_body_reuse_equals_full_recompute():
 
 def test_two_requests_in_flight_on_two_streams():
     """Two planned requests with device work at once (max_inflight regions, separate compute and
-    load streams): each has its own tables, split-KV workspace and layer counters; the in-kernel
-    split reduce (which needs its whole grid resident) steps aside for the combine kernel while
-    another request is active.  Both outputs match the oracle and the whole pool holds both."""
+    load streams): each has its own tables, split-KV workspace and layer counters (and the
+    experimental in-kernel split reduce, which needs its whole grid resident, steps aside while
+    another request is active).  Both outputs match the oracle and the pool holds both."""
     L, Hq, Hkv, d, C, S = 2, 32, 8, 128, 256, 64
     N1, N2 = 1024, 128
     rng = make_rng(71)
