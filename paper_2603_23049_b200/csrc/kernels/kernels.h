@@ -98,6 +98,9 @@ struct AttnParams {
   // wave): spin_ctr = [2][256] uint32 per plan region (arrival counts, generations), zeroed once.
   uint32_t* spin_ctr;
   int32_t spin_reduce;
+  // 1: no kernel before this one in the stream writes anything it reads (fused append): PDL's
+  // griddepcontrol.wait moves from the prologue to just before the epilogue's global writes.
+  int32_t late_dep_wait;
 };
 
 // Merge n_parts partials (O normalised per part, log2-domain LSE; part s at o + s*o_stride and

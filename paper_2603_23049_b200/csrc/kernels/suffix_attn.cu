@@ -347,7 +347,12 @@ __global__ void __maxnreg__(136)
   const uint32_t tmem = bars->tmem_base;
   // Everything above (barrier init, descriptor prefetch, TMEM alloc) overlaps the tail of the
   // append kernel before it under PDL; q and the pool are read only after it has completed.
-  grid_dep_wait();
+  // PDL: the kernel before this one in the stream may still be draining.  Without a separate append
+  // kernel (fused append) nothing this kernel READS was written by it -- the prefix arrives through
+  // the streamed gather's counters or cross-stream events, q/k_new/v_new from the caller -- so the
+  // wait moves to just before the first global WRITE that an earlier kernel may still read (the
+  // split-KV workspace a previous combine reads): the main loop overlaps that combine.
+  if (!p.late_dep_wait) grid_dep_wait();
   grid_dep_launch();
 
   float ep_lse = -INFINITY, ep_inv_l = 0.f;   // cluster reduce: this softmax thread's row LSE and 1/l
@@ -848,6 +853,7 @@ __global__ void __maxnreg__(136)
              tm_[3] / max(n_iter, 1), tm_[4] / max(n_iter, 1), tm_[5] / max(n_iter, 1));
 #endif
     // ---------------------------------------------------------------- epilogue
+    if (p.late_dep_wait) grid_dep_wait();
     const bool row_ok = i < p.n2;
     const int64_t row_id = int64_t(i) * p.hq + qh;
     if (n_iter > 0) {
@@ -916,6 +922,7 @@ __global__ void __maxnreg__(136)
     // group's (row, 8 columns) units -- out = sum_s 2^(lse_s - M) O_s / sum_s 2^(lse_s - M) -- from
     // L2, so no combine kernel runs.
     const int nsp = p.n_splits;
+    if (p.late_dep_wait) grid_dep_wait();
     uint32_t* cnt = p.spin_ctr + blockIdx.x;
     uint32_t* gen = p.spin_ctr + 256 + blockIdx.x;
     __syncthreads();   // every row of this CTA's partial is written
@@ -987,6 +994,7 @@ __global__ void __maxnreg__(136)
     // its own shared memory, (3) CTA s sums its 1/n_splits share of the (row, 8 columns) units over
     // the cluster's DSMEM and writes the output -- no workspace, no second kernel.
     const int nsp = p.n_splits;
+    if (p.late_dep_wait) grid_dep_wait();
     float* lse_own = reinterpret_cast<float*>(smem + Lay::kLse);
     float* lse_merged = lse_own + kNQ * kBlockM;
     cluster_sync_all();   // #1: every CTA's row LSEs are visible cluster-wide
@@ -1078,6 +1086,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
   constexpr int kVec = D / 8;  // 8 outputs (one 16-byte store) per thread
   const int64_t n = rows_total * kVec;
   grid_dep_wait();   // PDL: the partials are complete and visible past this point
+  grid_dep_launch(); // the next layer's attention may start its main loop while this merge runs
   for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < n; u += int64_t(gridDim.x) * blockDim.x) {
     const int64_t row = u / kVec;
     const int c8 = int(u % kVec) * 8;

@@ -173,6 +173,13 @@ bool stream_gather_enabled() {
   }();
   return on;
 }
+bool late_dep_wait_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PCR_LATE_DEP_WAIT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 bool fused_append_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PCR_FUSED_APPEND");
@@ -357,6 +364,7 @@ pcr_status enqueue_attn(pcr_ctx* c, Request* r, int32_t layer, const void* q, co
   if (fused) {
     p.k_new = static_cast<const uint16_t*>(k);
     p.v_new = static_cast<const uint16_t*>(v);
+    p.late_dep_wait = late_dep_wait_enabled() ? 1 : 0;
   }
   p.q = static_cast<const uint16_t*>(q);
   p.out = static_cast<uint16_t*>(out);
