@@ -241,14 +241,19 @@ pcr_status pcr_prefill_attn_layer(pcr_ctx* ctx, int64_t req_id, int32_t layer, c
                                   void* compute_stream);
 
 /* a5 — the whole layer pipeline for one planned request (Alg.1):
- *   mode 0 OVERLAP: load_stream: gather(l) -> record ev_load[l];
- *                   compute_stream: wait ev_load[l] -> append(l) -> attn(l)
- *                   so gather(l+1) overlaps attn(l);
- *   mode 1 SYNC:    everything in order on compute_stream (load(l), append(l), attn(l)).
+ *   mode 0 OVERLAP: load_stream: ONE streamed gather launch moves every layer in order and
+ *                   publishes layer l through a per-layer completion counter (release);
+ *                   compute_stream: attn(0), attn(1), ... each acquiring its layer's counter
+ *                   in-kernel before its first load (the suffix append is fused into the
+ *                   attention), so gather(l+1) overlaps attn(l).  With the copy-engine / TMA
+ *                   baselines, the context split or a wrapping host_io ring: gather(l) -> record
+ *                   ev_load[l] on load_stream, wait ev_load[l] -> attn(l) on compute_stream.
+ *   mode 1 SYNC:    everything in order on compute_stream (load(l), attn(l)).
  * compute_stream is the stream the caller synchronises on (load_stream is joined into it
- * at the end).  layer_times_ms (nullable) = [2L] floats: per-layer gather and
- * append+attention durations from CUDA events; when non-NULL the call blocks until the
- * request's device work has completed. */
+ * at the end).  layer_times_ms (nullable) = [2L] floats: per-layer gather and attention
+ * durations from CUDA events (streamed gather: its busy time / L for every layer, and each
+ * attention's time includes its in-kernel wait for the layer's load); when non-NULL the call
+ * blocks until the request's device work has completed. */
 pcr_status pcr_run_prefill(pcr_ctx* ctx, int64_t req_id, const void* q_all, const void* k_all,
                            const void* v_all, void* out_all, void* compute_stream,
                            void* load_stream, int32_t mode, float* layer_times_ms);

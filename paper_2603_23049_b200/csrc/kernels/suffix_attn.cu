@@ -1231,12 +1231,16 @@ template <int D>
 cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStream_t stream, int* launches) {
   // act[s] = clusters of s CTAs (one per SM: ~194 KB smem) that can be resident at once, s <= 16.
   // GPCs differ in SM count, so e.g. 16 clusters of 9 may not fit in one wave while 16 of 8 do.
-  static int act[17] = {0};
-  static bool configured = false;
+  // (One-time setup behind a thread-safe function-local static.)
+  struct Setup {
+    int act[17] = {0};
+    cudaError_t err = cudaSuccess;
+  };
   auto kern = suffix_attn_kernel<D>;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Layout<D>::kAlloc);
-    if (e != cudaSuccess) return e;
+  static const Setup setup = [kern] {
+    Setup su;
+    su.err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Layout<D>::kAlloc);
+    if (su.err != cudaSuccess) return su;
     const bool np = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
     for (int cs = 1; cs <= (np ? 16 : 8); ++cs) {
       cudaLaunchConfig_t cfg = {};
@@ -1251,16 +1255,18 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       int n = 0;
-      act[cs] = cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess ? n : 0;
+      su.act[cs] = cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess ? n : 0;
     }
     cudaGetLastError();
     if (const char* dbg = std::getenv("PCR_DEBUG"); dbg && dbg[0] == '1') {
       std::fprintf(stderr, "suffix_attn<%d> max active clusters by size:", D);
-      for (int cs = 1; cs <= 16; ++cs) std::fprintf(stderr, " %d:%d", cs, act[cs]);
+      for (int cs = 1; cs <= 16; ++cs) std::fprintf(stderr, " %d:%d", cs, su.act[cs]);
       std::fprintf(stderr, "\n");
     }
-    configured = true;
-  }
+    return su;
+  }();
+  if (setup.err != cudaSuccess) return setup.err;
+  const int* act = setup.act;
   AttnParams p = p0;
   const int G = p.hq / p.hkv;
   EncodeTiledFn enc = encode_fn();
