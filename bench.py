@@ -752,7 +752,10 @@ def measure(args, torch, dist, world, rank, local):
                  "ttft_ms": sm_leg["ttft_ms"], "steps": sm_leg["steps"],
                  "note": "the same steps re-timed with the SM gather kernel after the timed region"}
     rl_attn = None if attn_tflops is None else {
-        "bound": "tensor", "kernel": "kv_append+suffix_attn", "achieved": attn_tflops, "peak": bf16_peak,
+        "bound": "tensor", "kernel": "suffix_attn (suffix append fused; + split-KV combine at short suffixes)",
+        "pipeline_regime": ("load-bound: achieved here is the load's pace; the kernel's own speed is 'isolated'"
+                            if N1 and attn_ms_iso == attn_ms_iso and gather_ms >= attn_ms_iso else "attention-bound"),
+        "achieved": attn_tflops, "peak": bf16_peak,
         "unit": "TFLOP/s", "frac": attn_tflops / bf16_peak,
         "traffic": ncu_t.get("attn_M7_r05", {}).get("dram_bytes") if (args.workload, args.ratio, shard) == ("M7", 0.5, 1)
         else None,
