@@ -50,10 +50,14 @@ constexpr int kBlockM = 128;   // rows per Q tile (= TMEM lanes)
 // 64-column halves -- the softmax below is written for any multiple of 64) measured 7% slower on
 // the M7 shapes (profiles/r02_block_n_128.txt): the lost S double-buffering costs more than the
 // halved barrier round trips and operand traffic save.
-constexpr int kBlockN = 64;
+#ifndef PCR_BLOCK_N
+#define PCR_BLOCK_N 64
+#endif
+constexpr int kBlockN = PCR_BLOCK_N;
+static_assert(kBlockN == 64 || kBlockN == 128, "64- or 128-key tiles");
 constexpr int kNQ = 2;         // Q tiles per CTA
 #ifndef PCR_KV_STAGES
-#define PCR_KV_STAGES 4
+#define PCR_KV_STAGES (256 / PCR_BLOCK_N)
 #endif
 constexpr int kStages = PCR_KV_STAGES;  // K/V smem ring depth
 constexpr int kThreads = 128 + kNQ * 128;
@@ -63,7 +67,7 @@ constexpr int kThreads = 128 + kNQ * 128;
 #ifndef PCR_Q_TMEM
 #define PCR_Q_TMEM 0
 #endif
-constexpr int kSBuf = PCR_Q_TMEM ? 1 : 2;   // S buffers per Q tile (barrier parity domain)
+constexpr int kSBuf = (PCR_Q_TMEM || kBlockN == 128) ? 1 : 2;   // S buffers per Q tile (barrier parity domain)
 // PCR_Q0_TMEM=1: Q tile 0 lives in TMEM and its QK^T runs as a TS MMA (A from TMEM: no shared-
 // memory traffic for A), Q tile 1 stays in shared memory (SS).  The 64 TMEM columns for Q0 come
 // from sharing THREE rotating S buffers between the two tiles instead of two per tile: S_t(j) goes
@@ -210,7 +214,8 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* s
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m, int32_t c0, int32_t c1,
@@ -250,6 +255,25 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+
+// Experiment knobs (mbarrier polling): the K/V-landed checks of tile 0's softmax warpgroup by ONE
+// thread instead of 128 (PCR_KV_WAIT_ONE; the p_full arrival of that thread still orders the MMA
+// warp after the loads), and every other wait of a converged warp by lane 0 + __syncwarp
+// (PCR_LANE0_WAIT): 128 threads polling one mbarrier compete with the producers' arrivals.
+#ifndef PCR_KV_WAIT_ONE
+#define PCR_KV_WAIT_ONE 1
+#endif
+#ifndef PCR_LANE0_WAIT
+#define PCR_LANE0_WAIT 0
+#endif
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  if (PCR_LANE0_WAIT) {
+    if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);
+    __syncwarp();
+  } else {
+    mbar_wait(bar, parity);
+  }
 }
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
@@ -310,6 +334,7 @@ __global__ void __maxnreg__(136)
   const int j_begin = blockIdx.z * per_split;
   const int j_end = min(j_begin + per_split, n_tiles_all);
   const int n_iter = max(0, j_end - j_begin);
+  auto tile_of = [&](int it) { return j_begin + it; };
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->q_full, PCR_Q_TMEM ? kNQ * 128 : PCR_Q0_TMEM ? 1 + 128 : 1);
@@ -395,26 +420,27 @@ __global__ void __maxnreg__(136)
                         i0 + t * tok_per_tile, &bars->q_full);
       }
       __syncwarp();
-      const int64_t layer_rows = p.n_pool_pages * p.hkv * 2 * p.S;
+      // pool rows fit in 32 bits (TMA coordinates are int32); S_pg is a power of two
+      const int layer_row0 = p.layer * (p.n_pool_pages * p.hkv * 2 * p.S);
+      const int s_log2 = 31 - __clz(p.S);
       const int box = min(p.S, kBlockN);  // rows per TMA box (the pool tensor map's box height)
       const int n_box = kBlockN / box;    // 1 .. kMaxBox (S_pg >= 16)
-      int pg_base = -64, pg_val = 0;
+      int pg_base = -64, pg_row = 0;      // lane l: pool row of K of request page pg_base + l
       uint64_t kv_policy = 0;
 #if PCR_KV_L2HINT
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(kv_policy));
 #endif
       // Pool row of K for box b of tile `tile` (V = + S), and whether the box holds suffix keys
       // (fused append: read from k_new/v_new; `dst` = it has a pool page to be written to).
-      auto box_rows = [&](int tile, int b, int64_t& row, bool& sfx, bool& dst) {
-        const int key = (j_begin + tile) * kBlockN + b * box;
-        const bool in_req = key / p.S < p.n_req_pages;
-        const int pidx = in_req ? key / p.S : p.n_req_pages - 1;  // clamp: finite, masked
+      auto box_rows = [&](int tile, int b, int& row, bool& sfx, bool& dst) {
+        const int key = tile_of(tile) * kBlockN + b * box;
+        const bool in_req = (key >> s_log2) < p.n_req_pages;
+        const int pidx = in_req ? key >> s_log2 : p.n_req_pages - 1;  // clamp: finite, masked
         if (pidx < pg_base || pidx >= pg_base + 32) {
           pg_base = pidx;
-          pg_val = pidx + lane < p.n_req_pages ? p.pages[pidx + lane] : 0;
+          pg_row = pidx + lane < p.n_req_pages ? layer_row0 + ((p.pages[pidx + lane] * p.hkv + g) << (s_log2 + 1)) : 0;
         }
-        const int64_t page = __shfl_sync(0xffffffffu, pg_val, pidx - pg_base);
-        row = int64_t(p.layer) * layer_rows + ((page * p.hkv + g) * 2 + 0) * p.S + (in_req ? key % p.S : 0);
+        row = __shfl_sync(0xffffffffu, pg_row, pidx - pg_base) + (in_req ? key & (p.S - 1) : 0);
         sfx = fold && key >= p.n1;
         dst = sfx && in_req;
       };
@@ -426,34 +452,31 @@ __global__ void __maxnreg__(136)
 #pragma unroll
         for (int b = 0; b < kMaxBox; ++b) {
           if (b < n_box) {
-            int64_t row;
+            int row;
             bool sfx, dst;
             box_rows(tile, b, row, sfx, dst);
             if (dst && lane == 0) {
 #pragma unroll
               for (int hf = 0; hf < Lay::kHalves; ++hf)
-                tma_store_2d(&tmap_pool, base + hf * Lay::kKVHalf + b * box * 128, hf * 64,
-                             int32_t(row + (v ? p.S : 0)));
+                tma_store_2d(&tmap_pool, base + hf * Lay::kKVHalf + b * box * 128, hf * 64, row + (v ? p.S : 0));
             }
             any |= dst;
           }
         }
-        if (any && lane == 0) {
-          bulk_commit();
-          bulk_wait_read0();   // the stage may be refilled once the stores have read it
-        }
+        (void)any;
+        if (lane == 0) bulk_commit();   // one bulk group per stored tile (empty when no box is suffix)
         __syncwarp();
       };
       // load the K (or V) tile `it` into stage it % kStages (boxes from the pool, or -- suffix keys,
       // fused append -- from k_new / v_new)
       auto load_tile = [&](int it, bool v) {
         const int st = it % kStages;
-        int64_t row_k[kMaxBox];
+        int row_k[kMaxBox];
         bool sfx[kMaxBox], dst_unused;
 #pragma unroll
         for (int b = 0; b < kMaxBox; ++b)
           if (b < n_box) box_rows(it, b, row_k[b], sfx[b], dst_unused);
-        const int sfx_row0 = (j_begin + it) * kBlockN - p.n1;   // suffix row of box 0 (fused append)
+        const int sfx_row0 = tile_of(it) * kBlockN - p.n1;   // suffix row of box 0 (fused append)
         uint8_t* dst_s = smem + (v ? Lay::kV0 : Lay::kK0) + st * Lay::kKVTile;
         uint64_t* full = v ? &bars->v_full[st] : &bars->k_full[st];
         if (elect_one()) {
@@ -471,44 +494,63 @@ __global__ void __maxnreg__(136)
                                 sfx_row0 + b * box, full);
                   else
                     tma_load_2d_kv(dst_s + hf * Lay::kKVHalf + b * box * 128, &tmap_pool, hf * 64,
-                                   int32_t(row_k[b] + (v ? p.S : 0)), full, kv_policy);
+                                   row_k[b] + (v ? p.S : 0), full, kv_policy);
                 }
           }
         }
         __syncwarp();
       };
       // K(j) and V(j) go into stage j % kStages once their previous occupants are consumed: K after
-      // the last QK^T that read it (k_empty), V after the last PV (v_empty) -- and, in a writer CTA,
-      // after the previous occupant's suffix boxes have been stored into the pool.
-      for (int it = 0; it < n_iter; ++it) {
+      // the last QK^T that read it (k_empty), V after the last PV (v_empty).  A writer CTA (fused
+      // append) stores the suffix boxes of tile j into the pool from the stage it landed in, issued
+      // kStoreLag tiles later (j has landed by then: its wait is short) and without waiting for the
+      // store: one bulk group per tile, so before tile j + kStages refills the stage only the
+      // kStages - kStoreLag - 1 latest groups may still be reading (4 stages: wait_group.read 1).
+#if PCR_ATTN_TIMING
+      long long pw_ = 0, pl_ = 0, pc_ = clock64();
+#define PCR_PTICK(acc) do { const long long n_ = clock64(); acc += n_ - pc_; pc_ = n_; } while (0)
+#else
+#define PCR_PTICK(acc) do { } while (0)
+#endif
+      constexpr int kStoreLag = kStages > 2 ? 2 : 1;
+      static_assert(kStoreLag < kStages, "a tile is stored before its stage is refilled");
+      auto produce = [&](int it, bool v) {
         const int st = it % kStages;
-        const uint32_t ph = ((it / kStages) - 1) & 1;
-        if (do_k) {
-          if (it >= kStages) {
-            mbar_wait(&bars->k_empty[st], ph);
-            if (writer) store_tile(it - kStages, false);
+        if (it >= kStages) {
+          mbar_wait(v ? &bars->v_empty[st] : &bars->k_empty[st], ((it / kStages) - 1) & 1);
+          PCR_PTICK(pw_);
+          if (writer) {
+            if (lane == 0) bulk_wait_read<kStages - kStoreLag - 1>();
+            __syncwarp();
           }
-          load_tile(it, false);
         }
-        if (do_v) {
-          if (it >= kStages) {
-            mbar_wait(&bars->v_empty[st], ph);
-            if (writer) store_tile(it - kStages, true);
-          }
-          load_tile(it, true);
+        load_tile(it, v);
+        if (writer && it >= kStoreLag) {
+          const int js = it - kStoreLag;
+          mbar_wait(v ? &bars->v_full[js % kStages] : &bars->k_full[js % kStages], (js / kStages) & 1);
+          store_tile(js, v);
         }
+        PCR_PTICK(pl_);
+      };
+      for (int it = 0; it < n_iter; ++it) {
+        if (do_k) produce(it, false);
+        if (do_v) produce(it, true);
       }
+#if PCR_ATTN_TIMING
+      if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 8 || blockIdx.x == 300) && blockIdx.z == 0)
+        printf("PRODTIMING blk %d warp %d iters %d: empty-wait %lld load-issue %lld (clk/iter)\n", blockIdx.x, warp,
+               n_iter, pw_ / max(n_iter, 1), pl_ / max(n_iter, 1));
+#endif
       if (writer) {
-        // the last kStages tiles are never refilled: store their suffix boxes once they have landed
-        for (int it = max(0, n_iter - kStages); it < n_iter; ++it) {
-          const int st = it % kStages;
+        // the last kStoreLag tiles: store once they have landed, then wait for every pool write
+        for (int js = max(0, n_iter - kStoreLag); js < n_iter; ++js) {
           if (do_k) {
-            mbar_wait(&bars->k_full[st], (it / kStages) & 1);
-            store_tile(it, false);
+            mbar_wait(&bars->k_full[js % kStages], (js / kStages) & 1);
+            store_tile(js, false);
           }
           if (do_v) {
-            mbar_wait(&bars->v_full[st], (it / kStages) & 1);
-            store_tile(it, true);
+            mbar_wait(&bars->v_full[js % kStages], (js / kStages) & 1);
+            store_tile(js, true);
           }
         }
         if (lane == 0) bulk_wait0();   // the pool writes are complete (visible after the grid)
@@ -595,7 +637,7 @@ __global__ void __maxnreg__(136)
       for (int it = 0; it < n_iter; ++it) {
         const bool more = it + kSBuf < n_iter;
         PCR_MTICK(2);
-        if ((PCR_ATTN_PROFILE & 8) == 0) mbar_wait(&bars->p_full[0][it % kSBuf], (it / kSBuf) & 1);
+        if ((PCR_ATTN_PROFILE & 8) == 0) mbar_wait_warp(&bars->p_full[0][it % kSBuf], (it / kSBuf) & 1);
         tc_fence_after();
         PCR_MTICK(1);
         issue_pv(0, it);
@@ -605,7 +647,7 @@ __global__ void __maxnreg__(136)
           issue_s(0, it + kSBuf);
         }
         PCR_MTICK(2);
-        if ((PCR_ATTN_PROFILE & 8) == 0) mbar_wait(&bars->p_full[1][it % kSBuf], (it / kSBuf) & 1);
+        if ((PCR_ATTN_PROFILE & 8) == 0) mbar_wait_warp(&bars->p_full[1][it % kSBuf], (it / kSBuf) & 1);
         tc_fence_after();
         PCR_MTICK(1);
         issue_pv(1, it);
@@ -658,6 +700,12 @@ __global__ void __maxnreg__(136)
 #if PCR_EXP_PINGPONG
     if (t == 1 && n_iter > 0) named_bar_arrive(1, 256);  // tile 0 takes the first turn
 #endif
+#if PCR_ATTN_TIMING
+    long long tm_[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tc_ = clock64();
+#define PCR_TICK(k) do { const long long n_ = clock64(); tm_[k] += n_ - tc_; tc_ = n_; } while (0)
+#else
+#define PCR_TICK(k) do { } while (0)
+#endif
     const uint64_t scale2 = f2_pack(p.scale_log2, p.scale_log2);
     // Before publishing P_t(it) the warpgroup checks that the tiles the MMA warp reads right after
     // it have landed (the MMA warp waits only for P): PV_t(it) reads V(it); the S issued next reads
@@ -670,8 +718,9 @@ __global__ void __maxnreg__(136)
         } else if (it + 2 < n_iter) {
           mbar_wait(&bars->k_full[(it + 2) % kStages], ((it + 2) / kStages) & 1);
         }
-      } else if (t == 0) {
+      } else if (t == 0 && (!PCR_KV_WAIT_ONE || r == 0)) {
         mbar_wait(&bars->v_full[it % kStages], (it / kStages) & 1);
+        PCR_TICK(8);
         if (it + kSBuf < n_iter) mbar_wait(&bars->k_full[(it + kSBuf) % kStages], ((it + kSBuf) / kStages) & 1);
       }
     };
@@ -694,18 +743,12 @@ __global__ void __maxnreg__(136)
       mbar_arrive(&bars->q_full);
     }
 #endif
-#if PCR_ATTN_TIMING
-    long long tm_[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tc_ = clock64();
-#define PCR_TICK(k) do { const long long n_ = clock64(); tm_[k] += n_ - tc_; tc_ = n_; } while (0)
-#else
-#define PCR_TICK(k) do { } while (0)
-#endif
     for (int it = 0; it < n_iter; ++it) {
-      const int key0 = (j_begin + it) * kBlockN;
+      const int key0 = tile_of(it) * kBlockN;
       const bool diag = key0 + kBlockN - 1 > tile_first_key_limit;  // tile crosses this Q tile's diagonal
       const uint32_t s_col = lane_base + s_buf_col(t, it);
       PCR_TICK(5);
-      mbar_wait(&bars->s_full[t][it % kSBuf], (it / kSBuf) & 1);
+      mbar_wait_warp(&bars->s_full[t][it % kSBuf], (it / kSBuf) & 1);
       tc_fence_after();
       PCR_TICK(0);
       if (PCR_ATTN_PROFILE & 1) {
@@ -846,10 +889,10 @@ __global__ void __maxnreg__(136)
       m_raw = m_use;
     }
 #if PCR_ATTN_TIMING
-    if ((threadIdx.x & 31) == 0 && (blockIdx.x == 0 || blockIdx.x == 300) && blockIdx.z == 0)
-      printf("TIMING blk %d warp %d iters %d: wait %lld ld %lld max+kvwait %lld turn %lld exp %lld post %lld loop %lld\n",
+    if ((threadIdx.x & 31) == 0 && (blockIdx.x == 0 || blockIdx.x == 8 || blockIdx.x == 300) && blockIdx.z == 0)
+      printf("TIMING blk %d warp %d iters %d: wait %lld ld %lld max %lld vwait %lld kwait %lld turn %lld exp %lld post %lld loop %lld\n",
              blockIdx.x, threadIdx.x >> 5, n_iter, tm_[0] / max(n_iter, 1), tm_[1] / max(n_iter, 1),
-             (tm_[2] + tm_[6]) / max(n_iter, 1), tm_[7] / max(n_iter, 1),
+             tm_[2] / max(n_iter, 1), tm_[8] / max(n_iter, 1), tm_[6] / max(n_iter, 1), tm_[7] / max(n_iter, 1),
              tm_[3] / max(n_iter, 1), tm_[4] / max(n_iter, 1), tm_[5] / max(n_iter, 1));
 #endif
     // ---------------------------------------------------------------- epilogue
