@@ -101,6 +101,10 @@ struct AttnParams {
   // 1: no kernel before this one in the stream writes anything it reads (fused append): PDL's
   // griddepcontrol.wait moves from the prologue to just before the epilogue's global writes.
   int32_t late_dep_wait;
+  // Set by the launcher: the epilogue stages O (bf16 out, or the fp32 split-KV / context-split
+  // partial) in shared memory and writes it with TMA stores (coalesced, rows past N2 clipped)
+  // instead of one row per thread from registers.
+  int32_t tma_epilogue;
 };
 
 // Merge n_parts partials (O normalised per part, log2-domain LSE; part s at o + s*o_stride and

@@ -213,6 +213,21 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* s
                "r"(c0), "r"(c1), "r"(smem_u32(smem_src))
                : "memory");
 }
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* smem_src, int32_t c0, int32_t c1,
+                                             int32_t c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(smem_src))
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, const void* smem_src, int32_t c0, int32_t c1,
+                                             int32_t c2, int32_t c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(smem_src))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
@@ -311,7 +326,7 @@ template <int D>
 __global__ void __maxnreg__(136)
     suffix_attn_kernel(const __grid_constant__ CUtensorMap tmap_pool, const __grid_constant__ CUtensorMap tmap_q,
                        const __grid_constant__ CUtensorMap tmap_kn, const __grid_constant__ CUtensorMap tmap_vn,
-                       const AttnParams p) {
+                       const __grid_constant__ CUtensorMap tmap_out, const AttnParams p) {
   using Lay = Layout<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -320,6 +335,14 @@ __global__ void __maxnreg__(136)
   // warp index through a shuffle: provably warp-uniform, so role branches are uniform and the MMA
   // and TMA loops keep counters and descriptors in uniform registers (no R2UR per instruction)
   const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+#ifndef PCR_ATTN_TIMELINE
+#define PCR_ATTN_TIMELINE 0
+#endif
+#if PCR_ATTN_TIMELINE
+  // experiment: per-CTA timeline (globaltimer ns) printed by the first softmax thread
+  const uint64_t tl_start = globaltimer_ns();
+  uint64_t tl_loop0 = 0, tl_loop1 = 0;
+#endif
   // Longest-processing-time-first order (causal: the last M-blocks see the most keys)
   const int G = p.hq / p.hkv;
   const int tok_per_tile = kBlockM / G;
@@ -712,6 +735,7 @@ __global__ void __maxnreg__(136)
     // K(it+2) (two S buffers per tile), or in the Q0 mode K(it+1) after P0 and K(it+2) after P1.
     auto wait_kv_for_next_mmas = [&](int it) {
       if (PCR_Q0_TMEM) {
+        if (PCR_KV_WAIT_ONE && r != 0) return;
         if (t == 0) {
           mbar_wait(&bars->v_full[it % kStages], (it / kStages) & 1);
           if (it + 1 < n_iter) mbar_wait(&bars->k_full[(it + 1) % kStages], ((it + 1) / kStages) & 1);
@@ -751,6 +775,9 @@ __global__ void __maxnreg__(136)
       mbar_wait_warp(&bars->s_full[t][it % kSBuf], (it / kSBuf) & 1);
       tc_fence_after();
       PCR_TICK(0);
+#if PCR_ATTN_TIMELINE
+      if (it == 0) tl_loop0 = globaltimer_ns();
+#endif
       if (PCR_ATTN_PROFILE & 1) {
         tc_fence_before();
         wait_kv_for_next_mmas(it);
@@ -896,6 +923,9 @@ __global__ void __maxnreg__(136)
              tm_[3] / max(n_iter, 1), tm_[4] / max(n_iter, 1), tm_[5] / max(n_iter, 1));
 #endif
     // ---------------------------------------------------------------- epilogue
+#if PCR_ATTN_TIMELINE
+    tl_loop1 = globaltimer_ns();
+#endif
     if (p.late_dep_wait) grid_dep_wait();
     const bool row_ok = i < p.n2;
     const int64_t row_id = int64_t(i) * p.hq + qh;
@@ -910,6 +940,63 @@ __global__ void __maxnreg__(136)
       ep_lse = (n_iter > 0 && l > 0.f) ? m_raw * p.scale_log2 + __log2f(l) : -INFINITY;
       ep_inv_l = inv_l;
       reinterpret_cast<float*>(smem + Lay::kLse)[t * kBlockM + r] = ep_lse;
+    } else if (p.tma_epilogue) {
+      // O (bf16, or the fp32 partial) -> shared memory in the TMA box layout (128-byte rows,
+      // SWIZZLE_128B: 16-byte chunk c of row r at r*128 + ((c ^ r%8) << 4)), then one thread of the
+      // warpgroup stores the tile with TMA: coalesced, and rows past N2 are clipped by the map.
+      // Staging reuses [0, 64 KB) (bf16) or [0, 128 KB) (fp32) of the Q tiles and K ring, free once
+      // o_full certifies every MMA -- and, in a writer CTA, once its pool stores have read the ring.
+      const bool f32 = !(p.n_splits == 1 && p.part_o == nullptr);
+      if (writer) mbar_wait(&bars->store_done, 0);
+      uint8_t* stage = smem + t * (f32 ? kBlockM * D * 4 : Lay::kQTile);
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        float o[32];
+        if (n_iter > 0) {
+          tmem_ld32(o_col + c * 32, o);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = 0.f;
+        }
+        if (f32) {
+          uint8_t* box = stage + c * (kBlockM * 128) + r * 128;
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            *reinterpret_cast<float4*>(box + ((e ^ (r & 7)) << 4)) =
+                make_float4(o[4 * e] * inv_l, o[4 * e + 1] * inv_l, o[4 * e + 2] * inv_l, o[4 * e + 3] * inv_l);
+        } else {
+#pragma unroll
+          for (int q8 = 0; q8 < 4; ++q8) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 b = __floats2bfloat162_rn(o[q8 * 8 + 2 * e] * inv_l, o[q8 * 8 + 2 * e + 1] * inv_l);
+              w[e] = *reinterpret_cast<uint32_t*>(&b);
+            }
+            const int chunk = c * 4 + q8;   // 16-byte chunk of the row (8 per 64-column half)
+            *reinterpret_cast<uint4*>(stage + (chunk >> 3) * Lay::kQHalf + r * 128 + (((chunk & 7) ^ (r & 7)) << 4)) =
+                make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+      if (f32 && row_ok)
+        (p.ws_lse + int64_t(blockIdx.z) * p.n2 * p.hq)[row_id] =
+            (n_iter > 0 && l > 0.f) ? m_raw * p.scale_log2 + __log2f(l) : -INFINITY;
+      fence_proxy_async_smem();
+      named_bar_sync(3 + t, 128);
+      if (r == 0) {
+        const int tok0 = i0 + t * tok_per_tile;
+        if (f32) {
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) tma_store_4d(&tmap_out, stage + c * (kBlockM * 128), c * 32, g * G, tok0, blockIdx.z);
+        } else {
+#pragma unroll
+          for (int hf = 0; hf < Lay::kHalves; ++hf) tma_store_3d(&tmap_out, stage + hf * Lay::kQHalf, hf * 64, g * G, tok0);
+        }
+        bulk_commit();
+        bulk_wait0();   // complete before the CTA's shared memory is released
+      }
     } else if (p.n_splits == 1 && p.part_o == nullptr) {
       uint4* dst = reinterpret_cast<uint4*>(p.out + row_id * D);
 #pragma unroll
@@ -1116,6 +1203,14 @@ __global__ void __maxnreg__(136)
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
   }
+#if PCR_ATTN_TIMELINE
+  if (threadIdx.x == 128) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    printf("TL %d %d %d %u %llu %llu %llu %llu\n", p.layer, blockIdx.x, blockIdx.z, smid, (unsigned long long)tl_start,
+           (unsigned long long)tl_loop0, (unsigned long long)tl_loop1, (unsigned long long)globaltimer_ns());
+  }
+#endif
 }
 
 // Merge split-KV partials: out = sum_s 2^(lse_s - M) O_s / sum_s 2^(lse_s - M), M = max_s lse_s.
@@ -1260,6 +1355,15 @@ bool split_spin_enabled() {
   return on;
 }
 
+// TMA-store epilogue (PCR_TMA_EPILOGUE=0 restores the per-thread row stores).
+bool tma_epilogue_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PCR_TMA_EPILOGUE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // SMs the split-KV sizing may count on (PCR_ATTN_SMS; default all 148).
 int attn_sm_budget() {
   static const int n = [] {
@@ -1372,9 +1476,35 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
     p.ws_o = p.part_o;
     p.ws_lse = p.part_lse;
   }
+  // TMA-store epilogue (PCR_TMA_EPILOGUE=0: one row per thread from registers): bf16 out as a 3D
+  // map like q's, or the fp32 partial [splits][N2][Hq][D] as a 4D map with 32-float (128-byte) boxes
+  CUtensorMap tmap_out = tmap_q;
+  p.tma_epilogue = 0;
+  if (tma_epilogue_enabled() && !p.cluster_reduce && !p.spin_reduce) {
+    const bool f32 = !(splits == 1 && p.part_o == nullptr);
+    CUresult r;
+    if (f32) {
+      cuuint64_t dims[4] = {cuuint64_t(D), cuuint64_t(p.hq), cuuint64_t(p.n2), cuuint64_t(splits)};
+      cuuint64_t strides[3] = {cuuint64_t(D) * 4, cuuint64_t(p.hq) * D * 4, cuuint64_t(p.n2) * p.hq * D * 4};
+      cuuint32_t box[4] = {32, cuuint32_t(G), cuuint32_t(kBlockM / G), 1};
+      cuuint32_t estr[4] = {1, 1, 1, 1};
+      r = enc(&tmap_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.ws_o, dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+      cuuint64_t dims[3] = {cuuint64_t(D), cuuint64_t(p.hq), cuuint64_t(p.n2)};
+      cuuint64_t strides[2] = {cuuint64_t(D) * 2, cuuint64_t(p.hq) * D * 2};
+      cuuint32_t box[3] = {64, cuuint32_t(G), cuuint32_t(kBlockM / G)};
+      cuuint32_t estr[3] = {1, 1, 1};
+      r = enc(&tmap_out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, p.out, dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    p.tma_epilogue = r == CUDA_SUCCESS ? 1 : 0;
+  }
   dim3 grid(n_mblocks * p.hkv, 1, splits);
   cudaError_t e = launch_pdl(kern, grid, dim3(kThreads), Layout<D>::kAlloc, stream, p.cluster_reduce ? splits : 1,
-                             *tmap_pool, tmap_q, tmap_kn, tmap_vn, p);
+                             *tmap_pool, tmap_q, tmap_kn, tmap_vn, tmap_out, p);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   *launches += 1;
