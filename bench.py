@@ -574,6 +574,21 @@ def measure(args, torch, dist, world, rank, local):
     torch.cuda.synchronize()
     total_ms = ev0.elapsed_time(ev1)
     launches = ctx.kernel_launches - launches0
+    if os.environ.get("PCR_BENCH_TIMELINE"):   # experiment (-DPCR_ATTN_TIMELINE=1 build): one more step's CTA timeline
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import ctypes
+        from attn_timeline import read_tl, summarise
+        lib = ctx.lib
+        lib.pcr_debug_attn_timeline.argtypes = [ctypes.c_void_p, ctypes.c_longlong]
+        lib.pcr_debug_attn_timeline_clear()
+        e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_a.record(cs)
+        ls.wait_event(e_a)
+        step(q_d, k_d, v_d, out_d)
+        e_b.record(cs)
+        e_b.synchronize()
+        print(json.dumps({"timeline_step_ms": e_a.elapsed_time(e_b)}), file=sys.stderr)
+        summarise(read_tl(lib), L, "bench step")
     stats1 = ctx.stats
     ce_layers = stats1["ce_layer_loads"] - stats0["ce_layer_loads"]
     ce_copies_per_layer = (stats1["ce_copies"] - stats0["ce_copies"]) / max(1, ce_layers)

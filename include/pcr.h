@@ -242,7 +242,10 @@ pcr_status pcr_prefill_attn_layer(pcr_ctx* ctx, int64_t req_id, int32_t layer, c
 
 /* a5 — the whole layer pipeline for one planned request (Alg.1):
  *   mode 0 OVERLAP: load_stream: ONE streamed gather launch moves every layer in order and
- *                   publishes layer l through a per-layer completion counter (release);
+ *                   publishes layer l through a per-layer completion counter (release); the
+ *                   launch runs on a library-owned stream of the device's greatest priority,
+ *                   forked from and joined back into load_stream, so its CTAs are dispatched
+ *                   ahead of any attention CTA waiting for them (no caller priority needed);
  *                   compute_stream: attn(0), attn(1), ... each acquiring its layer's counter
  *                   in-kernel before its first load (the suffix append is fused into the
  *                   attention), so gather(l+1) overlaps attn(l).  With the copy-engine / TMA

@@ -320,6 +320,13 @@ __device__ __forceinline__ void exp2_poly2(uint64_t x2, float& y0, float& y1) {
   y1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
 }
 
+#if PCR_ATTN_TIMELINE
+// experiment: per-CTA timeline (globaltimer ns: start, first S ready, main loop end, end; SM; key
+// tiles) of the last launch of each layer, read back with pcr_debug_attn_timeline
+constexpr int kTlLayers = 128, kTlCtas = 2048;
+__device__ unsigned long long g_timeline[kTlLayers][kTlCtas][6];
+#endif
+
 // 136 registers x 384 threads = 52K of the SM's 64K: a 256-thread gather CTA (10K) still fits
 // beside an attention CTA, so layer l+1's host->HBM load never waits for attention SMs.
 template <int D>
@@ -1207,8 +1214,16 @@ __global__ void __maxnreg__(136)
   if (threadIdx.x == 128) {
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    printf("TL %d %d %d %u %llu %llu %llu %llu\n", p.layer, blockIdx.x, blockIdx.z, smid, (unsigned long long)tl_start,
-           (unsigned long long)tl_loop0, (unsigned long long)tl_loop1, (unsigned long long)globaltimer_ns());
+    const uint32_t cta = blockIdx.z * gridDim.x + blockIdx.x;
+    if (p.layer < kTlLayers && cta < kTlCtas) {
+      unsigned long long* rec = g_timeline[p.layer][cta];
+      rec[0] = tl_start;
+      rec[1] = tl_loop0;
+      rec[2] = tl_loop1;
+      rec[3] = globaltimer_ns();
+      rec[4] = smid;
+      rec[5] = uint64_t(n_iter);
+    }
   }
 #endif
 }
@@ -1549,3 +1564,16 @@ cudaError_t launch_suffix_attn(const CUtensorMap* tmap_pool, const AttnParams& p
 }
 
 }  // namespace pcr
+
+#if PCR_ATTN_TIMELINE
+extern "C" int pcr_debug_attn_timeline(void* host_dst, long long bytes) {
+  const long long n = sizeof(pcr::g_timeline) < (unsigned long long)bytes ? (long long)sizeof(pcr::g_timeline) : bytes;
+  if (cudaMemcpyFromSymbol(host_dst, pcr::g_timeline, size_t(n)) != cudaSuccess) return -1;
+  return 0;
+}
+extern "C" int pcr_debug_attn_timeline_clear() {
+  void* p = nullptr;
+  if (cudaGetSymbolAddress(&p, pcr::g_timeline) != cudaSuccess) return -1;
+  return cudaMemset(p, 0, sizeof(pcr::g_timeline)) == cudaSuccess ? 0 : -1;
+}
+#endif

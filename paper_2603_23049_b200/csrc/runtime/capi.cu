@@ -84,6 +84,12 @@ struct pcr_ctx {
   // attention launches of the current pcr_run_prefill call wait on (null outside such a call)
   int32_t* d_ready = nullptr;
   cudaEvent_t ev_ready_zero = nullptr;
+  // The streamed gather runs on a library-owned stream of the device's greatest priority, forked
+  // from and joined back into the caller's load stream: its CTAs are dispatched ahead of the
+  // attention grid's pending CTAs, which wait in-kernel for its per-layer counters (without the
+  // priority a full attention grid queued first could keep the gather from ever being scheduled).
+  cudaStream_t gather_hi = nullptr;
+  cudaEvent_t ev_gather_fork = nullptr, ev_gather_join = nullptr;
   const int32_t* cur_ready = nullptr;
   int32_t cur_ready_target = 0;
 };
@@ -556,8 +562,18 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
   } ready_reset{c};
   if (streamed) {
     int32_t* ready = c->d_ready + int64_t(r->plan.region) * L;
-    CUDA_TRY(c, cudaMemsetAsync(ready, 0, sizeof(int32_t) * L, ls));
-    CUDA_TRY(c, cudaEventRecord(c->ev_ready_zero, ls));
+    if (!c->gather_hi) {
+      int lo = 0, hi = 0;
+      CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CUDA_TRY(c, cudaStreamCreateWithPriority(&c->gather_hi, cudaStreamNonBlocking, hi));
+      CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_gather_fork, cudaEventDisableTiming));
+      CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_gather_join, cudaEventDisableTiming));
+    }
+    cudaStream_t gs = c->gather_hi;
+    CUDA_TRY(c, cudaEventRecord(c->ev_gather_fork, ls));
+    CUDA_TRY(c, cudaStreamWaitEvent(gs, c->ev_gather_fork, 0));
+    CUDA_TRY(c, cudaMemsetAsync(ready, 0, sizeof(int32_t) * L, gs));
+    CUDA_TRY(c, cudaEventRecord(c->ev_ready_zero, gs));
     CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_ready_zero, 0));   // (not the gather itself)
     pcr::LinearCopies lin{};
     if (o.host_io) {
@@ -572,11 +588,13 @@ pcr_status run_prefill_impl(pcr_ctx* c, int64_t req_id, const void* q_all, const
         lin.dst_stride16[i] = io_layer * 2 / 16;
       }
     }
-    if (times) CUDA_TRY(c, cudaEventRecord(c->ev_t[0], ls));
+    if (times) CUDA_TRY(c, cudaEventRecord(c->ev_t[0], gs));
     int32_t warps = 0;
     CUDA_TRY(c, pcr::launch_kv_gather_stream(c->store_dev, c->cfg.pool, d_slots_of(c, r), d_pages_of(c, r),
-                                             r->plan.n_matched, c->geom, c->gather_ctas, &lin, ready, ls, &warps));
-    if (times) CUDA_TRY(c, cudaEventRecord(c->ev_t[1], ls));
+                                             r->plan.n_matched, c->geom, c->gather_ctas, &lin, ready, gs, &warps));
+    if (times) CUDA_TRY(c, cudaEventRecord(c->ev_t[1], gs));
+    CUDA_TRY(c, cudaEventRecord(c->ev_gather_join, gs));
+    CUDA_TRY(c, cudaStreamWaitEvent(ls, c->ev_gather_join, 0));
     c->launches += 1;
     if (r->plan.n_matched > 0) c->sm_layer_loads += L;
     c->cur_ready = ready;
@@ -873,6 +891,9 @@ void pcr_destroy(pcr_ctx* c) {
     for (auto e : c->ev_t) cudaEventDestroy(e);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_ready_zero) cudaEventDestroy(c->ev_ready_zero);
+    if (c->ev_gather_fork) cudaEventDestroy(c->ev_gather_fork);
+    if (c->ev_gather_join) cudaEventDestroy(c->ev_gather_join);
+    if (c->gather_hi) cudaStreamDestroy(c->gather_hi);
     if (c->d_ready) cudaFree(c->d_ready);
     if (c->ev_comm) cudaEventDestroy(c->ev_comm);
     if (c->ev_off) cudaEventDestroy(c->ev_off);

@@ -739,3 +739,52 @@ def test_two_requests_in_flight_on_two_streams():
             assert np.array_equal(pool[l][pg], exp[l][pg]), (rid, l)
     for rid, *_ in reqs:
         rig.ctx.release(rid, False)
+
+
+@pytest.mark.gpu
+def test_streamed_pipeline_with_default_priority_streams_never_starves_the_gather():
+    """Regression: the streamed OVERLAP pipeline with the caller's streams at default priority and
+    a multi-wave attention grid (M7-shaped suffix, 528 CTAs per layer).  The attention CTAs wait
+    in-kernel for the gather's per-layer counters; the library runs the gather on its own
+    greatest-priority stream so a full attention grid queued first cannot keep it from being
+    dispatched (before the fix some runs ended in the attention's 10 s trap).  Every run must
+    complete and give the same output as the per-layer API on the same request."""
+    import torch
+    from paper_2603_23049_b200 import Context
+    from pcrgen import randn_bf16
+    L, Hq, Hkv, d, C, S, N1, N2 = 8, 32, 8, 128, 256, 64, 4096, 4224
+    rng = make_rng(31)
+    n_pages = 2 * (-(-(N1 + N2) // S)) + 4
+    pool = torch.zeros(n_pages * L * Hkv * 2 * S * d, dtype=torch.int16, device="cuda")
+    ctx = Context(L, Hq, Hkv, d, C, S, N1 // C + 2, 0, device=torch.cuda.current_device(), pool=pool)
+    doc = rng.integers(0, 1000, N1, dtype=np.uint32)
+    ctx.submit(0, np.concatenate([doc, [1]]).astype(np.uint32))
+    for s in ctx.match_prefix(0, [])["slots"]:
+        ctx.store_write(s, randn_bf16(rng, (ctx.slot_bytes // 2,)))
+    ctx.release(0, True)
+    toks = np.concatenate([doc, rng.integers(0, 1000, N2, dtype=np.uint32)])
+    q, k, v = (to_dev(randn_bf16(rng, (L, N2, h, d))) for h in (Hq, Hkv, Hkv))
+    cs, ls = torch.cuda.Stream(), torch.cuda.Stream()   # default priority
+    outs = []
+    for rid in range(1, 5):
+        ctx.submit(rid, toks, n_cacheable=N1)
+        assert ctx.match_prefix(rid, [])["n1"] == N1
+        o = torch.empty_like(q)
+        ctx.run_prefill(rid, q, k, v, o, cs, ls)
+        cs.synchronize()
+        outs.append(to_host(o))
+        ctx.release(rid, False)
+    ctx.submit(9, toks, n_cacheable=N1)
+    ctx.match_prefix(9, [])
+    o = torch.empty_like(q)
+    for l in range(L):
+        ctx.load_layer_kv(9, l, ls)
+        ev = torch.cuda.Event()
+        ev.record(ls)
+        cs.wait_event(ev)
+        ctx.prefill_attn_layer(9, l, q[l], k[l], v[l], o[l], cs)
+    cs.synchronize()
+    ctx.release(9, False)
+    ctx.close()
+    for x in outs:
+        assert np.array_equal(x, to_host(o))

@@ -17,7 +17,7 @@ from paper_2603_23049_b200 import Context  # noqa: E402
 from pcrgen import make_rng, randn_bf16  # noqa: E402
 
 
-def run(n1, n2, hq, hkv, d=128, L=4, iters=20, C=256, S=64):
+def run(n1, n2, hq, hkv, d=128, L=4, iters=20, C=256, S=64, bg=""):
     rng = make_rng(3)
     N = n1 + n2
     n_pages = 2 * (-(-N // S)) + 4
@@ -58,6 +58,21 @@ def run(n1, n2, hq, hkv, d=128, L=4, iters=20, C=256, S=64):
             pass
     th = threading.Thread(target=poll, daemon=True)
     th.start()
+    # interference experiment: a background host->HBM stream on another stream during the timed
+    # region -- "gather": the SM gather kernel re-loading the request's prefix (same bytes, same
+    # pages); "ce": copy-engine cudaMemcpyAsync of a pinned host buffer (no SMs)
+    if bg:
+        bs = torch.cuda.Stream()
+        if bg == "gather":
+            for _ in range(iters * 2):
+                for l in range(L):
+                    ctx.load_layer_kv(1, l, bs)
+        elif bg == "ce":
+            hb = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+            db = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+            with torch.cuda.stream(bs):
+                for _ in range(iters // 2 + 1):
+                    db.copy_(hb, non_blocking=True)
     a.record(cs)
     for _ in range(iters):
         for l in range(L):
@@ -70,7 +85,9 @@ def run(n1, n2, hq, hkv, d=128, L=4, iters=20, C=256, S=64):
     flops = 4 * hq * d * (n2 * n1 + n2 * (n2 + 1) // 2)
     ctx.release(1, False)
     ctx.close()
-    return dict(n1=n1, n2=n2, hq=hq, hkv=hkv, ms_per_layer=ms, tflops=flops / ms / 1e9,
+    if bg:
+        torch.cuda.synchronize()
+    return dict(n1=n1, n2=n2, hq=hq, hkv=hkv, bg=bg or None, ms_per_layer=ms, tflops=flops / ms / 1e9,
                 sm_mhz=sorted(clk)[len(clk) // 2] if clk else None)
 
 
@@ -80,6 +97,8 @@ if __name__ == "__main__":
     ap.add_argument("--small", action="store_true",
                     help="short-suffix shapes only: L8 at P=1/2/4/8 head slices, L70 r=1 rank slice of 8")
     ap.add_argument("--shape", default="", help="one shape n1,n2,hq,hkv")
+    ap.add_argument("--bg", default="", choices=["", "gather", "ce"],
+                    help="background host->HBM traffic during the timed region (interference experiment)")
     args = ap.parse_args()
     shapes = [(0, 8320, 32, 8), (4096, 4224, 32, 8), (6144, 2176, 32, 8), (4096, 128, 32, 8), (8192, 8320, 64, 8)]
     if args.small:
@@ -87,4 +106,4 @@ if __name__ == "__main__":
     if args.shape:
         shapes = [tuple(int(x) for x in args.shape.split(","))]
     for n1, n2, hq, hkv in shapes:
-        print(json.dumps(run(n1, n2, hq, hkv, iters=args.iters)), flush=True)
+        print(json.dumps(run(n1, n2, hq, hkv, iters=args.iters, bg=args.bg)), flush=True)
