@@ -74,7 +74,7 @@ constexpr int kSBuf = (PCR_Q_TMEM || kBlockN == 128) ? 1 : 2;   // S buffers per
 // to buffer (2j + t) % 3, and the MMA issue order [P0(j)] PV0(j) S1(j+1) [P1(j)] PV1(j) S0(j+2)
 // only ever writes the buffer the PV just issued has read (MMAs of one thread run in order).
 #ifndef PCR_Q0_TMEM
-#define PCR_Q0_TMEM 0
+#define PCR_Q0_TMEM 1
 #endif
 static_assert(!(PCR_Q0_TMEM && PCR_Q_TMEM), "one Q-in-TMEM mode at a time");
 constexpr int kSCols = PCR_Q0_TMEM ? 3 * kBlockN : kSBuf * kNQ * kBlockN;   // TMEM columns of S
