@@ -17,7 +17,7 @@ from paper_2603_23049_b200 import Context  # noqa: E402
 from pcrgen import make_rng, randn_bf16  # noqa: E402
 
 
-def run(n1, n2, hq, hkv, d=128, L=4, iters=20, C=256, S=64, bg=""):
+def run(n1, n2, hq, hkv, d=128, L=32, iters=20, C=256, S=64, bg=""):
     rng = make_rng(3)
     N = n1 + n2
     n_pages = 2 * (-(-N // S)) + 4
@@ -87,7 +87,7 @@ def run(n1, n2, hq, hkv, d=128, L=4, iters=20, C=256, S=64, bg=""):
     ctx.close()
     if bg:
         torch.cuda.synchronize()
-    return dict(n1=n1, n2=n2, hq=hq, hkv=hkv, bg=bg or None, ms_per_layer=ms, tflops=flops / ms / 1e9,
+    return dict(n1=n1, n2=n2, hq=hq, hkv=hkv, L=L, bg=bg or None, ms_per_layer=ms, tflops=flops / ms / 1e9,
                 sm_mhz=sorted(clk)[len(clk) // 2] if clk else None)
 
 
@@ -97,6 +97,8 @@ if __name__ == "__main__":
     ap.add_argument("--small", action="store_true",
                     help="short-suffix shapes only: L8 at P=1/2/4/8 head slices, L70 r=1 rank slice of 8")
     ap.add_argument("--shape", default="", help="one shape n1,n2,hq,hkv")
+    ap.add_argument("--layers", type=int, default=32,
+                    help="layers (32 = each layer's K/V cold in L2 as in the pipeline; 4 leaves some of it warm: +5-8%%)")
     ap.add_argument("--bg", default="", choices=["", "gather", "ce"],
                     help="background host->HBM traffic during the timed region (interference experiment)")
     args = ap.parse_args()
@@ -106,4 +108,4 @@ if __name__ == "__main__":
     if args.shape:
         shapes = [tuple(int(x) for x in args.shape.split(","))]
     for n1, n2, hq, hkv in shapes:
-        print(json.dumps(run(n1, n2, hq, hkv, iters=args.iters, bg=args.bg)), flush=True)
+        print(json.dumps(run(n1, n2, hq, hkv, L=args.layers, iters=args.iters, bg=args.bg)), flush=True)
