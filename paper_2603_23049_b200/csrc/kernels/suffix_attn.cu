@@ -1002,7 +1002,14 @@ __global__ void __maxnreg__(136)
           for (int hf = 0; hf < Lay::kHalves; ++hf) tma_store_3d(&tmap_out, stage + hf * Lay::kQHalf, hf * 64, g * G, tok0);
         }
         bulk_commit();
-        bulk_wait0();   // complete before the CTA's shared memory is released
+#ifndef PCR_EPI_WAIT_READ
+#define PCR_EPI_WAIT_READ 1
+#endif
+        // the staging must have been read before the CTA's shared memory is released; the global
+        // writes complete with the grid (the kernel boundary -- or the dependent's
+        // griddepcontrol.wait -- orders them before any reader)
+        if (PCR_EPI_WAIT_READ) bulk_wait_read<0>();
+        else bulk_wait0();
       }
     } else if (p.n_splits == 1 && p.part_o == nullptr) {
       uint4* dst = reinterpret_cast<uint4*>(p.out + row_id * D);
