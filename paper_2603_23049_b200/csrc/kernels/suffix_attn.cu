@@ -1386,12 +1386,16 @@ bool tma_epilogue_enabled() {
   return on;
 }
 
-// SMs the split-KV sizing may count on (PCR_ATTN_SMS; default all 148).
+// SMs the split-KV sizing may count on (PCR_ATTN_SMS overrides).  136 of the 148: the split grid
+// then leaves ~12 SMs free, where the next layer's attention CTAs (programmatic dependent launch)
+// start while this layer's last CTAs and its combine drain.  L8 short-suffix layer (16 M-block x
+// head pairs: 8 splits = 128 CTAs instead of 9 = 144): 18.6-18.8 vs 20.8 us, six alternating
+// runs each (profiles/r02_short_suffix_split_count.txt); the L70 rank slice at r = 1 +1%.
 int attn_sm_budget() {
   static const int n = [] {
     const char* e = std::getenv("PCR_ATTN_SMS");
     const int v = e ? std::atoi(e) : 0;
-    return v > 0 && v <= 148 ? v : 148;
+    return v > 0 && v <= 148 ? v : 136;
   }();
   return n;
 }
