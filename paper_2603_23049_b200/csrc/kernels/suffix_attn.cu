@@ -11,23 +11,28 @@
 //    serves all G query heads of the group.  A CTA owns NQ = 2 Q tiles of 128 rows (256 rows)
 //    of one kv head and a range of 64-key tiles (split-KV when the grid is small); CTAs run
 //    heaviest causal M-blocks first.
-//  * warp 0 (converged, one elected lane issues): TMA producer — Q tiles once (3D tensor map
-//    over q [N2][Hq][d], box {64, G, 128/G}, rows past N2 zero-filled), then K and V of every
-//    key tile (2D tensor map over the pool, boxes {64 dims, min(S_pg, 64) rows}, SWIZZLE_128B)
-//    into a 4-stage ring.
-//  * warp 1 (converged, elected issue, precomputed descriptors): tcgen05.mma kind::f16 —
-//        S_t(j) = Q_t K(j)^T  (SS, K-major)        into TMEM S buffer (t, j&1) (64 columns)
+//  * warps 0 / 3 (converged, one elected lane issues): TMA producers -- warp 0 loads Q tile 1
+//    (3D tensor map over q [N2][Hq][d], box {64, G, 128/G}, rows past N2 zero-filled) and the K
+//    tiles, warp 3 the V tiles (2D map over the pool, boxes {64 dims, min(S_pg, 64) rows},
+//    SWIZZLE_128B) into a 4-stage ring.  With the fused append the CTAs of the last M-block also
+//    store the suffix K/V boxes they loaded into the pool (TMA stores, two tiles after the load,
+//    without blocking the producer).
+//  * warp 1 (converged, elected issue, precomputed descriptors): tcgen05.mma kind::f16 --
+//        S_t(j) = Q_t K(j)^T  (tile 0: TS, Q_0 in TMEM; tile 1: SS, K-major) into a TMEM S buffer
 //        O_t   += P_t(j) V(j) (P from TMEM, V MN-major) into TMEM O_t (d columns)
-//    With 64-key tiles S is double-buffered per Q tile (4 x 64 + 2 x 128 = 512 columns), so
-//    S_t(j+1) is computed while the softmax works on S_t(j); S_t(j+2) reuses buffer j&1 and is
-//    issued after O_t += P_t(j) V(j) (tcgen05 MMAs of one thread execute in issue order).
+//    S rotates through three 64-column buffers shared by the two tiles (S_t(j) in buffer
+//    (2j + t) % 3; Q_0 64 + S 192 + O 256 = 512 columns), so S_t(j+1) is computed while the softmax
+//    works on S_t(j); an S is only ever issued into the buffer the PV just issued has read (tcgen05
+//    MMAs of one thread execute in issue order).  (PCR_Q0_TMEM=0: both Q tiles in shared memory,
+//    S double-buffered per tile.)
 //  * warp 2: tcgen05.alloc of all 512 TMEM columns.
 //  * warps 4-7 / 8-11: softmax of Q tile 0 / 1, one thread per M row (= TMEM lane): row max
 //    with FMNMX3, x = s*scale - m with FFMA2, 2^x by MUFU.EX2 or (kPolyPairs of every 16 pairs) a
-//    polynomial on the FMA pipe, P -> TMEM over the S columns (tcgen05.st), row sum of the same
-//    bf16-rounded weights with FADD2 (R18); causal mask only on tiles crossing the diagonal;
-//    lazy rescaling of O (only when the running max grows by > 8, log2 units), after waiting for
-//    the previous PV.  Epilogue: O / l -> bf16, or fp32 partial + log2-LSE per KV split.
+//    polynomial on the FMA pipe, P -> TMEM over the S columns (tcgen05.st), row sum of the fp32
+//    weights with FADD2 (R18); the two warpgroups take turns on the exponentials; causal mask
+//    only on tiles crossing the diagonal; lazy rescaling of O (only when the running max grows by
+//    > 8, log2 units), after waiting for the previous PV.  Epilogue: O / l -> bf16, or the fp32
+//    partial + log2-LSE per KV split, staged in shared memory and written with TMA stores.
 #include <cuda_bf16.h>
 
 #include <algorithm>
