@@ -311,16 +311,39 @@ def _hugepage_pinned(torch, nbytes, flags=0):
     memory as the library's store (2 MiB pages: few IOMMU / GPU TLB translations per transfer).
     flags 3 = cudaHostRegisterMapped | Portable (device-readable, as host_io's gather reads it)."""
     import mmap
-    m = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    huge = 2 << 20
+    m = mmap.mmap(-1, nbytes + huge, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    base = np.frombuffer(m, dtype=np.uint8)
+    off = (-base.ctypes.data) % huge          # a 2 MiB-aligned start: every 2 MiB range can be huge
     try:
-        m.madvise(mmap.MADV_HUGEPAGE)
+        m.madvise(mmap.MADV_HUGEPAGE, off, nbytes)
     except Exception:
         pass
-    a = np.frombuffer(m, dtype=np.uint8)
+    a = base[off:off + nbytes]
     a[:] = 1
     t = torch.from_numpy(a)
     rc = torch._C._cudart.cudaHostRegister(t.data_ptr(), nbytes, flags)
     return (t, m) if int(rc) == 0 else (None, m)
+
+
+def _anon_huge_frac(addrs):
+    """Fraction of the given mappings' resident bytes on transparent huge pages (/proc/self/smaps):
+    a diagnostic for the e2e host buffers (4 KiB pages read markedly slower from the GPU)."""
+    try:
+        size = huge = 0
+        cur = None
+        for line in open("/proc/self/smaps"):
+            f = line.split()
+            if "-" in f[0] and len(f) > 4 and ":" not in f[0]:
+                lo, hi = (int(x, 16) for x in f[0].split("-"))
+                cur = any(lo <= a < hi for a in addrs)
+            elif cur and f[0] == "Rss:":
+                size += int(f[1])
+            elif cur and f[0] == "AnonHugePages:":
+                huge += int(f[1])
+        return huge / size if size else None
+    except Exception:
+        return None
 
 
 def _host_buffer(torch, arr_or_shape, keep):
@@ -705,11 +728,13 @@ def measure(args, torch, dist, world, rank, local):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_ms = float(tt.item())
         h2d_b, d2h_b = int(q_p.nbytes + k_p.nbytes + v_p.nbytes), int(o_p.nbytes)
+        huge_frac = _anon_huge_frac([t_.data_ptr() for t_, _ in host_keep])
         del q_p, k_p, v_p, o_p
         for t_, _ in host_keep:
             torch._C._cudart.cudaHostUnregister(t_.data_ptr())
         e2e = {"value": n_e2e * N / (e2e_ms * 1e-3), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "steps": n_e2e,
+               "host_hugepage_frac": huge_frac,
                "path": "pcr_run_prefill_ex(host_io=1): each layer's q/k/v read by its gather launch from "
                        "page-locked (hugepage-registered) host buffers, its output returned by one cudaMemcpyAsync "
                        "on the library's D2H stream" if host_io
