@@ -396,10 +396,17 @@ __global__ void __maxnreg__(136)
       tma_prefetch_desc(&tmap_vn);
     }
   }
-  // fused append: the CTAs of the last M-block (they see every key) write the suffix K/V tiles of
-  // their key range into the pool; every other CTA only reads them (from k_new/v_new)
+  // fused append: the CTAs of the last M-block (they see every key) write every suffix K/V box of
+  // their key range into the pool; every other read of the suffix keys comes from k_new/v_new.
+  // Experiment (PCR_APPEND_OWNER=1): each box is written by the CTA whose own query tokens contain
+  // its first key (about one tile per CTA, on its causal diagonal) -- measured 5% slower on the
+  // long shapes: every CTA's epilogue then waits for its own tail stores
+  // (profiles/r02_append_owner.txt).
+#ifndef PCR_APPEND_OWNER
+#define PCR_APPEND_OWNER 0
+#endif
   const bool fold = p.k_new != nullptr;
-  const bool writer = fold && blockIdx.x / p.hkv == 0;
+  const bool writer = fold && (PCR_APPEND_OWNER || blockIdx.x / p.hkv == 0);
   if (warp == 2) tmem_alloc<kTmemCols>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
@@ -477,7 +484,22 @@ __global__ void __maxnreg__(136)
         }
         row = __shfl_sync(0xffffffffu, pg_row, pidx - pg_base) + (in_req ? key & (p.S - 1) : 0);
         sfx = fold && key >= p.n1;
-        dst = sfx && in_req;
+        // dst: this CTA stores the box (a suffix box of a request page it owns)
+        dst = sfx && in_req && (!PCR_APPEND_OWNER || (key - p.n1 >= i0 && key - p.n1 < i_end));
+      };
+      // whether tile `tile` holds a box this CTA stores (fused append)
+      auto tile_stores = [&](int tile) {
+        bool any = false;
+#pragma unroll
+        for (int b = 0; b < kMaxBox; ++b) {
+          if (b < n_box) {
+            int row;
+            bool sfx, dst;
+            box_rows(tile, b, row, sfx, dst);
+            any |= dst;
+          }
+        }
+        return any;
       };
       // fused append: write the suffix boxes of tile `tile` (its K or V stage) into the pool
       auto store_tile = [&](int tile, bool v) {
@@ -536,11 +558,12 @@ __global__ void __maxnreg__(136)
         __syncwarp();
       };
       // K(j) and V(j) go into stage j % kStages once their previous occupants are consumed: K after
-      // the last QK^T that read it (k_empty), V after the last PV (v_empty).  A writer CTA (fused
-      // append) stores the suffix boxes of tile j into the pool from the stage it landed in, issued
-      // kStoreLag tiles later (j has landed by then: its wait is short) and without waiting for the
-      // store: one bulk group per tile, so before tile j + kStages refills the stage only the
-      // kStages - kStoreLag - 1 latest groups may still be reading (4 stages: wait_group.read 1).
+      // the last QK^T that read it (k_empty), V after the last PV (v_empty).  A tile holding boxes
+      // this CTA stores (fused append) is written into the pool from the stage it landed in,
+      // kStoreLag tiles later (it has landed by then: the wait is short) and without waiting for
+      // the store; before such a stage is refilled the producer waits until its stores have read
+      // it (wait_group.read 0: a CTA stores one or two tiles, or -- PCR_APPEND_OWNER=0, last
+      // M-block -- every suffix tile).
 #if PCR_ATTN_TIMING
       long long pw_ = 0, pl_ = 0, pc_ = clock64();
 #define PCR_PTICK(acc) do { const long long n_ = clock64(); acc += n_ - pc_; pc_ = n_; } while (0)
@@ -549,21 +572,26 @@ __global__ void __maxnreg__(136)
 #endif
       constexpr int kStoreLag = kStages > 2 ? 2 : 1;
       static_assert(kStoreLag < kStages, "a tile is stored before its stage is refilled");
+      uint32_t stored[2] = {0u, 0u};   // per K / V: stages whose tile has pool stores in flight
+      bool any_store = false;
       auto produce = [&](int it, bool v) {
         const int st = it % kStages;
         if (it >= kStages) {
           mbar_wait(v ? &bars->v_empty[st] : &bars->k_empty[st], ((it / kStages) - 1) & 1);
           PCR_PTICK(pw_);
-          if (writer) {
-            if (lane == 0) bulk_wait_read<kStages - kStoreLag - 1>();
+          if (writer && ((stored[v] >> st) & 1u)) {
+            if (lane == 0) bulk_wait_read<0>();
             __syncwarp();
+            stored[v] &= ~(1u << st);
           }
         }
         load_tile(it, v);
-        if (writer && it >= kStoreLag) {
+        if (writer && it >= kStoreLag && tile_stores(it - kStoreLag)) {
           const int js = it - kStoreLag;
           mbar_wait(v ? &bars->v_full[js % kStages] : &bars->k_full[js % kStages], (js / kStages) & 1);
           store_tile(js, v);
+          stored[v] |= 1u << (js % kStages);
+          any_store = true;
         }
         PCR_PTICK(pl_);
       };
@@ -579,6 +607,7 @@ __global__ void __maxnreg__(136)
       if (writer) {
         // the last kStoreLag tiles: store once they have landed, then wait for every pool write
         for (int js = max(0, n_iter - kStoreLag); js < n_iter; ++js) {
+          if (!tile_stores(js)) continue;
           if (do_k) {
             mbar_wait(&bars->k_full[js % kStages], (js / kStages) & 1);
             store_tile(js, false);
@@ -587,8 +616,9 @@ __global__ void __maxnreg__(136)
             mbar_wait(&bars->v_full[js % kStages], (js / kStages) & 1);
             store_tile(js, true);
           }
+          any_store = true;
         }
-        if (lane == 0) bulk_wait0();   // the pool writes are complete (visible after the grid)
+        if (any_store && lane == 0) bulk_wait0();   // the pool writes are complete (visible after the grid)
         __syncwarp();
       }
     }
