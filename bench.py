@@ -525,8 +525,10 @@ def measure(args, torch, dist, world, rank, local):
         cs.wait_stream(ls)
         return None
 
-    def step(q, k, v, out, times=False, load_events=None, step_mode=None):
-        """One request.  The caller's stream sync precedes pcr_release (pages are reused)."""
+    def step(q, k, v, out, times=False, load_events=None, step_mode=None, dev_events=None):
+        """One request.  The caller's stream sync precedes pcr_release (pages are reused).
+        dev_events: two events recorded on the compute stream just before the pipeline is enqueued
+        and right after it (SURVEY 8(d) TTFT: the device pipeline, host planning reported apart)."""
         rid = req_counter[0]
         req_counter[0] += 1
         t0 = time.perf_counter()
@@ -534,6 +536,8 @@ def measure(args, torch, dist, world, rank, local):
         plan = ctx.match_prefix(rid, [])
         match_us.append((time.perf_counter() - t0) * 1e6)
         assert plan["n1"] == N1, plan["n1"]
+        if dev_events:
+            dev_events[0].record(cs)
         if load_events:
             load_events[0].record(ls)
         if body is not None:
@@ -554,6 +558,8 @@ def measure(args, torch, dist, world, rank, local):
                     dist.all_gather_into_tensor(gathered.view(-1), out.view(-1))
         if load_events:
             load_events[1].record(ls)
+        if dev_events:
+            dev_events[1].record(cs)
         cs.synchronize()
         # The step is the hot path without the f1 offload (it would change the hit ratio from one
         # step to the next): newly reserved chunks are dropped, the cached prefix stays resident.
@@ -582,17 +588,19 @@ def measure(args, torch, dist, world, rank, local):
     clocks.begin()
     ev0.record(cs)
     ls.wait_event(ev0)
-    step_ms, load_ms = [], []
+    step_ms, load_ms, dev_ms = [], [], []
     for _ in range(args.steps):
         e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l_a, l_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d_a, d_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e_a.record(cs)
         ls.wait_event(e_a)
-        step(q_d, k_d, v_d, out_d, load_events=(l_a, l_b))
+        step(q_d, k_d, v_d, out_d, load_events=(l_a, l_b), dev_events=(d_a, d_b))
         e_b.record(cs)
         e_b.synchronize()
         step_ms.append(e_a.elapsed_time(e_b))
         load_ms.append(l_a.elapsed_time(l_b))
+        dev_ms.append(d_a.elapsed_time(d_b))
     ev1.record(cs)
     torch.cuda.synchronize()
     total_ms = ev0.elapsed_time(ev1)
@@ -864,6 +872,12 @@ def measure(args, torch, dist, world, rank, local):
                     "OVERLAP's; exposed = OVERLAP - sum of SYNC-isolated append+attention; contention = "
                     "append+attention time beside the loads / SYNC-isolated"},
         "ttft_ms": statistics.median(step_ms), "ttft_ms_p90": float(np.percentile(step_ms, 90)),
+        "ttft_device_ms": statistics.median(dev_ms), "ttft_device_ms_p90": float(np.percentile(dev_ms, 90)),
+        "ttft_note": "ttft_ms = the whole step on the device clock: host pcr_submit + pcr_match_prefix "
+                     "(match_prefix_us), the pipeline, the host's stream sync and pcr_release; ttft_device_ms "
+                     "= SURVEY 8(d)'s TTFT: from just before the pipeline is enqueued to the end of the last "
+                     "layer's attention (incl. the re-assembly at P > 1)",
+        "ttft_device_over_t_star": statistics.median(dev_ms) / t_star if t_star else None,
         "ttft_pred_ms": ttft_pred, "sync_bound_ms": L * (gather_ms + attn_ms) if attn_tflops else None,
         "gather_ms_per_layer": gather_ms,
         "gather_ms_per_layer_evented": gather_ms_evented if attn_tflops else None,
@@ -893,7 +907,7 @@ def north_star_point(m7):
     the SM gather sharing the GPU with the attention (OVERLAP)."""
     rg, ra = m7["roofline_gather"], m7["roofline_attn"]
     ov = m7.get("overlap") or {}
-    return {"workload": m7["config"]["workload"], "ttft_ms": m7["ttft_ms"],
+    return {"workload": m7["config"]["workload"], "ttft_ms": m7["ttft_ms"], "ttft_device_ms": m7.get("ttft_device_ms"),
             "load_gbs": rg["achieved"], "load_frac_of_h2d_peak": rg["frac"], "h2d_peak_gbs": rg["peak"],
             "attn_tflops_in_pipeline": ra["achieved"] if ra else None,
             "attn_frac_of_bf16_peak": ra["frac"] if ra else None, "bf16_peak_tflops": ra["peak"] if ra else None,
