@@ -788,3 +788,52 @@ def test_streamed_pipeline_with_default_priority_streams_never_starves_the_gathe
     ctx.close()
     for x in outs:
         assert np.array_equal(x, to_host(o))
+
+
+_EPILOGUE_SCRIPT = r"""
+import hashlib, sys
+import numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_2603_23049_b200 import Context
+from pcrgen import make_rng, randn_bf16
+h = hashlib.sha256()
+for (n1, n2, hq, hkv) in ((1024, 128, 32, 8), (512, 700, 32, 8), (256, 300, 8, 1)):
+    L, d, C, S = 2, 128, 256, 64
+    rng = make_rng(n1 + n2)
+    pool = torch.zeros((2 * (-(-(n1 + n2) // S)) + 4) * L * hkv * 2 * S * d, dtype=torch.int16, device="cuda")
+    ctx = Context(L, hq, hkv, d, C, S, n1 // C + 2, 0, device=0, pool=pool)
+    doc = rng.integers(0, 1000, n1, dtype=np.uint32)
+    ctx.submit(0, np.concatenate([doc, [1]]).astype(np.uint32))
+    for s in ctx.match_prefix(0, [])["slots"]:
+        ctx.store_write(s, randn_bf16(rng, (ctx.slot_bytes // 2,)))
+    ctx.release(0, True)
+    ctx.submit(1, np.concatenate([doc, rng.integers(0, 1000, n2, dtype=np.uint32)]), n_cacheable=n1)
+    ctx.match_prefix(1, [])
+    q, k, v = (torch.from_numpy(randn_bf16(rng, (L, n2, x, d)).view(np.int16)).cuda() for x in (hq, hkv, hkv))
+    o = torch.empty_like(q)
+    cs, ls = torch.cuda.Stream(), torch.cuda.Stream()
+    ctx.run_prefill(1, q, k, v, o, cs, ls)
+    cs.synchronize()
+    h.update(o.cpu().numpy().tobytes())
+    h.update(pool.cpu().numpy().tobytes())
+    ctx.release(1, False)
+    ctx.close()
+print(h.hexdigest())
+"""
+
+
+def test_tma_store_epilogue_is_bitwise_identical_to_row_stores():
+    """The TMA-store epilogue (bf16 out, and the fp32 split-KV partials a short suffix produces)
+    writes exactly the bytes the per-thread row stores write (PCR_TMA_EPILOGUE=0), pool included."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = _EPILOGUE_SCRIPT.format(root=root)
+    digests = []
+    for flag in ("1", "0"):
+        env = dict(os.environ, PCR_TMA_EPILOGUE=flag)
+        res = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, env=env, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        digests.append(res.stdout.strip().splitlines()[-1])
+    assert digests[0] == digests[1]
