@@ -505,7 +505,6 @@ __global__ void __maxnreg__(136)
       auto store_tile = [&](int tile, bool v) {
         const int st = tile % kStages;
         const uint8_t* base = smem + (v ? Lay::kV0 : Lay::kK0) + st * Lay::kKVTile;
-        bool any = false;
 #pragma unroll
         for (int b = 0; b < kMaxBox; ++b) {
           if (b < n_box) {
@@ -517,11 +516,9 @@ __global__ void __maxnreg__(136)
               for (int hf = 0; hf < Lay::kHalves; ++hf)
                 tma_store_2d(&tmap_pool, base + hf * Lay::kKVHalf + b * box * 128, hf * 64, row + (v ? p.S : 0));
             }
-            any |= dst;
           }
         }
-        (void)any;
-        if (lane == 0) bulk_commit();   // one bulk group per stored tile (empty when no box is suffix)
+        if (lane == 0) bulk_commit();   // one bulk group per stored tile
         __syncwarp();
       };
       // load the K (or V) tile `it` into stage it % kStages (boxes from the pool, or -- suffix keys,
