@@ -661,7 +661,7 @@ def measure(args, torch, dist, world, rank, local):
         # the pipeline), nothing beside it -- the SYNC figures above also carry each launch's wait
         # for the gather before it
         attn_ms_b2b = float("nan")
-        if world == 1 and part_d is None and os_ is None:
+        if part_d is None and os_ is None and not ctx_split:   # (each rank alone at P > 1: no collective)
             rid = req_counter[0]
             req_counter[0] += 1
             ctx.submit(rid, toks, n_cacheable=n_doc)
@@ -789,7 +789,10 @@ def measure(args, torch, dist, world, rank, local):
     if rank != 0:
         ctx.close()
         return None
-    dominant = "kv_gather" if N1 and (attn_ms != attn_ms or gather_ms >= attn_ms) else "suffix_attn"
+    # the dominant kernel by its own speed: in a load-bound pipeline the attention's in-pipeline time
+    # includes its wait for the load (~ the load's pace), so it cannot decide
+    attn_own = next((x for x in (attn_ms_b2b, attn_ms_iso, attn_ms) if x == x), float("nan"))
+    dominant = "kv_gather" if N1 and (attn_own != attn_own or gather_ms >= attn_own) else "suffix_attn"
     # per-launch traffic of the dominant kernels from the committed ncu capture (profiles/)
     try:
         ncu_t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
