@@ -105,6 +105,9 @@ struct AttnParams {
   // partial) in shared memory and writes it with TMA stores (coalesced, rows past N2 clipped)
   // instead of one row per thread from registers.
   int32_t tma_epilogue;
+  // Set by the launcher: fused-append placement (0: the last M-block's CTAs store every suffix box
+  // of their range; 1: each suffix box is stored by the CTA whose query tokens contain it).
+  int32_t append_owner;
 };
 
 // Merge n_parts partials (O normalised per part, log2-domain LSE; part s at o + s*o_stride and

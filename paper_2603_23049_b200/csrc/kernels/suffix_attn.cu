@@ -14,9 +14,9 @@
 //  * warps 0 / 3 (converged, one elected lane issues): TMA producers -- warp 0 loads Q tile 1
 //    (3D tensor map over q [N2][Hq][d], box {64, G, 128/G}, rows past N2 zero-filled) and the K
 //    tiles, warp 3 the V tiles (2D map over the pool, boxes {64 dims, min(S_pg, 64) rows},
-//    SWIZZLE_128B) into a 4-stage ring.  With the fused append the CTAs of the last M-block also
-//    store the suffix K/V boxes they loaded into the pool (TMA stores, two tiles after the load,
-//    without blocking the producer).
+//    SWIZZLE_128B) into a 4-stage ring.  With the fused append the CTAs of the last M-block (or,
+//    in a split-KV grid with a long suffix, each box's owning CTA) also store the suffix K/V boxes
+//    they loaded into the pool (TMA stores, two tiles after the load, not blocking the producer).
 //  * warp 1 (converged, elected issue, precomputed descriptors): tcgen05.mma kind::f16 --
 //        S_t(j) = Q_t K(j)^T  (tile 0: TS, Q_0 in TMEM; tile 1: SS, K-major) into a TMEM S buffer
 //        O_t   += P_t(j) V(j) (P from TMEM, V MN-major) into TMEM O_t (d columns)
@@ -396,17 +396,17 @@ __global__ void __maxnreg__(136)
       tma_prefetch_desc(&tmap_vn);
     }
   }
-  // fused append: the CTAs of the last M-block (they see every key) write every suffix K/V box of
-  // their key range into the pool; every other read of the suffix keys comes from k_new/v_new.
-  // Experiment (PCR_APPEND_OWNER=1): each box is written by the CTA whose own query tokens contain
-  // its first key (about one tile per CTA, on its causal diagonal) -- measured 5% slower on the
-  // long shapes: every CTA's epilogue then waits for its own tail stores
-  // (profiles/r02_append_owner.txt).
-#ifndef PCR_APPEND_OWNER
-#define PCR_APPEND_OWNER 0
-#endif
+  // fused append (every other read of the suffix keys comes from k_new/v_new), two placements
+  // chosen by the launcher (p.append_owner):
+  //  * 0: the CTAs of the last M-block (they see every key) write every suffix K/V box of their key
+  //    range -- best when the grid runs in several waves, which absorb those CTAs' extra work;
+  //  * 1: each box is written by the CTA whose own query tokens contain its first key (about one
+  //    tile per CTA, on its causal diagonal) -- best for a split-KV grid with a long suffix, where
+  //    the last M-block's CTAs would be the critical path (M7 r=0.5 on one kv head: 102 -> 71 us
+  //    per layer; 4-6% slower on the multi-wave shapes, profiles/r02_append_owner.txt).
   const bool fold = p.k_new != nullptr;
-  const bool writer = fold && (PCR_APPEND_OWNER || blockIdx.x / p.hkv == 0);
+  const bool owner_mode = p.append_owner != 0;
+  const bool writer = fold && (owner_mode || blockIdx.x / p.hkv == 0);
   if (warp == 2) tmem_alloc<kTmemCols>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
@@ -485,7 +485,7 @@ __global__ void __maxnreg__(136)
         row = __shfl_sync(0xffffffffu, pg_row, pidx - pg_base) + (in_req ? key & (p.S - 1) : 0);
         sfx = fold && key >= p.n1;
         // dst: this CTA stores the box (a suffix box of a request page it owns)
-        dst = sfx && in_req && (!PCR_APPEND_OWNER || (key - p.n1 >= i0 && key - p.n1 < i_end));
+        dst = sfx && in_req && (!owner_mode || (key - p.n1 >= i0 && key - p.n1 < i_end));
       };
       // whether tile `tile` holds a box this CTA stores (fused append)
       auto tile_stores = [&](int tile) {
@@ -559,7 +559,7 @@ __global__ void __maxnreg__(136)
       // this CTA stores (fused append) is written into the pool from the stage it landed in,
       // kStoreLag tiles later (it has landed by then: the wait is short) and without waiting for
       // the store; before such a stage is refilled the producer waits until its stores have read
-      // it (wait_group.read 0: a CTA stores one or two tiles, or -- PCR_APPEND_OWNER=0, last
+      // it (wait_group.read 0: a CTA stores one or two tiles, or -- append_owner = 0, last
       // M-block -- every suffix tile).
 #if PCR_ATTN_TIMING
       long long pw_ = 0, pl_ = 0, pc_ = clock64();
@@ -615,7 +615,9 @@ __global__ void __maxnreg__(136)
           }
           any_store = true;
         }
-        if (any_store && lane == 0) bulk_wait0();   // the pool writes are complete (visible after the grid)
+        // the stores have read the ring (the epilogue may stage over it); their global writes
+        // complete with the grid, like the epilogue's own TMA stores
+        if (any_store && lane == 0) bulk_wait_read<0>();
         __syncwarp();
       }
     }
@@ -1533,6 +1535,19 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
   if (p.part_o && splits == 1) {   // one split: the kernel writes the partial itself
     p.ws_o = p.part_o;
     p.ws_lse = p.part_lse;
+  }
+  // fused-append placement (see the kernel): the owning CTAs when the grid is split-KV and the
+  // suffix spans more than 4 key tiles -- the combine waits for every split, so the last M-block's
+  // CTAs (storing every suffix tile) are then the layer's critical path; without splits the next
+  // layer's CTAs absorb their extra time (M7 r=0.5 per-rank slices, same box: P = 8, 2 splits:
+  // 3.71 -> 2.53 ms with the owners; P = 4, no split: 2.97-2.99 vs 3.07 with the owners).
+  // PCR_APPEND_OWNER=0 / 1 forces either placement.
+  {
+    static const int force = [] {
+      const char* e = std::getenv("PCR_APPEND_OWNER");
+      return e ? std::atoi(e) : -1;
+    }();
+    p.append_owner = force >= 0 ? (force ? 1 : 0) : (splits > 1 && p.n2 > 4 * kBlockN ? 1 : 0);
   }
   // TMA-store epilogue (PCR_TMA_EPILOGUE=0: one row per thread from registers): bf16 out as a 3D
   // map like q's, or the fp32 partial [splits][N2][Hq][D] as a 4D map with 32-float (128-byte) boxes

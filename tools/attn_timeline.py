@@ -54,6 +54,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shape", default="4096,4224,32,8")
     ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--dump", default="", help="save the raw timelines (npz) to this path")
     args = ap.parse_args()
     n1, n2, hq, hkv = (int(x) for x in args.shape.split(","))
     d, C, S, L = 128, 256, 64, args.layers
@@ -91,7 +92,8 @@ def main():
     b.record(cs)
     torch.cuda.synchronize()
     print(json.dumps({"pipeline_ttft_ms": a.elapsed_time(b)}))
-    summarise(read_tl(lib), L, "pipeline (streamed OVERLAP)")
+    tl_pipe = read_tl(lib)
+    summarise(tl_pipe, L, "pipeline (streamed OVERLAP)")
     # the attention alone, back to back (pool already loaded)
     lib.pcr_debug_attn_timeline_clear()
     a.record(cs)
@@ -100,7 +102,10 @@ def main():
     b.record(cs)
     torch.cuda.synchronize()
     print(json.dumps({"attention_only_ms": a.elapsed_time(b)}))
-    summarise(read_tl(lib), L, "attention only")
+    tl_alone = read_tl(lib)
+    summarise(tl_alone, L, "attention only")
+    if args.dump:
+        np.savez_compressed(args.dump, pipeline=tl_pipe[:L], alone=tl_alone[:L])
     ctx.release(1, False)
     ctx.close()
 
