@@ -617,7 +617,13 @@ __global__ void __maxnreg__(136)
         }
         // the stores have read the ring (the epilogue may stage over it); their global writes
         // complete with the grid, like the epilogue's own TMA stores
-        if (any_store && lane == 0) bulk_wait_read<0>();
+#ifndef PCR_TAIL_WAIT_FULL
+#define PCR_TAIL_WAIT_FULL 0
+#endif
+        if (any_store && lane == 0) {
+          if (PCR_TAIL_WAIT_FULL) bulk_wait0();
+          else bulk_wait_read<0>();
+        }
         __syncwarp();
       }
     }
@@ -1513,7 +1519,13 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
   const bool cluster_ok = split_cluster_enabled();
   int splits = 1;
   const int sms = attn_sm_budget();
-  if ((p.ws_o || cluster_ok) && ctas < sms) {   // (kv_len < n1 + n2 only shortens the key range: fewer tiles)
+  // Split only small grids (< 48 CTAs): a split-KV layer ends in a combine that waits for every
+  // split, while an unsplit grid of >= ~1/3 of the SMs lets the next layer's CTAs run beside it
+  // (programmatic dependent launch) -- M7 r=0.5 per-rank slice at P = 8 (66 CTAs): 2.53 -> 1.70 ms
+  // TTFT unsplit; 34 and 18 CTAs (r = 0.75 / 0.875) and L8 (16) stay faster split
+  // (profiles/r02_split_threshold.txt).
+  constexpr int kSplitMaxCtas = 48;
+  if ((p.ws_o || cluster_ok) && ctas < std::min(sms, kSplitMaxCtas)) {   // (kv_len < n1 + n2 only shortens the key range)
     splits = std::max(1, sms / ctas);
     splits = std::min(splits, std::max(1, max_tiles / PCR_SPLIT_MIN_TILES));
     if (cluster_ok) {
