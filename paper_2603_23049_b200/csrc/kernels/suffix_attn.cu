@@ -1548,18 +1548,23 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
     p.ws_o = p.part_o;
     p.ws_lse = p.part_lse;
   }
-  // fused-append placement (see the kernel): the owning CTAs when the grid is split-KV and the
-  // suffix spans more than 4 key tiles -- the combine waits for every split, so the last M-block's
-  // CTAs (storing every suffix tile) are then the layer's critical path; without splits the next
-  // layer's CTAs absorb their extra time (M7 r=0.5 per-rank slices, same box: P = 8, 2 splits:
-  // 3.71 -> 2.53 ms with the owners; P = 4, no split: 2.97-2.99 vs 3.07 with the owners).
-  // PCR_APPEND_OWNER=0 / 1 forces either placement.
+  // fused-append placement (see the kernel): the owning CTAs when the whole grid is one wave, the
+  // suffix spans more than 4 key tiles, and either the grid is split-KV (the combine waits for
+  // every split, so the last M-block's CTAs, storing every suffix tile, are the layer's critical
+  // path) or the suffix is >= 70% of the keys (those CTAs store nearly every tile they load);
+  // otherwise the next layer's CTAs absorb their extra time.  Same-box A/B (M7 per-rank slices,
+  // TTFT): P = 8 r = 0.5 (2 splits) 3.71 -> 2.53 ms, r = 0 2.58-2.66 -> 2.08-2.13, r = 0.25
+  // 2.18-2.22 -> 1.97; kept on the last M-block: P = 4 r = 0.5 2.97-2.99 (3.07 with the owners),
+  // P = 4 r = 0 (two waves) 3.85-3.88 (3.97-3.98).  PCR_APPEND_OWNER=0 / 1 forces either placement.
   {
     static const int force = [] {
       const char* e = std::getenv("PCR_APPEND_OWNER");
       return e ? std::atoi(e) : -1;
     }();
-    p.append_owner = force >= 0 ? (force ? 1 : 0) : (splits > 1 && p.n2 > 4 * kBlockN ? 1 : 0);
+    const bool one_wave = int64_t(ctas) * splits <= 148;
+    const bool long_sfx = p.n2 > 4 * kBlockN;
+    const bool heavy = splits > 1 || int64_t(p.n2) * 10 >= int64_t(p.n1 + p.n2) * 7;
+    p.append_owner = force >= 0 ? (force ? 1 : 0) : (one_wave && long_sfx && heavy ? 1 : 0);
   }
   // TMA-store epilogue (PCR_TMA_EPILOGUE=0: one row per thread from registers): bf16 out as a 3D
   // map like q's, or the fp32 partial [splits][N2][Hq][D] as a 4D map with 32-float (128-byte) boxes
