@@ -1524,7 +1524,10 @@ cudaError_t launch_d(const CUtensorMap* tmap_pool, const AttnParams& p0, cudaStr
   // (programmatic dependent launch) -- M7 r=0.5 per-rank slice at P = 8 (66 CTAs): 2.53 -> 1.70 ms
   // TTFT unsplit; 34 and 18 CTAs (r = 0.75 / 0.875) and L8 (16) stay faster split
   // (profiles/r02_split_threshold.txt).
-  constexpr int kSplitMaxCtas = 48;
+#ifndef PCR_SPLIT_MAX_CTAS
+#define PCR_SPLIT_MAX_CTAS 48
+#endif
+  constexpr int kSplitMaxCtas = PCR_SPLIT_MAX_CTAS;
   if ((p.ws_o || cluster_ok) && ctas < std::min(sms, kSplitMaxCtas)) {   // (kv_len < n1 + n2 only shortens the key range)
     splits = std::max(1, sms / ctas);
     splits = std::min(splits, std::max(1, max_tiles / PCR_SPLIT_MIN_TILES));
